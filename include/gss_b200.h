@@ -1,0 +1,230 @@
+/* gss_b200.h — C ABI of the B200-native GS-Scale hot path (libgss_b200.so).
+ *
+ * This is the drop-in boundary for the per-iteration training path of the reference
+ * (/root/reference/proj/include/gss/*.hpp, header-template C++ API). Each entry point names the
+ * reference function it replaces (file:line). Conventions:
+ *   - fp32 data, plain pointers and sizes; no C++ or torch types cross this boundary;
+ *   - device buffers are caller-allocated; every call is enqueued on the given CUDA stream and
+ *     returns immediately (stream-ordered), except where a host-visible result is documented;
+ *   - status codes: GSS_OK 0, GSS_ERR_CUDA 1, GSS_ERR_INVALID 2 (reference: ConfigError /
+ *     std::invalid_argument), GSS_ERR_INVARIANT 3 (reference: InvariantViolation); the message of
+ *     the last failure on the calling thread is returned by gss_last_error();
+ *   - there is no CPU fallback: without a CUDA device every compute entry point fails with
+ *     GSS_ERR_CUDA.
+ */
+#ifndef GSS_B200_H
+#define GSS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* gss_stream_t; /* a cudaStream_t */
+
+enum { GSS_OK = 0, GSS_ERR_CUDA = 1, GSS_ERR_INVALID = 2, GSS_ERR_INVARIANT = 3 };
+
+/* Camera<float> (scene.hpp:77-96): world->camera p_c = rot * p + trans, row-major rot. 80 bytes,
+ * layout-identical to the reference struct. */
+typedef struct {
+  float rot[9];
+  float trans[3];
+  float fx, fy, cx, cy;
+  int32_t width, height;
+  float near_plane, far_plane;
+} gss_camera;
+
+/* Viewport<float> (render.hpp:46-49): closed pixel rectangle; pixel (x, y) has centre (x+.5, y+.5). */
+typedef struct {
+  float x0, x1, y0, y1;
+} gss_viewport;
+
+/* GroupSpec + Hyperparams (adam.hpp:14-34): contiguous columns [col0, col0+dim) with their own lr. */
+typedef struct {
+  int32_t col0, dim;
+  double lr, beta1, beta2, eps;
+} gss_group;
+
+/* Arena<float> (adam.hpp:119-159): row-major w/m/v [n][dim] + uint8 counter[n], all device
+ * pointers (or pinned host pointers where documented). `step` = applied update passes; the
+ * update entry points advance it on the host at enqueue time. */
+typedef struct {
+  float* w;
+  float* m;
+  float* v;
+  uint8_t* counter;
+  int64_t n;
+  int32_t dim;
+  int32_t defer_max;
+  int64_t step;
+  int32_t ngroups;
+  gss_group groups[8];
+} gss_arena;
+
+/* SparseGrads<float> (adam.hpp:163-169): sorted ids; row(k) = rows + k*stride + col0.
+ * count_dev (optional device int64) overrides count so a device-produced length (gss_cull) can
+ * feed the optimizer without a host round trip. */
+typedef struct {
+  const int32_t* ids;
+  int64_t count;
+  const int64_t* count_dev;
+  const float* rows;
+  int64_t stride;
+  int32_t col0;
+} gss_sparse_grads;
+
+/* ---- library ------------------------------------------------------------------------------ */
+const char* gss_last_error(void);
+int32_t gss_abi_version(void);
+/* Number of CUDA devices visible (0 = no GPU; compute calls then fail with GSS_ERR_CUDA). */
+int32_t gss_device_count(void);
+/* Kernels launched by this library since load (process-wide; bench `gpu_launches`). */
+int64_t gss_launch_count(void);
+
+/* glibc-exact expf on the device, for n inputs (parity probe of render.hpp:105). */
+int gss_expf_device(const float* x, float* y, int64_t n, gss_stream_t stream);
+
+/* ---- frustum cull (render.hpp:243-260 cull_keep / frustum_cull) ---------------------------- */
+/* Workspace for n Gaussians (look-back tile states + ticket). */
+size_t gss_cull_workspace_bytes(int64_t n);
+/* ids_out: capacity n, receives the kept ids ascending (bit-exact with frustum_cull);
+ * mask_opt: optional bit mask, ceil(n/32) words, bit i of word i/32 = kept(i);
+ * count_dev: device int64 receiving the kept count. geo rows are read with `stride` floats per
+ * row (10 for the geometric tier, 59 for a dense arena). */
+int gss_cull(const float* geo, int64_t n, int64_t stride, const gss_camera* cam, const gss_viewport* vp,
+             float low_pass, uint32_t* mask_opt, int32_t* ids_out, int64_t* count_dev, void* workspace,
+             size_t workspace_bytes, gss_stream_t stream);
+
+/* ---- optimizer (adam.hpp:67-313) -------------------------------------------------------- */
+/* build_group_luts (adam.hpp:67-97), fp64 on the host, cast to float. Arrays have max_delay+1
+ * entries; scalars[5] = one_minus_b1, one_minus_b2, bias_correction, step_size, eps. */
+int gss_build_group_luts(double lr, double beta1, double beta2, double eps, int64_t t, int32_t max_delay,
+                         float* param, float* mom, float* var, float* pow_b1, float* pow_b2, float* scalars);
+/* adam_step_dense (adam.hpp:198-207): every row at delay 0; grads n*dim (device) or NULL. */
+int gss_adam_step_dense(gss_arena* arena, const float* grads, gss_stream_t stream);
+/* deferred_update (adam.hpp:211-238): touched = has grad or counter == defer_max; touched rows are
+ * restored at their delay and stepped, counters reset, others advance. Optional outputs:
+ * touched_ids (device, capacity n, ascending) and touched_count_dev. Unsorted / out-of-range ids
+ * are detected on the device and reported by gss_arena_check (GSS_ERR_INVARIANT). */
+int gss_deferred_update(gss_arena* arena, const gss_sparse_grads* grads, int32_t* touched_ids,
+                        int64_t* touched_count_dev, gss_stream_t stream);
+/* restore_view (adam.hpp:252-289): out[k] = row ids[k] restored (+ the pending pass when
+ * pending != NULL). ids must be ascending (the reference's merge walk assumes it).
+ * ids_count_dev optionally supplies the id count from the device. Arena state untouched. */
+int gss_restore_view(const gss_arena* arena, const int32_t* ids, int64_t count, const int64_t* ids_count_dev,
+                     const gss_sparse_grads* pending, float* out_rows, gss_stream_t stream);
+/* flush_deferred (adam.hpp:293-313). */
+int gss_flush_deferred(gss_arena* arena, gss_stream_t stream);
+/* Device-side invariant flag of the last deferred_update on this arena's counters:
+ * returns GSS_ERR_INVARIANT if grad ids were unsorted/out of range (adam.hpp:231) or a
+ * counter exceeded defer_max (adam.hpp:154-158). Synchronises the stream. */
+int gss_arena_check(const gss_arena* arena, gss_stream_t stream);
+
+/* ---- rasterizer (render.hpp:361-640) ---------------------------------------------------- */
+/* A render context is the device-side RenderResult (render.hpp:284-289): it owns the splat
+ * records, the tile-binned sorted contribution lists and the per-pixel aux of the last forward,
+ * which rasterize_backward consumes. Memory grows on demand from a stream-ordered pool. */
+typedef struct gss_render_ctx gss_render_ctx;
+gss_render_ctx* gss_render_ctx_create(void);
+void gss_render_ctx_destroy(gss_render_ctx* ctx);
+
+/* RenderScene (render.hpp:70-77). nongeo rows: compact (slot-indexed, row k = nongeo + k*stride)
+ * or by global id; slot_map (optional device) remaps compact slots as NonGeoView does. */
+typedef struct {
+  const int32_t* ids; /* device, ascending */
+  int64_t count;      /* host-known count (see count_dev) */
+  const int64_t* count_dev; /* optional: read the count from the device (one sync) */
+  const float* geo;
+  int64_t geo_stride;
+  const float* nongeo;
+  int64_t nongeo_stride;
+  int32_t nongeo_compact;
+  const int32_t* slot_map;
+  int32_t sh_degree;
+  float background[3];
+  float low_pass;
+} gss_render_scene;
+
+/* rasterize_forward (render.hpp:384-464) fused with compute_loss_l1 (render.hpp:497-511) when
+ * gt != NULL: image (ph*pw*3 device, pixel window of vp) is bit-identical to the reference;
+ * gt is the FULL camera image (height*width*3); d_img (window-sized) and loss_dev (device float)
+ * receive the L1 gradient and loss normalised by `normalizer` (0 = window element count).
+ * final_T_opt / n_contrib_opt: optional per-pixel transmittance and used-contribution counts.
+ * meta_host (optional, host int64[6]): px0, py0, pw, ph, visible count, tile instances
+ * (filling it synchronises the stream). */
+int gss_rasterize_forward(gss_render_ctx* ctx, const gss_render_scene* scene, const gss_camera* cam,
+                          const gss_viewport* vp, float* image, const float* gt, int64_t normalizer, float* d_img,
+                          float* loss_dev, float* final_T_opt, int32_t* n_contrib_opt, int64_t* meta_host,
+                          gss_stream_t stream);
+/* compute_loss_l1 (render.hpp:497-511) on window-sized images; loss in fp64 then cast. */
+int gss_loss_l1(const float* image, const float* gt, int64_t elems, int64_t normalizer, float* d_img,
+                float* loss_dev, gss_stream_t stream);
+/* rasterize_backward (render.hpp:526-640) for the ctx's last forward: d_img (window-sized).
+ * Outputs per visible slot k (zero-filled by this call): grad_geo[k*geo_stride + 0..9],
+ * grad_nongeo[k*ng_stride + 0..48] (use grad_geo = rows, grad_nongeo = rows + 10 and both strides
+ * 59 for the reference GradBuffer layout), mean2d_opt[k*2 + 0..1]. Deterministic (no float
+ * atomics): per-tile fixed-order reductions, then per-Gaussian fixed-order sums. */
+int gss_rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* grad_geo, int64_t geo_stride,
+                           float* grad_nongeo, int64_t ng_stride, float* mean2d_opt, gss_stream_t stream);
+
+/* ---- offload engine (engine.hpp:55-522) ------------------------------------------------- */
+/* OptimConfig (store.hpp:110-145) + EngineConfig (engine.hpp:30-49). */
+typedef struct {
+  double lr_mean, lr_scale, lr_quat, lr_opacity, lr_sh, sh_rest_divisor;
+  double beta1, beta2, eps, scene_extent;
+  int32_t defer_max, geo_defer_max;
+  int32_t pipelined;      /* 0 = run_serial order on one stream, 1 = two-stream DAG (run_pipelined) */
+  int32_t sh_degree, sh_warmup_step;
+  float background[3];
+  float low_pass;
+  int32_t nongeo_on_host; /* 0: non-geometric tier in HBM; 1: pinned host tier (offload) */
+  int64_t chunk_bytes;    /* forwarding chunk (store.hpp:204-213), default 32 MB */
+} gss_engine_config;
+
+typedef struct gss_engine gss_engine;
+void gss_engine_config_default(gss_engine_config* cfg);
+/* init_rows: host n x 59 (scene.hpp:13-31 row layout). cams: host; gts: host ncams*H*W*3 or NULL
+ * (then gss_engine_step must supply the ground truth per step). */
+gss_engine* gss_engine_create(int64_t n, const float* init_rows, int32_t ncams, const gss_camera* cams,
+                              const float* gts, const gss_engine_config* cfg);
+void gss_engine_destroy(gss_engine* e);
+/* OffloadEngine::run (engine.hpp:73-88): n iterations over the stored cameras, drained.
+ * losses / valid_counts (host, n entries) receive IterResult. */
+int gss_engine_run(gss_engine* e, int32_t iters, float* losses, int32_t* valid_counts);
+/* One iteration with a host-supplied camera and ground truth (pinned or pageable host memory;
+ * copied H2D inside the call) returning the loss to the host — the end-to-end entry point. */
+int gss_engine_step(gss_engine* e, const gss_camera* cam, const float* gt_host, float* loss_host,
+                    int32_t* valid_count_host);
+/* Applies the lazy update still owed by an open step() segment (run() always drains itself). */
+int gss_engine_drain(gss_engine* e);
+/* snapshot (engine.hpp:91-111): restored parameters, host n x 59. */
+int gss_engine_snapshot(gss_engine* e, float* rows_out);
+/* Raw tier state (stored, not restored) for parity checks; any pointer may be NULL. */
+int gss_engine_state(gss_engine* e, float* geo_w, float* ng_w, float* ng_m, float* ng_v, uint8_t* ng_counter,
+                     int64_t* steps2);
+/* accum_grad_norm / accum_grad_count (engine.hpp:187-188). */
+int gss_engine_accum(gss_engine* e, double* norm, int32_t* cnt);
+int64_t gss_engine_count(gss_engine* e);
+/* Per-stage device time of the last run in ms (CUDA events): cull, forward_params, render,
+ * geo_update, handoff, lazy_update. */
+int gss_engine_stage_ms(gss_engine* e, double* out6);
+/* Kernel launches issued by the last run/step (for bench accounting). */
+int64_t gss_engine_launches(gss_engine* e);
+
+/* ---- scene inputs (not on the hot path) ---------------------------------------------------- */
+/* synth_scene parameter + camera generation (synth.hpp:100-154), bit-identical to the reference
+ * generator; cfg[14] = box, radius_min, radius_max, fov_deg, fov_ramp, target_jitter, near, far,
+ * scale_min, scale_max, scale_aniso, opacity_min, opacity_max, sh_rest_noise.
+ * rows_out: host n x 59; cams_out: host cams. Ground truth is rendered with gss_rasterize_forward. */
+int gss_synth_scene(uint64_t seed, int64_t n, int32_t cams, int32_t width, int32_t height, int32_t sh_degree,
+                    const double* cfg, float* rows_out, gss_camera* cams_out);
+/* look_at_camera (scene.hpp:99-126). */
+int gss_look_at_camera(const float* eye, const float* target, float fx, float fy, int32_t w, int32_t h,
+                       float near_p, float far_p, gss_camera* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSS_B200_H */

@@ -1,0 +1,226 @@
+// extern "C" entry points of libgss_b200.so (declared in include/gss_b200.h). Each one validates
+// its arguments, maps library exceptions to status codes and records the message for
+// gss_last_error(). No entry point has a CPU fallback.
+#include <atomic>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace gssd {
+// cull.cu
+size_t cull_workspace_bytes(int64_t n);
+void cull(const float* geo, int64_t n, int64_t stride, const gss_camera* cam, const gss_viewport* vp, float lp,
+          uint32_t* mask, int32_t* ids, int64_t* count, void* ws, size_t ws_bytes, cudaStream_t st);
+void expf_device(const float* x, float* y, int64_t n, cudaStream_t st);
+// adam.cu
+void build_group_luts(double lr, double b1, double b2, double eps, int64_t t, int max_delay, float* param,
+                      float* mom, float* var, float* pow_b1, float* pow_b2, float* scalars);
+void adam_update(gss_arena* ap, const gss_sparse_grads* grads, int32_t* touched_ids, int64_t* touched_count,
+                 cudaStream_t st);
+void adam_dense(gss_arena* ap, const float* grads, cudaStream_t st);
+void adam_flush(gss_arena* ap, cudaStream_t st);
+void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const int64_t* count_dev,
+                  const gss_sparse_grads* pending, float* out, cudaStream_t st);
+int arena_check(const gss_arena* ap, cudaStream_t st);
+// raster.cu
+gss_render_ctx* render_ctx_create();
+void render_ctx_destroy(gss_render_ctx* ctx);
+void rasterize_forward(gss_render_ctx* ctx, const gss_render_scene* scene, const gss_camera* cam,
+                       const gss_viewport* vp, float* image, const float* gt, int64_t normalizer, float* d_img,
+                       float* loss_dev, float* final_T_opt, int32_t* ncontrib_opt, int64_t* meta, cudaStream_t st);
+void loss_l1(const float* image, const float* gt, int64_t elems, int64_t normalizer, float* d_img, float* loss_dev,
+             cudaStream_t st);
+void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int64_t gstride, float* gn,
+                        int64_t nstride, float* mean2d, cudaStream_t st);
+// engine.cu
+void engine_config_default(gss_engine_config* c);
+gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss_camera* cams, const float* gts,
+                          const gss_engine_config* cfg);
+void engine_destroy(gss_engine* e);
+void engine_run(gss_engine* e, int iters, float* losses, int32_t* valid);
+void engine_step(gss_engine* e, const gss_camera* cam, const float* gt_host, float* loss_host, int32_t* valid_host);
+void engine_drain(gss_engine* e);
+void engine_snapshot(gss_engine* e, float* rows_out);
+void engine_state(gss_engine* e, float* geo_w, float* ng_w, float* ng_m, float* ng_v, uint8_t* ng_counter,
+                  int64_t* steps2);
+void engine_accum(gss_engine* e, double* norm, int32_t* cnt);
+void engine_stage_ms(gss_engine* e, double* out6);
+int64_t engine_launches(gss_engine* e);
+int64_t engine_count(gss_engine* e);
+
+namespace {
+thread_local std::string t_err;
+std::atomic<int64_t> g_launches{0};
+
+void require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw Error(GSS_ERR_CUDA, "no CUDA device: libgss_b200 has no CPU fallback");
+  }
+}
+}  // namespace
+
+void set_error(const std::string& msg) { t_err = msg; }
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launches() { return g_launches.load(std::memory_order_relaxed); }
+
+}  // namespace gssd
+
+using namespace gssd;
+
+#define GSS_API extern "C" __attribute__((visibility("default")))
+
+GSS_API const char* gss_last_error(void) { return t_err.c_str(); }
+GSS_API int32_t gss_abi_version(void) { return 1; }
+GSS_API int32_t gss_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+GSS_API int64_t gss_launch_count(void) { return launches(); }
+
+GSS_API int gss_expf_device(const float* x, float* y, int64_t n, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    require(n >= 0 && (n == 0 || (x && y)), "expf: bad arguments");
+    expf_device(x, y, n, as_stream(stream));
+  });
+}
+
+GSS_API size_t gss_cull_workspace_bytes(int64_t n) { return cull_workspace_bytes(n); }
+
+GSS_API int gss_cull(const float* geo, int64_t n, int64_t stride, const gss_camera* cam, const gss_viewport* vp,
+                     float low_pass, uint32_t* mask_opt, int32_t* ids_out, int64_t* count_dev, void* workspace,
+                     size_t workspace_bytes, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    cull(geo, n, stride, cam, vp, low_pass, mask_opt, ids_out, count_dev, workspace, workspace_bytes,
+         as_stream(stream));
+  });
+}
+
+GSS_API int gss_build_group_luts(double lr, double beta1, double beta2, double eps, int64_t t, int32_t max_delay,
+                                 float* param, float* mom, float* var, float* pow_b1, float* pow_b2, float* scalars) {
+  return guarded([&] {
+    require(t >= 1, "build_group_luts: t must be >= 1");
+    require(max_delay >= 0 && max_delay <= 254, "build_group_luts: max_delay must be in [0, 254]");
+    require(param && scalars, "build_group_luts: null output");
+    build_group_luts(lr, beta1, beta2, eps, t, max_delay, param, mom, var, pow_b1, pow_b2, scalars);
+  });
+}
+
+GSS_API int gss_adam_step_dense(gss_arena* arena, const float* grads, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    adam_dense(arena, grads, as_stream(stream));
+  });
+}
+
+GSS_API int gss_deferred_update(gss_arena* arena, const gss_sparse_grads* grads, int32_t* touched_ids,
+                                int64_t* touched_count_dev, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    adam_update(arena, grads, touched_ids, touched_count_dev, as_stream(stream));
+  });
+}
+
+GSS_API int gss_restore_view(const gss_arena* arena, const int32_t* ids, int64_t count, const int64_t* ids_count_dev,
+                             const gss_sparse_grads* pending, float* out_rows, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    adam_restore(arena, ids, count, ids_count_dev, pending, out_rows, as_stream(stream));
+  });
+}
+
+GSS_API int gss_flush_deferred(gss_arena* arena, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    adam_flush(arena, as_stream(stream));
+  });
+}
+
+GSS_API int gss_arena_check(const gss_arena* arena, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    arena_check(arena, as_stream(stream));
+  });
+}
+
+GSS_API gss_render_ctx* gss_render_ctx_create(void) {
+  gss_render_ctx* c = nullptr;
+  const int st = guarded([&] { c = render_ctx_create(); });
+  return st == GSS_OK ? c : nullptr;
+}
+GSS_API void gss_render_ctx_destroy(gss_render_ctx* ctx) { render_ctx_destroy(ctx); }
+
+GSS_API int gss_rasterize_forward(gss_render_ctx* ctx, const gss_render_scene* scene, const gss_camera* cam,
+                                  const gss_viewport* vp, float* image, const float* gt, int64_t normalizer,
+                                  float* d_img, float* loss_dev, float* final_T_opt, int32_t* n_contrib_opt,
+                                  int64_t* meta_host, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    rasterize_forward(ctx, scene, cam, vp, image, gt, normalizer, d_img, loss_dev, final_T_opt, n_contrib_opt,
+                      meta_host, as_stream(stream));
+  });
+}
+
+GSS_API int gss_loss_l1(const float* image, const float* gt, int64_t elems, int64_t normalizer, float* d_img,
+                        float* loss_dev, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    loss_l1(image, gt, elems, normalizer, d_img, loss_dev, as_stream(stream));
+  });
+}
+
+GSS_API int gss_rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* grad_geo, int64_t geo_stride,
+                                   float* grad_nongeo, int64_t ng_stride, float* mean2d_opt, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    rasterize_backward(ctx, d_img, grad_geo, geo_stride, grad_nongeo, ng_stride, mean2d_opt, as_stream(stream));
+  });
+}
+
+GSS_API void gss_engine_config_default(gss_engine_config* cfg) {
+  if (cfg) engine_config_default(cfg);
+}
+
+GSS_API gss_engine* gss_engine_create(int64_t n, const float* init_rows, int32_t ncams, const gss_camera* cams,
+                                      const float* gts, const gss_engine_config* cfg) {
+  gss_engine* e = nullptr;
+  const int st = guarded([&] {
+    require_device();
+    e = engine_create(n, init_rows, ncams, cams, gts, cfg);
+  });
+  return st == GSS_OK ? e : nullptr;
+}
+GSS_API void gss_engine_destroy(gss_engine* e) { engine_destroy(e); }
+GSS_API int gss_engine_run(gss_engine* e, int32_t iters, float* losses, int32_t* valid_counts) {
+  return guarded([&] { engine_run(e, iters, losses, valid_counts); });
+}
+GSS_API int gss_engine_step(gss_engine* e, const gss_camera* cam, const float* gt_host, float* loss_host,
+                            int32_t* valid_count_host) {
+  return guarded([&] { engine_step(e, cam, gt_host, loss_host, valid_count_host); });
+}
+GSS_API int gss_engine_drain(gss_engine* e) {
+  return guarded([&] { engine_drain(e); });
+}
+GSS_API int gss_engine_snapshot(gss_engine* e, float* rows_out) {
+  return guarded([&] { engine_snapshot(e, rows_out); });
+}
+GSS_API int gss_engine_state(gss_engine* e, float* geo_w, float* ng_w, float* ng_m, float* ng_v, uint8_t* ng_counter,
+                             int64_t* steps2) {
+  return guarded([&] { engine_state(e, geo_w, ng_w, ng_m, ng_v, ng_counter, steps2); });
+}
+GSS_API int gss_engine_accum(gss_engine* e, double* norm, int32_t* cnt) {
+  return guarded([&] { engine_accum(e, norm, cnt); });
+}
+GSS_API int64_t gss_engine_count(gss_engine* e) { return engine_count(e); }
+GSS_API int gss_engine_stage_ms(gss_engine* e, double* out6) {
+  return guarded([&] { engine_stage_ms(e, out6); });
+}
+GSS_API int64_t gss_engine_launches(gss_engine* e) { return engine_launches(e); }

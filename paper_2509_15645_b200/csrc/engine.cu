@@ -1,0 +1,640 @@
+// OffloadEngine on the B200 (reference: engine.hpp:55-522, store.hpp:149-248).
+//
+// The reference runs six stages on two std::threads (a "device" worker and a "host" worker)
+// synchronised by condition-variable Events; here the two workers are two CUDA streams and the
+// Events are cudaEvents, enqueued by one host thread:
+//   stream D: cull(g) -> render(g) -> geo_update(g) -> handoff(g)
+//   stream H: forward_params(g) -> lazy_update(g-1)
+// with the reference's edges (engine.hpp:477-516): fp(g) waits cull(g) and handoff(g-1);
+// render(g) waits fp(g); lazy(g-1) runs after fp(g) on H, overlapping render(g) on D.
+// Serial mode issues the same stages on one stream in run_serial's order. Every kernel is
+// deterministic, so serial and pipelined trajectories are bitwise identical.
+//
+// Tier placement (selective offloading, store.hpp:149-192): the geometric tier (N x 10 w/m/v,
+// geo_defer_max = 0 => dense immediate update) lives in HBM. The non-geometric tier (N x 49
+// w/m/v + uint8 counters, defer_max) lives in HBM (scene fits: 180 GB) or, with
+// nongeo_on_host, in pinned host memory read by the forwarding gather through the PCIe/C2C
+// mapping and updated lazily in place (zero-copy), see DESIGN.md §offload.
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+#include "gss_math.cuh"
+
+namespace gssd {
+void cull(const float* geo, int64_t n, int64_t stride, const gss_camera* cam, const gss_viewport* vp, float lp,
+          uint32_t* mask, int32_t* ids, int64_t* count, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t cull_workspace_bytes(int64_t n);
+void adam_update(gss_arena* ap, const gss_sparse_grads* grads, int32_t* touched_ids, int64_t* touched_count,
+                 cudaStream_t st);
+void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const int64_t* count_dev,
+                  const gss_sparse_grads* pending, float* out, cudaStream_t st);
+void rasterize_forward(gss_render_ctx* ctx, const gss_render_scene* scene, const gss_camera* cam,
+                       const gss_viewport* vp, float* image, const float* gt, int64_t normalizer, float* d_img,
+                       float* loss_dev, float* final_T_opt, int32_t* ncontrib_opt, int64_t* meta, cudaStream_t st);
+void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int64_t gstride, float* gn,
+                        int64_t nstride, float* mean2d, cudaStream_t st);
+void render_ctx_destroy(gss_render_ctx* ctx);
+gss_render_ctx* render_ctx_create();
+}  // namespace gssd
+
+struct gss_render_ctx;
+
+namespace gssd {
+namespace {
+
+constexpr int kGeoDim = 10, kNgDim = 49, kRowDim = 59;
+
+__global__ void handoff_stats_kernel(const int32_t* ids, const int64_t* count, const float* mean2d, double* norm,
+                                     int32_t* cnt) {
+  const int64_t V = *count;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < V; k += (int64_t)gridDim.x * blockDim.x) {
+    const double gx = (double)mean2d[k * 2], gy = (double)mean2d[k * 2 + 1];
+    const int id = ids[k];
+    norm[id] += sqrt(gx * gx + gy * gy);  // engine.hpp:404-408
+    cnt[id] += 1;
+  }
+}
+
+__global__ void split_rows_kernel(const float* rows, int64_t n, float* geo, float* ng) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n * kRowDim) return;
+  const int64_t r = i / kRowDim;
+  const int c = (int)(i - r * kRowDim);
+  if (c < kGeoDim) geo[r * kGeoDim + c] = rows[i]; else ng[r * kNgDim + (c - kGeoDim)] = rows[i];
+}
+
+__global__ void join_rows_kernel(const float* geo, const float* ng, int64_t n, float* rows) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n * kRowDim) return;
+  const int64_t r = i / kRowDim;
+  const int c = (int)(i - r * kRowDim);
+  rows[i] = c < kGeoDim ? geo[r * kGeoDim + c] : ng[r * kNgDim + (c - kGeoDim)];
+}
+
+__global__ void iota_kernel(int32_t* ids, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) ids[i] = (int32_t)i;
+}
+
+template <class T> T* dmalloc(size_t count) {
+  T* p = nullptr;
+  if (count == 0) count = 1;
+  GSS_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  return p;
+}
+
+struct Ev {
+  cudaEvent_t e = nullptr;
+  Ev() { GSS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+  ~Ev() { if (e) cudaEventDestroy(e); }
+};
+
+enum Stage { kCull = 0, kFwd, kRender, kGeo, kHandoff, kLazy, kStages };
+
+}  // namespace
+}  // namespace gssd
+
+struct gss_engine {
+  gss_engine_config cfg{};
+  int64_t n = 0;
+  std::vector<gss_camera> cams;
+  float* gts_dev = nullptr;  // ncams x H x W x 3 (optional)
+  int W = 0, H = 0;
+  // tiers
+  float *gw = nullptr, *gm = nullptr, *gv = nullptr;
+  uint8_t* gcnt = nullptr;
+  float *nw = nullptr, *nm = nullptr, *nv = nullptr;
+  uint8_t* ncnt = nullptr;
+  bool ng_host = false;
+  gss_arena geo{}, ng{};
+  // plans: ring of 3 (engine.hpp:195-203)
+  int32_t* ids[3] = {nullptr, nullptr, nullptr};
+  int64_t* count[3] = {nullptr, nullptr, nullptr};
+  int64_t* count_host = nullptr;  // pinned [3]
+  void* cull_ws = nullptr;
+  size_t cull_ws_bytes = 0;
+  // forward stage (double-buffered, engine.hpp:211)
+  float* fwd[2] = {nullptr, nullptr};
+  int fwd_iter[2] = {-1, -1};
+  // gradient stage (double-buffered GradStage, store.hpp:227-248)
+  float* g_geo[2] = {nullptr, nullptr};
+  float* g_ng[2] = {nullptr, nullptr};
+  float* g_m2d[2] = {nullptr, nullptr};
+  int g_iter[2] = {-1, -1};
+  int g_plan[2] = {-1, -1};
+  int64_t cap_rows = 0;  // capacity of fwd / grad buffers in rows
+  // render
+  gss_render_ctx* rctx = nullptr;
+  float* image = nullptr;
+  float* d_img = nullptr;
+  float* gt_step = nullptr;
+  float* loss_dev = nullptr;  // per iteration of a run
+  int loss_cap = 0;
+  double* accum_norm = nullptr;
+  int32_t* accum_cnt = nullptr;
+  // streams / events
+  cudaStream_t sD = nullptr, sH = nullptr;
+  gssd::Ev ev_cull[3], ev_fp[2], ev_handoff[2], ev_lazy[2], ev_render[2];
+  struct TimeRec {
+    int stage;
+    cudaEvent_t a, b;
+  };
+  std::vector<cudaEvent_t> ev_free;
+  std::vector<TimeRec> pending_times;
+  double stage_ms[gssd::kStages] = {0, 0, 0, 0, 0, 0};
+  // iteration bookkeeping
+  int next_iter = 0;
+  int seg_begin = 0;
+  int open_pending = -1;  // iteration whose lazy update is still owed
+  int64_t launches_at_start = 0, launches_last = 0;
+  std::vector<int64_t> valid_counts;
+};
+
+namespace gssd {
+namespace {
+
+cudaStream_t S(gss_engine* e, bool host_tier) { return (e->cfg.pipelined && host_tier) ? e->sH : e->sD; }
+
+void ensure_rows(gss_engine* e, int64_t V) {
+  if (V <= e->cap_rows) return;
+  GSS_CUDA(cudaDeviceSynchronize());
+  const int64_t cap = std::min<int64_t>(e->n, std::max<int64_t>(V + V / 4, 1024));
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(e->fwd[b]);
+    cudaFree(e->g_geo[b]);
+    cudaFree(e->g_ng[b]);
+    cudaFree(e->g_m2d[b]);
+    e->fwd[b] = dmalloc<float>((size_t)cap * kNgDim);
+    e->g_geo[b] = dmalloc<float>((size_t)cap * kGeoDim);
+    e->g_ng[b] = dmalloc<float>((size_t)cap * kNgDim);
+    e->g_m2d[b] = dmalloc<float>((size_t)cap * 2);
+  }
+  e->cap_rows = cap;
+}
+
+cudaEvent_t take_event(gss_engine* e) {
+  if (!e->ev_free.empty()) {
+    cudaEvent_t ev = e->ev_free.back();
+    e->ev_free.pop_back();
+    return ev;
+  }
+  cudaEvent_t ev;
+  GSS_CUDA(cudaEventCreate(&ev));
+  return ev;
+}
+void stage_begin(gss_engine* e, int st, cudaStream_t s, int) {
+  gss_engine::TimeRec r{st, take_event(e), take_event(e)};
+  GSS_CUDA(cudaEventRecord(r.a, s));
+  e->pending_times.push_back(r);
+}
+void stage_end(gss_engine* e, int st, cudaStream_t s, int) {
+  for (auto it = e->pending_times.rbegin(); it != e->pending_times.rend(); ++it)
+    if (it->stage == st) {
+      GSS_CUDA(cudaEventRecord(it->b, s));
+      return;
+    }
+}
+// After a drain: fold the recorded stage intervals into stage_ms and recycle the events.
+void collect_times(gss_engine* e) {
+  for (auto& r : e->pending_times) {
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) e->stage_ms[r.stage] += ms;
+    e->ev_free.push_back(r.a);
+    e->ev_free.push_back(r.b);
+  }
+  cudaGetLastError();
+  e->pending_times.clear();
+}
+
+// engine.hpp:255-278 (no split cameras: the split machinery is §8f "next").
+void stage_cull(gss_engine* e, int g, const gss_camera& cam) {
+  const int p = g % 3;
+  cudaStream_t s = e->sD;
+  stage_begin(e, kCull, s, g & 1);
+  const gss_viewport vp{0.0f, (float)cam.width, 0.0f, (float)cam.height};
+  cull(e->gw, e->n, kGeoDim, &cam, &vp, e->cfg.low_pass, nullptr, e->ids[p], e->count[p], e->cull_ws,
+       e->cull_ws_bytes, s);
+  GSS_CUDA(cudaMemcpyAsync(e->count_host + p, e->count[p], sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  stage_end(e, kCull, s, g & 1);
+  GSS_CUDA(cudaEventRecord(e->ev_cull[p].e, s));
+}
+
+// engine.hpp:282-307: restore_view of ids(g) with pending grads(g-1).
+void stage_forward_params(gss_engine* e, int g) {
+  const int p = g % 3, b = g % 2;
+  cudaStream_t s = S(e, true);
+  if (e->cfg.pipelined) {
+    GSS_CUDA(cudaStreamWaitEvent(s, e->ev_cull[p].e, 0));
+    if (g > e->seg_begin) GSS_CUDA(cudaStreamWaitEvent(s, e->ev_handoff[(g - 1) % 2].e, 0));
+    // fwd[b] is free once render(g-2) consumed it
+    GSS_CUDA(cudaStreamWaitEvent(s, e->ev_render[b].e, 0));
+  }
+  // V is needed on the host to size staging buffers: wait for this plan's count.
+  GSS_CUDA(cudaEventSynchronize(e->ev_cull[p].e));
+  const int64_t V = e->count_host[p];
+  ensure_rows(e, V);
+  stage_begin(e, kFwd, s, b);
+  const int pb = (g - 1) % 2;
+  const bool pending = g > e->seg_begin && e->g_iter[pb] == g - 1;
+  gss_sparse_grads pg{};
+  if (pending) {
+    const int pp = e->g_plan[pb];
+    pg.ids = e->ids[pp];
+    pg.count = e->count_host[pp];
+    pg.count_dev = e->count[pp];
+    pg.rows = e->g_ng[pb];
+    pg.stride = kNgDim;
+    pg.col0 = 0;
+  }
+  adam_restore(&e->ng, e->ids[p], V, e->count[p], pending ? &pg : nullptr, e->fwd[b], s);
+  e->fwd_iter[b] = g;
+  stage_end(e, kFwd, s, b);
+  GSS_CUDA(cudaEventRecord(e->ev_fp[b].e, s));
+}
+
+// engine.hpp:311-377.
+void stage_render(gss_engine* e, int g, const gss_camera& cam, const float* gt_dev, float* loss_out) {
+  const int p = g % 3, b = g % 2;
+  cudaStream_t s = e->sD;
+  if (e->cfg.pipelined) {
+    GSS_CUDA(cudaStreamWaitEvent(s, e->ev_fp[b].e, 0));
+    // grads[b] is free once lazy(g-2) consumed it
+    GSS_CUDA(cudaStreamWaitEvent(s, e->ev_lazy[b].e, 0));
+  }
+  require(e->fwd_iter[b] == g, "render: forwarded buffer is not for this iteration", GSS_ERR_INVARIANT);
+  stage_begin(e, kRender, s, b);
+  const int64_t V = e->count_host[p];
+  gss_render_scene sc{};
+  sc.ids = e->ids[p];
+  sc.count = V;
+  sc.geo = e->gw;
+  sc.geo_stride = kGeoDim;
+  sc.nongeo = e->fwd[b];
+  sc.nongeo_stride = kNgDim;
+  sc.nongeo_compact = 1;
+  const int deg = e->cfg.sh_warmup_step > 0 ? std::min(e->cfg.sh_degree, g / e->cfg.sh_warmup_step)
+                                            : e->cfg.sh_degree;  // engine.hpp:45-48
+  sc.sh_degree = deg;
+  for (int c = 0; c < 3; ++c) sc.background[c] = e->cfg.background[c];
+  sc.low_pass = e->cfg.low_pass;
+  const gss_viewport vp{0.0f, (float)cam.width, 0.0f, (float)cam.height};
+  const int64_t full = (int64_t)cam.width * cam.height * 3;
+  rasterize_forward(e->rctx, &sc, &cam, &vp, e->image, gt_dev, full, e->d_img, loss_out,
+                    nullptr, nullptr, nullptr, s);
+  rasterize_backward(e->rctx, e->d_img, e->g_geo[b], kGeoDim, e->g_ng[b], kNgDim, e->g_m2d[b], s);
+  e->g_plan[b] = p;
+  stage_end(e, kRender, s, b);
+  GSS_CUDA(cudaEventRecord(e->ev_render[b].e, s));
+}
+
+// engine.hpp:380-386: immediate dense update of the geometric tier (geo_defer_max = 0).
+void stage_geo_update(gss_engine* e, int g) {
+  const int p = g % 3, b = g % 2;
+  cudaStream_t s = e->sD;
+  stage_begin(e, kGeo, s, b);
+  gss_sparse_grads gr{};
+  gr.ids = e->ids[p];
+  gr.count = e->count_host[p];
+  gr.count_dev = e->count[p];
+  gr.rows = e->g_geo[b];
+  gr.stride = kGeoDim;
+  gr.col0 = 0;
+  adam_update(&e->geo, &gr, nullptr, nullptr, s);
+  stage_end(e, kGeo, s, b);
+}
+
+// engine.hpp:391-417: gradients stay in HBM (the stage buffer render wrote); densification
+// statistics are accumulated and the stage is handed to forward_params(g+1) / lazy(g).
+void stage_handoff(gss_engine* e, int g) {
+  const int p = g % 3, b = g % 2;
+  cudaStream_t s = e->sD;
+  stage_begin(e, kHandoff, s, b);
+  const int64_t V = e->count_host[p];
+  if (V > 0) {
+    const int blocks = (int)std::min<int64_t>(ceil_div(V, 256), 148 * 8);
+    handoff_stats_kernel<<<blocks, 256, 0, s>>>(e->ids[p], e->count[p], e->g_m2d[b], e->accum_norm, e->accum_cnt);
+    GSS_LAUNCHED();
+  }
+  e->g_iter[b] = g;
+  stage_end(e, kHandoff, s, b);
+  GSS_CUDA(cudaEventRecord(e->ev_handoff[b].e, s));
+}
+
+// engine.hpp:420-430: lazy deferred update of the non-geometric tier with grads(g).
+void stage_lazy(gss_engine* e, int g) {
+  const int b = g % 2;
+  cudaStream_t s = S(e, true);
+  require(e->g_iter[b] == g, "lazy update: staging buffer holds a different iteration", GSS_ERR_INVARIANT);
+  if (e->cfg.pipelined) GSS_CUDA(cudaStreamWaitEvent(s, e->ev_handoff[b].e, 0));
+  stage_begin(e, kLazy, s, b);
+  const int p = e->g_plan[b];
+  gss_sparse_grads gr{};
+  gr.ids = e->ids[p];
+  gr.count = e->count_host[p];
+  gr.count_dev = e->count[p];
+  gr.rows = e->g_ng[b];
+  gr.stride = kNgDim;
+  gr.col0 = 0;
+  adam_update(&e->ng, &gr, nullptr, nullptr, s);
+  stage_end(e, kLazy, s, b);
+  GSS_CUDA(cudaEventRecord(e->ev_lazy[b].e, s));
+}
+
+// One iteration g of the DAG. Serial mode keeps run_serial's order on one stream
+// (engine.hpp:434-445); pipelined mode enqueues lazy(g-1) on the host-tier stream right after
+// fp(g) so it overlaps render(g) (engine.hpp:498-508). The data each stage reads is the same in
+// both orders, so the trajectories are bitwise identical.
+void iteration(gss_engine* e, int g, const gss_camera& cam, const float* gt_dev, float* loss_out) {
+  stage_cull(e, g, cam);
+  stage_forward_params(e, g);
+  const int owed = e->open_pending;
+  if (e->cfg.pipelined && owed >= 0) stage_lazy(e, owed);
+  stage_render(e, g, cam, gt_dev, loss_out);
+  if (!e->cfg.pipelined && owed >= 0) stage_lazy(e, owed);
+  stage_geo_update(e, g);
+  stage_handoff(e, g);
+  e->open_pending = g;
+  e->valid_counts.push_back(e->count_host[g % 3]);
+}
+
+void drain(gss_engine* e) {
+  if (e->open_pending >= 0) {
+    stage_lazy(e, e->open_pending);
+    e->open_pending = -1;
+  }
+  GSS_CUDA(cudaStreamSynchronize(e->sD));
+  GSS_CUDA(cudaStreamSynchronize(e->sH));
+  collect_times(e);
+}
+
+void ensure_loss(gss_engine* e, int n) {
+  if (n <= e->loss_cap) return;
+  GSS_CUDA(cudaDeviceSynchronize());
+  cudaFree(e->loss_dev);
+  e->loss_dev = dmalloc<float>((size_t)n);
+  e->loss_cap = n;
+}
+
+void setup_arena(gss_arena& a, float* w, float* m, float* v, uint8_t* c, int64_t n, int dim, int defer_max,
+                 bool geo, const gss_engine_config& cfg) {
+  a = gss_arena{};
+  a.w = w; a.m = m; a.v = v; a.counter = c; a.n = n; a.dim = dim; a.defer_max = defer_max; a.step = 0;
+  auto grp = [&](int col0, int d, double lr) {
+    gss_group gg{col0, d, lr, cfg.beta1, cfg.beta2, cfg.eps};
+    a.groups[a.ngroups++] = gg;
+  };
+  if (geo) {  // store.hpp:129-131
+    grp(0, 3, cfg.lr_mean * cfg.scene_extent);
+    grp(3, 3, cfg.lr_scale);
+    grp(6, 4, cfg.lr_quat);
+  } else {  // store.hpp:132-136
+    grp(0, 1, cfg.lr_opacity);
+    grp(1, 3, cfg.lr_sh);
+    grp(4, 45, cfg.lr_sh / cfg.sh_rest_divisor);
+  }
+}
+
+}  // namespace
+
+void engine_config_default(gss_engine_config* c) {
+  *c = gss_engine_config{};
+  c->lr_mean = 1.6e-4; c->lr_scale = 5e-3; c->lr_quat = 1e-3; c->lr_opacity = 5e-2; c->lr_sh = 2.5e-3;
+  c->sh_rest_divisor = 20.0; c->beta1 = 0.9; c->beta2 = 0.999; c->eps = 1e-8; c->scene_extent = 1.0;
+  c->defer_max = 15; c->geo_defer_max = 0; c->pipelined = 1; c->sh_degree = 3; c->sh_warmup_step = 0;
+  c->background[0] = c->background[1] = c->background[2] = 0.0f;
+  c->low_pass = 0.3f;
+  c->nongeo_on_host = 0;
+  c->chunk_bytes = int64_t(32) << 20;
+}
+
+gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss_camera* cams, const float* gts,
+                          const gss_engine_config* cfg) {
+  require(n >= 0 && n <= INT32_MAX, "engine: n out of range");
+  require(n == 0 || rows, "engine: null init rows");
+  require(ncams >= 0 && (ncams == 0 || cams), "engine: null cameras");
+  require(cfg != nullptr, "engine: null config");
+  require(cfg->defer_max >= 0 && cfg->defer_max <= 254 && cfg->geo_defer_max >= 0 && cfg->geo_defer_max <= 254,
+          "config: defer max must be in [0,254]");
+  require(cfg->sh_degree >= 0 && cfg->sh_degree <= 3, "config: sh_degree must be in [0,3]");
+  for (int i = 0; i < ncams; ++i) {
+    require(cams[i].near_plane > 0 && cams[i].far_plane > cams[i].near_plane, "camera: require 0 < near < far");
+    require(cams[i].width >= 1 && cams[i].height >= 1, "camera: require W, H >= 1");
+  }
+  auto e = std::make_unique<gss_engine>();
+  e->cfg = *cfg;
+  e->n = n;
+  e->cams.assign(cams, cams + ncams);
+  e->ng_host = cfg->nongeo_on_host != 0;
+  GSS_CUDA(cudaStreamCreateWithFlags(&e->sD, cudaStreamNonBlocking));
+  GSS_CUDA(cudaStreamCreateWithFlags(&e->sH, cudaStreamNonBlocking));
+  const size_t nn = (size_t)std::max<int64_t>(n, 1);
+  e->gw = dmalloc<float>(nn * kGeoDim);
+  e->gm = dmalloc<float>(nn * kGeoDim);
+  e->gv = dmalloc<float>(nn * kGeoDim);
+  e->gcnt = dmalloc<uint8_t>(nn);
+  if (e->ng_host) {
+    GSS_CUDA(cudaHostAlloc((void**)&e->nw, nn * kNgDim * 4, cudaHostAllocMapped));
+    GSS_CUDA(cudaHostAlloc((void**)&e->nm, nn * kNgDim * 4, cudaHostAllocMapped));
+    GSS_CUDA(cudaHostAlloc((void**)&e->nv, nn * kNgDim * 4, cudaHostAllocMapped));
+    GSS_CUDA(cudaHostAlloc((void**)&e->ncnt, nn, cudaHostAllocMapped));
+  } else {
+    e->nw = dmalloc<float>(nn * kNgDim);
+    e->nm = dmalloc<float>(nn * kNgDim);
+    e->nv = dmalloc<float>(nn * kNgDim);
+    e->ncnt = dmalloc<uint8_t>(nn);
+  }
+  GSS_CUDA(cudaMemsetAsync(e->gm, 0, nn * kGeoDim * 4, e->sD));
+  GSS_CUDA(cudaMemsetAsync(e->gv, 0, nn * kGeoDim * 4, e->sD));
+  GSS_CUDA(cudaMemsetAsync(e->gcnt, 0, nn, e->sD));
+  GSS_CUDA(cudaMemsetAsync(e->nm, 0, nn * kNgDim * 4, e->sD));
+  GSS_CUDA(cudaMemsetAsync(e->nv, 0, nn * kNgDim * 4, e->sD));
+  GSS_CUDA(cudaMemsetAsync(e->ncnt, 0, nn, e->sD));
+  if (n > 0) {
+    float* rows_dev = dmalloc<float>((size_t)n * kRowDim);
+    GSS_CUDA(cudaMemcpyAsync(rows_dev, rows, (size_t)n * kRowDim * 4, cudaMemcpyHostToDevice, e->sD));
+    split_rows_kernel<<<(unsigned)ceil_div(n * kRowDim, 256), 256, 0, e->sD>>>(rows_dev, n, e->gw, e->nw);
+    GSS_LAUNCHED();
+    GSS_CUDA(cudaStreamSynchronize(e->sD));
+    cudaFree(rows_dev);
+  }
+  setup_arena(e->geo, e->gw, e->gm, e->gv, e->gcnt, n, kGeoDim, cfg->geo_defer_max, true, *cfg);
+  setup_arena(e->ng, e->nw, e->nm, e->nv, e->ncnt, n, kNgDim, cfg->defer_max, false, *cfg);
+  for (int p = 0; p < 3; ++p) {
+    e->ids[p] = dmalloc<int32_t>(nn);
+    e->count[p] = dmalloc<int64_t>(1);
+  }
+  GSS_CUDA(cudaHostAlloc((void**)&e->count_host, 3 * sizeof(int64_t), cudaHostAllocDefault));
+  e->cull_ws_bytes = cull_workspace_bytes(n);
+  e->cull_ws = dmalloc<char>(e->cull_ws_bytes);
+  e->accum_norm = dmalloc<double>(nn);
+  e->accum_cnt = dmalloc<int32_t>(nn);
+  GSS_CUDA(cudaMemsetAsync(e->accum_norm, 0, nn * 8, e->sD));
+  GSS_CUDA(cudaMemsetAsync(e->accum_cnt, 0, nn * 4, e->sD));
+  int maxW = 1, maxH = 1;
+  for (const auto& c : e->cams) {
+    maxW = std::max(maxW, c.width);
+    maxH = std::max(maxH, c.height);
+  }
+  e->W = maxW;
+  e->H = maxH;
+  const size_t img = (size_t)maxW * maxH * 3;
+  e->image = dmalloc<float>(img);
+  e->d_img = dmalloc<float>(img);
+  e->gt_step = dmalloc<float>(img);
+  if (gts && ncams > 0) {
+    e->gts_dev = dmalloc<float>(img * ncams);
+    size_t off = 0;
+    for (int i = 0; i < ncams; ++i) {
+      const size_t sz = (size_t)cams[i].width * cams[i].height * 3;
+      GSS_CUDA(cudaMemcpyAsync(e->gts_dev + img * i, gts + off, sz * 4, cudaMemcpyHostToDevice, e->sD));
+      off += sz;
+    }
+  }
+  e->rctx = render_ctx_create();
+  GSS_CUDA(cudaStreamSynchronize(e->sD));
+  return e.release();
+}
+
+void engine_destroy(gss_engine* e) {
+  if (!e) return;
+  cudaDeviceSynchronize();
+  auto f = [](void* p) { if (p) cudaFree(p); };
+  f(e->gts_dev); f(e->gw); f(e->gm); f(e->gv); f(e->gcnt);
+  if (e->ng_host) {
+    cudaFreeHost(e->nw); cudaFreeHost(e->nm); cudaFreeHost(e->nv); cudaFreeHost(e->ncnt);
+  } else {
+    f(e->nw); f(e->nm); f(e->nv); f(e->ncnt);
+  }
+  for (int p = 0; p < 3; ++p) { f(e->ids[p]); f(e->count[p]); }
+  if (e->count_host) cudaFreeHost(e->count_host);
+  f(e->cull_ws);
+  for (int b = 0; b < 2; ++b) { f(e->fwd[b]); f(e->g_geo[b]); f(e->g_ng[b]); f(e->g_m2d[b]); }
+  render_ctx_destroy(e->rctx);
+  f(e->image); f(e->d_img); f(e->gt_step); f(e->loss_dev); f(e->accum_norm); f(e->accum_cnt);
+  collect_times(e);
+  for (auto ev : e->ev_free) cudaEventDestroy(ev);
+  if (e->sD) cudaStreamDestroy(e->sD);
+  if (e->sH) cudaStreamDestroy(e->sH);
+  cudaGetLastError();
+  delete e;
+}
+
+// OffloadEngine::run (engine.hpp:73-88): n iterations over the stored cameras, then drained.
+void engine_run(gss_engine* e, int iters, float* losses, int32_t* valid) {
+  require(e != nullptr, "engine: null");
+  require(iters >= 0, "engine: negative iteration count");
+  if (iters == 0) return;
+  require(!e->cams.empty(), "engine: no cameras");
+  require(e->gts_dev != nullptr, "engine: run() needs stored ground-truth images");
+  require(e->open_pending < 0, "engine: run() inside an open step() segment; call drain first",
+          GSS_ERR_INVARIANT);
+  const int64_t l0 = launches();
+  ensure_loss(e, iters);
+  const int g0 = e->next_iter;
+  e->seg_begin = g0;
+  e->valid_counts.clear();
+  const size_t img = (size_t)e->W * e->H * 3;
+  for (int j = 0; j < iters; ++j) {
+    const int g = g0 + j;
+    const size_t ci = (size_t)g % e->cams.size();
+    iteration(e, g, e->cams[ci], e->gts_dev + img * ci, e->loss_dev + j);
+  }
+  drain(e);
+  e->next_iter = g0 + iters;
+  if (losses) GSS_CUDA(cudaMemcpy(losses, e->loss_dev, (size_t)iters * 4, cudaMemcpyDeviceToHost));
+  if (valid)
+    for (int j = 0; j < iters; ++j) valid[j] = (int32_t)e->valid_counts[j];
+  e->launches_last = launches() - l0;
+}
+
+// Streaming entry point: one iteration with a host camera + ground truth. The segment stays open
+// (the lazy update of this iteration is applied by the next step, exactly as inside run()).
+void engine_step(gss_engine* e, const gss_camera* cam, const float* gt_host, float* loss_host, int32_t* valid_host) {
+  require(e && cam && gt_host, "engine_step: null argument");
+  require(cam->width <= e->W && cam->height <= e->H, "engine_step: camera larger than the engine's image buffers");
+  require(cam->near_plane > 0 && cam->far_plane > cam->near_plane, "camera: require 0 < near < far");
+  const int64_t l0 = launches();
+  ensure_loss(e, 1);
+  const int g = e->next_iter;
+  if (e->open_pending < 0) {
+    e->seg_begin = g;
+    e->valid_counts.clear();
+  }
+  const size_t bytes = (size_t)cam->width * cam->height * 3 * 4;
+  GSS_CUDA(cudaMemcpyAsync(e->gt_step, gt_host, bytes, cudaMemcpyHostToDevice, e->sD));
+  iteration(e, g, *cam, e->gt_step, e->loss_dev);
+  e->next_iter = g + 1;
+  float l = 0.0f;
+  GSS_CUDA(cudaMemcpyAsync(&l, e->loss_dev, 4, cudaMemcpyDeviceToHost, e->sD));
+  GSS_CUDA(cudaStreamSynchronize(e->sD));
+  if (loss_host) *loss_host = l;
+  if (valid_host) *valid_host = (int32_t)e->count_host[g % 3];
+  e->launches_last = launches() - l0;
+}
+
+void engine_drain(gss_engine* e) {
+  require(e != nullptr, "engine: null");
+  drain(e);
+}
+
+// snapshot (engine.hpp:91-111): both tiers restored (no pending pass), joined to n x 59.
+void engine_snapshot(gss_engine* e, float* rows_out) {
+  require(e && rows_out, "snapshot: null argument");
+  if (e->open_pending >= 0) drain(e);
+  const int64_t n = e->n;
+  if (n == 0) return;
+  cudaStream_t s = e->sD;
+  int32_t* all = dmalloc<int32_t>((size_t)n);
+  float* geo = dmalloc<float>((size_t)n * kGeoDim);
+  float* ng = dmalloc<float>((size_t)n * kNgDim);
+  float* rows = dmalloc<float>((size_t)n * kRowDim);
+  iota_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(all, n);
+  GSS_LAUNCHED();
+  adam_restore(&e->geo, all, n, nullptr, nullptr, geo, s);
+  adam_restore(&e->ng, all, n, nullptr, nullptr, ng, s);
+  join_rows_kernel<<<(unsigned)ceil_div(n * kRowDim, 256), 256, 0, s>>>(geo, ng, n, rows);
+  GSS_LAUNCHED();
+  GSS_CUDA(cudaMemcpyAsync(rows_out, rows, (size_t)n * kRowDim * 4, cudaMemcpyDeviceToHost, s));
+  GSS_CUDA(cudaStreamSynchronize(s));
+  cudaFree(all); cudaFree(geo); cudaFree(ng); cudaFree(rows);
+}
+
+void engine_state(gss_engine* e, float* geo_w, float* ng_w, float* ng_m, float* ng_v, uint8_t* ng_counter,
+                  int64_t* steps2) {
+  require(e != nullptr, "engine: null");
+  if (e->open_pending >= 0) drain(e);
+  GSS_CUDA(cudaDeviceSynchronize());
+  const size_t n = (size_t)e->n;
+  if (geo_w) GSS_CUDA(cudaMemcpy(geo_w, e->gw, n * kGeoDim * 4, cudaMemcpyDefault));
+  if (ng_w) GSS_CUDA(cudaMemcpy(ng_w, e->nw, n * kNgDim * 4, cudaMemcpyDefault));
+  if (ng_m) GSS_CUDA(cudaMemcpy(ng_m, e->nm, n * kNgDim * 4, cudaMemcpyDefault));
+  if (ng_v) GSS_CUDA(cudaMemcpy(ng_v, e->nv, n * kNgDim * 4, cudaMemcpyDefault));
+  if (ng_counter) GSS_CUDA(cudaMemcpy(ng_counter, e->ncnt, n, cudaMemcpyDefault));
+  if (steps2) {
+    steps2[0] = e->geo.step;
+    steps2[1] = e->ng.step;
+  }
+}
+
+void engine_accum(gss_engine* e, double* norm, int32_t* cnt) {
+  require(e != nullptr, "engine: null");
+  GSS_CUDA(cudaDeviceSynchronize());
+  if (norm) GSS_CUDA(cudaMemcpy(norm, e->accum_norm, (size_t)e->n * 8, cudaMemcpyDeviceToHost));
+  if (cnt) GSS_CUDA(cudaMemcpy(cnt, e->accum_cnt, (size_t)e->n * 4, cudaMemcpyDeviceToHost));
+}
+
+void engine_stage_ms(gss_engine* e, double* out6) {
+  require(e && out6, "engine: null");
+  for (int i = 0; i < kStages; ++i) {
+    out6[i] = e->stage_ms[i];
+    e->stage_ms[i] = 0.0;
+  }
+}
+
+int64_t engine_launches(gss_engine* e) { return e ? e->launches_last : 0; }
+int64_t engine_count(gss_engine* e) { return e ? e->n : 0; }
+
+}  // namespace gssd

@@ -1,0 +1,822 @@
+// Tile-binned rasterizer forward / L1 loss / backward on the device — the B200 replacement of
+// project_all, rasterize_forward, compute_loss_l1 and rasterize_backward (render.hpp:361-640).
+//
+// The reference builds a per-pixel CSR list over each splat's integer 3-sigma pixel box, in
+// (depth, id) order, then composites every pixel front to back. Here:
+//   preprocess  thread per visible slot: exact project_geo + sigmoid + SH colour (render.hpp:361-380),
+//               the fp64 pixel box (render.hpp:307-314), and the number of 16x16 tiles it touches.
+//   duplicate   one (tile, depth) key per touched tile; CUB stable radix sort keeps equal depths in
+//               slot order = ascending id, i.e. the reference's std::stable_sort order per pixel.
+//   forward     CTA per tile, thread per pixel: batches of 256 splat records staged in SMEM, the
+//               per-pixel box test reproduces the CSR membership, compositing is the reference's
+//               op sequence (T-stop tested before each covering contribution, alpha clamp 0.999,
+//               no 1/255 cut), so pixels are bit-identical. L1 loss + its gradient are fused in.
+//   backward    CTA per tile: reverse sweep with transmittance recovered by division, 9-float
+//               screen-space gradients reduced per splat with warp shuffles and a fixed-order
+//               cross-warp sum into one partial per (splat, tile) instance — no float atomics,
+//               so the result is deterministic run to run.
+//   chain       thread per slot: fixed-order sum of its instance partials, then the reference's
+//               chain through sigmoid, SH and project_geo_backward (render.hpp:600-638).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "common.cuh"
+#include "gss_math.cuh"
+
+namespace gssd {
+
+constexpr int kTileSize = 16;
+constexpr int kTilePix = kTileSize * kTileSize;  // 256 threads per CTA
+constexpr int kFwdBatch = 256;
+constexpr int kBwdBatch = 64;
+
+struct __align__(16) SplatRec {
+  float mx, my, a, b;
+  float c, ab, r, g;
+  float bl, depth;
+  int32_t off, pad;
+  int32_t bx0, bx1, by0, by1;  // absolute pixels, half-open, clipped to the window
+};
+static_assert(sizeof(SplatRec) == 64, "record is 4 x 16 B");
+
+struct Win {
+  int px0, py0, pw, ph, tw, th;
+};
+
+struct SceneDev {
+  const int32_t* ids;
+  const float* geo;
+  int64_t geo_stride;
+  const float* nongeo;
+  int64_t ng_stride;
+  int compact;
+  const int32_t* slot_map;
+  int sh_degree;
+  float bg[3];
+  float lp;
+};
+
+// Growable device buffer on the stream-ordered pool.
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes, cudaStream_t st) {
+    if (bytes > cap) {
+      if (p) GSS_CUDA(cudaFreeAsync(p, st));
+      const size_t nb = std::max<size_t>(bytes + bytes / 4, 4096);
+      GSS_CUDA(cudaMallocAsync(&p, nb, st));
+      cap = nb;
+    }
+    return p;
+  }
+  void release(cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace gssd
+
+struct gss_render_ctx {
+  gssd::DBuf recs, ntiles, offsets, keys_a, keys_b, vals_a, vals_b, cub_tmp, ranges, last, fT, partials, lossp,
+      hostcnt;
+  gssd::Win win{};
+  gssd::SceneDev sc{};
+  gssd::Cam cam{};
+  int64_t V = 0, I = 0;
+  int have_forward = 0;
+  int64_t* pinned = nullptr;  // host-visible counts
+  cudaStream_t last_stream = nullptr;
+};
+
+namespace gssd {
+namespace {
+
+__device__ __forceinline__ const float* ng_row(const SceneDev& s, int k, int id) {
+  const int64_t r = s.compact ? (int64_t)(s.slot_map ? s.slot_map[k] : k) : (int64_t)id;
+  return s.nongeo + r * s.ng_stride;
+}
+
+// project_all (render.hpp:361-380) + CSR box (render.hpp:297-314, 418-419) + tile count.
+__global__ void preprocess_kernel(SceneDev s, Cam cam, Win w, int64_t V, SplatRec* recs, int32_t* ntiles) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= V) return;
+  const int id = s.ids[k];
+  const float* g = s.geo + (int64_t)id * s.geo_stride;
+  Proj p;
+  f3 t;
+  SplatRec r;
+  memset(&r, 0, sizeof(r));
+  int nt = 0;
+  if (project_geo(cam, g, s.lp, p, t)) {
+    const float* ng = ng_row(s, (int)k, id);
+    const float ab = 1.0f / (1.0f + gss_expf(-ng[0]));
+    const f3 cp = cam_position(cam);
+    f3 dir{g[0] - cp.x, g[1] - cp.y, g[2] - cp.z};
+    const float dn = sqrtf(dir.x * dir.x + dir.y * dir.y + dir.z * dir.z);
+    if (dn > 1e-12f) {
+      const float inv = 1.0f / dn;
+      dir = f3{dir.x * inv, dir.y * inv, dir.z * inv};
+    } else {
+      dir = f3{0.0f, 0.0f, 1.0f};
+    }
+    float basis[16];
+    sh_basis(dir.x, dir.y, dir.z, s.sh_degree, basis);
+    const int nb = (s.sh_degree + 1) * (s.sh_degree + 1);
+    float rgb0 = 0.5f, rgb1 = 0.5f, rgb2 = 0.5f;
+    for (int b = 0; b < nb; ++b) {
+      rgb0 += basis[b] * ng[1 + 3 * b];
+      rgb1 += basis[b] * ng[2 + 3 * b];
+      rgb2 += basis[b] * ng[3 + 3 * b];
+    }
+    r.mx = p.mx; r.my = p.my; r.a = p.a; r.b = p.b; r.c = p.c; r.ab = ab;
+    r.r = clamp01(rgb0); r.g = clamp01(rgb1); r.bl = clamp01(rgb2);
+    r.depth = t.z;
+    if (p.a * p.c - p.b * p.b > 0.0f) {
+      const double mx = (double)p.mx, my = (double)p.my, rad = (double)p.radius;
+      const int a0 = d2i_x86(ceil(mx - rad - 0.5));
+      const int a1 = (int)((unsigned)d2i_x86(floor(mx + rad - 0.5)) + 1u);
+      const int b0 = d2i_x86(ceil(my - rad - 0.5));
+      const int b1 = (int)((unsigned)d2i_x86(floor(my + rad - 0.5)) + 1u);
+      const int wx1 = w.px0 + w.pw, wy1 = w.py0 + w.ph;
+      const int bx0 = max(w.px0, a0), bx1 = min(wx1, a1), by0 = max(w.py0, b0), by1 = min(wy1, b1);
+      if (bx0 < bx1 && by0 < by1) {
+        r.bx0 = bx0; r.bx1 = bx1; r.by0 = by0; r.by1 = by1;
+        const int tx0 = (bx0 - w.px0) / kTileSize, tx1 = (bx1 - 1 - w.px0) / kTileSize;
+        const int ty0 = (by0 - w.py0) / kTileSize, ty1 = (by1 - 1 - w.py0) / kTileSize;
+        nt = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+      }
+    }
+  }
+  if (nt == 0) r.bx0 = r.bx1 = r.by0 = r.by1 = 0;
+  recs[k] = r;
+  ntiles[k] = nt;
+}
+
+__device__ __forceinline__ void tile_box(const SplatRec& r, const Win& w, int& tx0, int& ty0, int& ntx, int& nty) {
+  tx0 = (r.bx0 - w.px0) / kTileSize;
+  ty0 = (r.by0 - w.py0) / kTileSize;
+  ntx = (r.bx1 - 1 - w.px0) / kTileSize - tx0 + 1;
+  nty = (r.by1 - 1 - w.py0) / kTileSize - ty0 + 1;
+}
+
+__global__ void duplicate_kernel(const SplatRec* recs, const int32_t* offsets, Win w, int64_t V,
+                                 unsigned long long* keys, int32_t* vals, SplatRec* recs_rw) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= V) return;
+  const SplatRec r = recs[k];
+  const int32_t off = offsets[k];
+  recs_rw[k].off = off;
+  if (r.bx1 <= r.bx0) return;
+  int tx0, ty0, ntx, nty;
+  tile_box(r, w, tx0, ty0, ntx, nty);
+  const unsigned long long dbits = (unsigned long long)__float_as_uint(r.depth);
+  int j = 0;
+  for (int ty = ty0; ty < ty0 + nty; ++ty)
+    for (int tx = tx0; tx < tx0 + ntx; ++tx, ++j) {
+      const unsigned long long tile = (unsigned long long)(ty * w.tw + tx);
+      keys[off + j] = (tile << 32) | dbits;
+      vals[off + j] = (int32_t)k;
+    }
+}
+
+__global__ void ranges_kernel(const unsigned long long* keys, int64_t I, int2* ranges) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= I) return;
+  const int tile = (int)(keys[i] >> 32);
+  if (i == 0 || (int)(keys[i - 1] >> 32) != tile) ranges[tile].x = (int)i;
+  if (i == I - 1 || (int)(keys[i + 1] >> 32) != tile) ranges[tile].y = (int)(i + 1);
+}
+
+struct EvalOut {
+  float alpha, q, weight;
+  bool clamped;
+};
+
+// contrib_eval (render.hpp:342-358); det > 0 holds for every binned splat (render.hpp:418).
+__device__ __forceinline__ EvalOut contrib_eval(const SplatRec& r, float cx, float cy) {
+  EvalOut o;
+  const float det = r.a * r.c - r.b * r.b;
+  const float dx = cx - r.mx, dy = cy - r.my;
+  o.q = max0((r.c * dx * dx - 2.0f * r.b * dx * dy + r.a * dy * dy) / det);
+  o.weight = gss_expf(-0.5f * o.q);
+  const float raw = r.ab * o.weight;
+  o.clamped = raw > 0.999f;
+  o.alpha = o.clamped ? 0.999f : raw;
+  return o;
+}
+
+__device__ __forceinline__ void load_rec(SplatRec* dst, const SplatRec* recs, int slot) {
+  const float4* s = reinterpret_cast<const float4*>(recs + slot);
+  float4* d = reinterpret_cast<float4*>(dst);
+  d[0] = s[0]; d[1] = s[1]; d[2] = s[2]; d[3] = s[3];
+}
+
+// Forward composite (render.hpp:438-462) fused with the L1 loss (render.hpp:497-511).
+__global__ void __launch_bounds__(kTilePix) forward_kernel(const SplatRec* __restrict__ recs,
+                                                           const int32_t* __restrict__ vals,
+                                                           const int2* __restrict__ ranges, Win w, float bg0,
+                                                           float bg1, float bg2, float* image, float* fT_out,
+                                                           int32_t* last_out, int32_t* ncontrib_out,
+                                                           const float* gt, int gt_width, float inv_norm,
+                                                           float* d_img, double* loss_partials) {
+  __shared__ SplatRec sh[kFwdBatch];
+  __shared__ double red[kTilePix / 32];
+  const int tile = blockIdx.x;
+  const int tx = tile % w.tw, ty = tile / w.tw;
+  const int lx = threadIdx.x % kTileSize, ly = threadIdx.x / kTileSize;
+  const int x = w.px0 + tx * kTileSize + lx, y = w.py0 + ty * kTileSize + ly;
+  const bool inside = x < w.px0 + w.pw && y < w.py0 + w.ph;
+  const float cx = (float)x + 0.5f, cy = (float)y + 0.5f;
+  const int2 rg = ranges[tile];
+  float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
+  int used = 0, last = 0;
+  bool done = !inside;
+  for (int b = rg.x; b < rg.y; b += kFwdBatch) {
+    if (__syncthreads_count(done) == kTilePix) break;
+    const int nb = min(kFwdBatch, rg.y - b);
+    if ((int)threadIdx.x < nb) load_rec(&sh[threadIdx.x], recs, vals[b + threadIdx.x]);
+    __syncthreads();
+    if (!done) {
+      for (int j = 0; j < nb; ++j) {
+        const SplatRec& r = sh[j];
+        if (x < r.bx0 || x >= r.bx1 || y < r.by0 || y >= r.by1) continue;
+        if (T < 1e-4f) {
+          done = true;
+          break;
+        }
+        const EvalOut ev = contrib_eval(r, cx, cy);
+        c0 += r.r * ev.alpha * T;
+        c1 += r.g * ev.alpha * T;
+        c2 += r.bl * ev.alpha * T;
+        T *= (1.0f - ev.alpha);
+        ++used;
+        last = b + j - rg.x + 1;
+      }
+    }
+    __syncthreads();
+  }
+  double acc = 0.0;
+  if (inside) {
+    const int64_t pix = (int64_t)(y - w.py0) * w.pw + (x - w.px0);
+    const float o0 = c0 + T * bg0, o1 = c1 + T * bg1, o2 = c2 + T * bg2;
+    image[pix * 3 + 0] = o0;
+    image[pix * 3 + 1] = o1;
+    image[pix * 3 + 2] = o2;
+    fT_out[pix] = T;
+    last_out[pix] = last;
+    if (ncontrib_out) ncontrib_out[pix] = used;
+    if (gt) {
+      const float* gp = gt + ((int64_t)y * gt_width + x) * 3;
+      const float o[3] = {o0, o1, o2};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float d = o[c] - gp[c];
+        acc += fabs((double)d);
+        d_img[pix * 3 + c] = d > 0.0f ? inv_norm : (d < 0.0f ? -inv_norm : 0.0f);
+      }
+    }
+  }
+  if (gt) {
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int i = 0; i < kTilePix / 32; ++i) s += red[i];
+      loss_partials[blockIdx.x] = s;
+    }
+  }
+}
+
+__global__ void loss_partial_kernel(const float* img, const float* gt, int64_t n, float inv, float* d_img,
+                                    double* partials) {
+  __shared__ double red[8];
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float d = img[i] - gt[i];
+    acc += fabs((double)d);
+    d_img[i] = d > 0.0f ? inv : (d < 0.0f ? -inv : 0.0f);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    partials[blockIdx.x] = s;
+  }
+}
+
+// Fixed-order final reduction: loss = float(sum) * inv (render.hpp:510).
+__global__ void loss_final_kernel(const double* partials, int n, float inv, float* loss) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partials[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    *loss = (float)s * inv;
+  }
+}
+
+// Reverse sweep (render.hpp:542-589) per tile; one partial SlotAcc per (splat, tile) instance.
+// partial layout: [instance][9] = rgb3, m2d2, cov3, ab.
+__global__ void __launch_bounds__(kTilePix) backward_kernel(const SplatRec* __restrict__ recs,
+                                                            const int32_t* __restrict__ vals,
+                                                            const int2* __restrict__ ranges, Win w, float bg0,
+                                                            float bg1, float bg2, const float* __restrict__ fT_in,
+                                                            const int32_t* __restrict__ last_in,
+                                                            const float* __restrict__ d_img, float* partials) {
+  __shared__ SplatRec sh[kBwdBatch];
+  __shared__ float red[kBwdBatch][kTilePix / 32][9];
+  __shared__ int smax;
+  const int tile = blockIdx.x;
+  const int tx = tile % w.tw, ty = tile / w.tw;
+  const int lx = threadIdx.x % kTileSize, ly = threadIdx.x / kTileSize;
+  const int x = w.px0 + tx * kTileSize + lx, y = w.py0 + ty * kTileSize + ly;
+  const bool inside = x < w.px0 + w.pw && y < w.py0 + w.ph;
+  const float cx = (float)x + 0.5f, cy = (float)y + 0.5f;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int2 rg = ranges[tile];
+  int L = 0;
+  float T = 1.0f, g0 = 0.0f, g1 = 0.0f, g2 = 0.0f;
+  if (inside) {
+    const int64_t pix = (int64_t)(y - w.py0) * w.pw + (x - w.px0);
+    L = last_in[pix];
+    T = fT_in[pix];
+    g0 = d_img[pix * 3];
+    g1 = d_img[pix * 3 + 1];
+    g2 = d_img[pix * 3 + 2];
+    if (g0 == 0.0f && g1 == 0.0f && g2 == 0.0f) L = 0;  // render.hpp:551
+  }
+  float s0 = T * bg0, s1 = T * bg1, s2 = T * bg2;
+  if (threadIdx.x == 0) smax = 0;
+  __syncthreads();
+  if (L > 0) atomicMax(&smax, L);
+  __syncthreads();
+  const int Lmax = smax;
+  const int txi = tx, tyi = ty;
+  for (int bend = Lmax; bend > 0; bend -= kBwdBatch) {
+    const int bstart = max(0, bend - kBwdBatch);
+    const int nb = bend - bstart;
+    __syncthreads();
+    if ((int)threadIdx.x < nb) load_rec(&sh[threadIdx.x], recs, vals[rg.x + bstart + threadIdx.x]);
+    __syncthreads();
+    for (int jj = nb - 1; jj >= 0; --jj) {
+      const SplatRec& r = sh[jj];
+      float v[9];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) v[i] = 0.0f;
+      const bool act = (bstart + jj) < L && x >= r.bx0 && x < r.bx1 && y >= r.by0 && y < r.by1;
+      if (act) {
+        const EvalOut ev = contrib_eval(r, cx, cy);
+        const float alpha = ev.alpha;
+        const float Tb = T / (1.0f - alpha);  // transmittance before this contribution
+        const float w_rgb = alpha * Tb;
+        v[0] = w_rgb * g0;
+        v[1] = w_rgb * g1;
+        v[2] = w_rgb * g2;
+        const float dot_c = r.r * g0 + r.g * g1 + r.bl * g2;
+        const float dot_suf = s0 * g0 + s1 * g1 + s2 * g2;
+        const float d_alpha = Tb * dot_c - dot_suf / (1.0f - alpha);
+        s0 += r.r * alpha * Tb;
+        s1 += r.g * alpha * Tb;
+        s2 += r.bl * alpha * Tb;
+        T = Tb;
+        if (!ev.clamped) {
+          v[8] = ev.weight * d_alpha;
+          const float d_q = -0.5f * alpha * d_alpha;
+          const float det = r.a * r.c - r.b * r.b;
+          const float inv_det = 1.0f / det;
+          const float dx = cx - r.mx, dy = cy - r.my;
+          v[5] = d_q * (dy * dy - ev.q * r.c) * inv_det;
+          v[6] = d_q * (-2.0f * dx * dy + 2.0f * ev.q * r.b) * inv_det;
+          v[7] = d_q * (dx * dx - ev.q * r.a) * inv_det;
+          const float dq_dmx = (-2.0f * r.c * dx + 2.0f * r.b * dy) * inv_det;
+          const float dq_dmy = (2.0f * r.b * dx - 2.0f * r.a * dy) * inv_det;
+          v[3] = d_q * dq_dmx;
+          v[4] = d_q * dq_dmy;
+        }
+      }
+      if (__any_sync(0xffffffffu, act)) {
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+          float s = v[i];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          v[i] = s;
+        }
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < 9; ++i) red[jj][warp][i] = v[i];
+      }
+    }
+    __syncthreads();
+    // Fixed-order cross-warp sum, one instance partial per splat of the batch.
+    for (int e = threadIdx.x; e < nb * 9; e += kTilePix) {
+      const int jj = e / 9, i = e - jj * 9;
+      float s = 0.0f;
+#pragma unroll
+      for (int q = 0; q < kTilePix / 32; ++q) s += red[jj][q][i];
+      const SplatRec& r = sh[jj];
+      int tx0, ty0, ntx, nty;
+      tile_box(r, w, tx0, ty0, ntx, nty);
+      const int64_t inst = (int64_t)r.off + (int64_t)(tyi - ty0) * ntx + (txi - tx0);
+      partials[inst * 9 + i] = s;
+    }
+  }
+}
+
+// render.hpp:600-638 + project_geo_backward (render.hpp:152-237), per slot.
+__global__ void chain_kernel(SceneDev s, Cam cam, Win w, int64_t V, const SplatRec* recs, const int32_t* offsets,
+                             const float* partials, float* gg, int64_t gstride, float* gn, int64_t nstride,
+                             float* mean2d) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= V) return;
+  float* outg = gg + k * gstride;
+  float* outn = gn + k * nstride;
+  float out[59];
+#pragma unroll
+  for (int i = 0; i < 59; ++i) out[i] = 0.0f;
+  float sa[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) sa[i] = 0.0f;
+  const int id = s.ids[k];
+  const float* g = s.geo + (int64_t)id * s.geo_stride;
+  Proj p;
+  f3 t;
+  const bool valid = project_geo(cam, g, s.lp, p, t);
+  if (valid) {
+    const int32_t o0 = offsets[k], o1 = offsets[k + 1];
+    for (int32_t i = o0; i < o1; ++i)
+#pragma unroll
+      for (int c = 0; c < 9; ++c) sa[c] += partials[(int64_t)i * 9 + c];
+    const SplatRec r = recs[k];
+    const float* ng = ng_row(s, (int)k, id);
+    const float ab = r.ab;
+    out[10] += sa[8] * ab * (1.0f - ab);
+    const f3 cp = cam_position(cam);
+    const f3 dir{g[0] - cp.x, g[1] - cp.y, g[2] - cp.z};
+    const float dn = sqrtf(dir.x * dir.x + dir.y * dir.y + dir.z * dir.z);
+    f3 dmd{0.0f, 0.0f, 0.0f};
+    if (dn > 1e-12f) {
+      const float inv = 1.0f / dn;
+      const f3 u{dir.x * inv, dir.y * inv, dir.z * inv};
+      float basis[16];
+      f3 bgr[16];
+      sh_basis(u.x, u.y, u.z, s.sh_degree, basis);
+      sh_basis_grad(u.x, u.y, u.z, s.sh_degree, bgr);
+      const int nb = (s.sh_degree + 1) * (s.sh_degree + 1);
+      float gc[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {  // eval_sh_clamp_mask (sh.hpp:114-125)
+        float v = 0.5f;
+        for (int b = 0; b < nb; ++b) v += basis[b] * ng[1 + 3 * b + c];
+        gc[c] = (v < 0.0f || v > 1.0f) ? 0.0f : sa[c];
+      }
+      f3 ddir{0.0f, 0.0f, 0.0f};
+      for (int b = 0; b < nb; ++b) {  // eval_sh_backward (sh.hpp:92-110)
+        float coef_dot = 0.0f;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          out[11 + 3 * b + c] += basis[b] * gc[c];
+          coef_dot += ng[1 + 3 * b + c] * gc[c];
+        }
+        ddir.x += bgr[b].x * coef_dot;
+        ddir.y += bgr[b].y * coef_dot;
+        ddir.z += bgr[b].z * coef_dot;
+      }
+      const float dotp = u.x * ddir.x + u.y * ddir.y + u.z * ddir.z;
+      const float inv2 = 1.0f / dn;
+      dmd = f3{(ddir.x - u.x * dotp) * inv2, (ddir.y - u.y * dotp) * inv2, (ddir.z - u.z * dotp) * inv2};
+    }
+    out[0] += dmd.x;
+    out[1] += dmd.y;
+    out[2] += dmd.z;
+    // project_geo_backward
+    const float dmx = sa[3], dmy = sa[4], da = sa[5], db = sa[6], dc = sa[7];
+    const float iz = 1.0f / t.z, iz2 = iz * iz;
+    const float qw = g[6], qx = g[7], qy = g[8], qz = g[9];
+    const float qn = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
+    const float qinv = qn > 1e-12f ? 1.0f / qn : 0.0f;
+    const float uq[4] = {qw * qinv, qx * qinv, qy * qinv, qz * qinv};
+    float R[9];
+    quat_to_rot(uq[0], uq[1], uq[2], uq[3], R);
+    const float es[3] = {gss_expf(g[3]), gss_expf(g[4]), gss_expf(g[5])};
+    float B[9], S[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      B[i * 3 + 0] = R[i * 3 + 0] * es[0];
+      B[i * 3 + 1] = R[i * 3 + 1] * es[1];
+      B[i * 3 + 2] = R[i * 3 + 2] * es[2];
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        S[i * 3 + j] = B[i * 3] * B[j * 3] + B[i * 3 + 1] * B[j * 3 + 1] + B[i * 3 + 2] * B[j * 3 + 2];
+    const float fx = cam.fx, fy = cam.fy;
+    const float j00 = fx * iz, j02 = -fx * t.x * iz2;
+    const float j11 = fy * iz, j12 = -fy * t.y * iz2;
+    const float* W = cam.m;
+    const float m0[3] = {j00 * W[0] + j02 * W[6], j00 * W[1] + j02 * W[7], j00 * W[2] + j02 * W[8]};
+    const float m1[3] = {j11 * W[3] + j12 * W[6], j11 * W[4] + j12 * W[7], j11 * W[5] + j12 * W[8]};
+    float v0[3], v1[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      v0[i] = S[i * 3] * m0[0] + S[i * 3 + 1] * m0[1] + S[i * 3 + 2] * m0[2];
+      v1[i] = S[i * 3] * m1[0] + S[i * 3 + 1] * m1[1] + S[i * 3 + 2] * m1[2];
+    }
+    float dm0[3], dm1[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      dm0[i] = v0[i] * (2.0f * da) + v1[i] * db;
+      dm1[i] = v1[i] * (2.0f * dc) + v0[i] * db;
+    }
+    float dS[9], dB[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) dS[i * 3 + j] = da * m0[i] * m0[j] + db * m0[i] * m1[j] + dc * m1[i] * m1[j];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        float a2 = 0.0f;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) a2 += (dS[i * 3 + q] + dS[q * 3 + i]) * B[q * 3 + j];
+        dB[i * 3 + j] = a2;
+      }
+    float G[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      G[i * 3 + 0] = dB[i * 3 + 0] * es[0];
+      G[i * 3 + 1] = dB[i * 3 + 1] * es[1];
+      G[i * 3 + 2] = dB[i * 3 + 2] * es[2];
+    }
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      float a2 = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) a2 += dB[i * 3 + j] * R[i * 3 + j];
+      out[3 + j] += a2 * es[j];
+    }
+    const float qw_ = uq[0], qx_ = uq[1], qy_ = uq[2], qz_ = uq[3];
+#define GG(i, j) G[(i) * 3 + (j)]
+    float dq[4];
+    dq[0] = 2.0f * (-qz_ * GG(0, 1) + qy_ * GG(0, 2) + qz_ * GG(1, 0) - qx_ * GG(1, 2) - qy_ * GG(2, 0) +
+                    qx_ * GG(2, 1));
+    dq[1] = 2.0f * (qy_ * GG(0, 1) + qz_ * GG(0, 2) + qy_ * GG(1, 0) - 2.0f * qx_ * GG(1, 1) - qw_ * GG(1, 2) +
+                    qz_ * GG(2, 0) + qw_ * GG(2, 1) - 2.0f * qx_ * GG(2, 2));
+    dq[2] = 2.0f * (-2.0f * qy_ * GG(0, 0) + qx_ * GG(0, 1) + qw_ * GG(0, 2) + qx_ * GG(1, 0) + qz_ * GG(1, 2) -
+                    qw_ * GG(2, 0) + qz_ * GG(2, 1) - 2.0f * qy_ * GG(2, 2));
+    dq[3] = 2.0f * (-2.0f * qz_ * GG(0, 0) - qw_ * GG(0, 1) + qx_ * GG(0, 2) + qw_ * GG(1, 0) -
+                    2.0f * qz_ * GG(1, 1) + qy_ * GG(1, 2) + qx_ * GG(2, 0) + qy_ * GG(2, 1));
+#undef GG
+    const float nq = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);  // quat_normalize_backward
+    const float qi = 1.0f / nq;
+    const float u4[4] = {qw * qi, qx * qi, qy * qi, qz * qi};
+    const float dotq = u4[0] * dq[0] + u4[1] * dq[1] + u4[2] * dq[2] + u4[3] * dq[3];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[6 + i] += (dq[i] - u4[i] * dotq) * qi;
+    const float dj00 = dm0[0] * W[0] + dm0[1] * W[1] + dm0[2] * W[2];
+    const float dj02 = dm0[0] * W[6] + dm0[1] * W[7] + dm0[2] * W[8];
+    const float dj11 = dm1[0] * W[3] + dm1[1] * W[4] + dm1[2] * W[5];
+    const float dj12 = dm1[0] * W[6] + dm1[1] * W[7] + dm1[2] * W[8];
+    f3 dt;
+    dt.x = dmx * fx * iz + dj02 * (-fx * iz2);
+    dt.y = dmy * fy * iz + dj12 * (-fy * iz2);
+    dt.z = dmx * (-fx * t.x * iz2) + dmy * (-fy * t.y * iz2) + dj00 * (-fx * iz2) + dj11 * (-fy * iz2) +
+           dj02 * (2.0f * fx * t.x * iz2 * iz) + dj12 * (2.0f * fy * t.y * iz2 * iz);
+    out[0] += W[0] * dt.x + W[3] * dt.y + W[6] * dt.z;
+    out[1] += W[1] * dt.x + W[4] * dt.y + W[7] * dt.z;
+    out[2] += W[2] * dt.x + W[5] * dt.y + W[8] * dt.z;
+  }
+#pragma unroll
+  for (int i = 0; i < 10; ++i) outg[i] = out[i];
+#pragma unroll
+  for (int i = 0; i < 49; ++i) outn[i] = out[10 + i];
+  if (mean2d) {
+    mean2d[k * 2] = sa[3];
+    mean2d[k * 2 + 1] = sa[4];
+  }
+}
+
+__global__ void fill_bg_kernel(float* image, float* fT, int32_t* last, int32_t* nc, int64_t npix, float b0, float b1,
+                               float b2) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= npix) return;
+  image[i * 3] = b0;
+  image[i * 3 + 1] = b1;
+  image[i * 3 + 2] = b2;
+  fT[i] = 1.0f;
+  last[i] = 0;
+  if (nc) nc[i] = 0;
+}
+
+Win make_window(const gss_viewport& vp) {
+  // viewport_pixels (render.hpp:297-304)
+  auto cvt = [](double d) -> int {
+    if (!(d >= -2147483648.0 && d < 2147483648.0)) return (int)0x80000000u;
+    return (int)d;
+  };
+  int px0 = cvt(std::ceil(double(vp.x0) - 0.5)), px1 = cvt(std::ceil(double(vp.x1) - 0.5));
+  int py0 = cvt(std::ceil(double(vp.y0) - 0.5)), py1 = cvt(std::ceil(double(vp.y1) - 0.5));
+  px0 = std::max(px0, 0);
+  py0 = std::max(py0, 0);
+  Win w;
+  w.px0 = px0;
+  w.py0 = py0;
+  w.pw = std::max(0, px1 - px0);
+  w.ph = std::max(0, py1 - py0);
+  w.tw = (w.pw + kTileSize - 1) / kTileSize;
+  w.th = (w.ph + kTileSize - 1) / kTileSize;
+  return w;
+}
+
+}  // namespace
+
+void rasterize_forward(gss_render_ctx* ctx, const gss_render_scene* scene, const gss_camera* cam,
+                       const gss_viewport* vp, float* image, const float* gt, int64_t normalizer, float* d_img,
+                       float* loss_dev, float* final_T_opt, int32_t* ncontrib_opt, int64_t* meta, cudaStream_t st) {
+  require(ctx && scene && cam && vp && image, "rasterize_forward: null argument");
+  require(scene->sh_degree >= 0 && scene->sh_degree <= 3, "rasterize_forward: sh_degree must be in [0,3]");
+  require(!gt || (d_img && loss_dev), "rasterize_forward: gt needs d_img and loss_dev");
+  require(scene->geo_stride >= 10 && scene->nongeo_stride >= 49, "rasterize_forward: bad strides");
+  ctx->last_stream = st;
+  if (!ctx->pinned) GSS_CUDA(cudaMallocHost(&ctx->pinned, 4 * sizeof(int64_t)));
+  const Win w = make_window(*vp);
+  require(!gt || (w.px0 + w.pw <= cam->width && w.py0 + w.ph <= cam->height),
+          "compute_loss_l1: image and ground-truth shapes differ");
+  int64_t V = scene->count;
+  if (scene->count_dev) {
+    GSS_CUDA(cudaMemcpyAsync(ctx->pinned, scene->count_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GSS_CUDA(cudaStreamSynchronize(st));
+    V = ctx->pinned[0];
+  }
+  require(V >= 0 && V <= INT32_MAX, "rasterize_forward: visible count out of range");
+  SceneDev& s = ctx->sc;
+  s.ids = scene->ids; s.geo = scene->geo; s.geo_stride = scene->geo_stride; s.nongeo = scene->nongeo;
+  s.ng_stride = scene->nongeo_stride; s.compact = scene->nongeo_compact; s.slot_map = scene->slot_map;
+  s.sh_degree = scene->sh_degree; s.lp = scene->low_pass;
+  for (int c = 0; c < 3; ++c) s.bg[c] = scene->background[c];
+  std::memcpy(&ctx->cam, cam, sizeof(Cam));
+  ctx->win = w;
+  ctx->V = V;
+  ctx->I = 0;
+  ctx->have_forward = 1;
+  const int64_t npix = (int64_t)w.pw * w.ph;
+  float* fT = static_cast<float*>(ctx->fT.get((size_t)std::max<int64_t>(npix, 1) * 4, st));
+  int32_t* last = static_cast<int32_t*>(ctx->last.get((size_t)std::max<int64_t>(npix, 1) * 4, st));
+  const float inv = gt ? 1.0f / (float)(double)(normalizer > 0 ? normalizer : npix * 3) : 0.0f;
+  if (npix == 0) {
+    if (gt) GSS_CUDA(cudaMemsetAsync(loss_dev, 0, sizeof(float), st));
+    if (meta) { meta[0] = w.px0; meta[1] = w.py0; meta[2] = w.pw; meta[3] = w.ph; meta[4] = V; meta[5] = 0; }
+    return;
+  }
+  if (V == 0) {
+    fill_bg_kernel<<<(unsigned)ceil_div(npix, 256), 256, 0, st>>>(image, fT, last, ncontrib_opt, npix, s.bg[0],
+                                                                  s.bg[1], s.bg[2]);
+    GSS_LAUNCHED();
+    if (final_T_opt) GSS_CUDA(cudaMemcpyAsync(final_T_opt, fT, npix * 4, cudaMemcpyDeviceToDevice, st));
+    if (gt) {
+      const int blocks = (int)std::min<int64_t>(ceil_div(npix * 3, 256), 1024);
+      double* lp = static_cast<double*>(ctx->lossp.get((size_t)blocks * 8, st));
+      // gt window == full image only when the window covers it; extract rows for a sub-window.
+      require(w.pw == cam->width && w.px0 == 0, "loss on an empty scene needs a full-width window");
+      loss_partial_kernel<<<blocks, 256, 0, st>>>(image, gt + (int64_t)w.py0 * cam->width * 3, npix * 3, inv, d_img,
+                                                  lp);
+      GSS_LAUNCHED();
+      loss_final_kernel<<<1, 1024, 0, st>>>(lp, blocks, inv, loss_dev);
+      GSS_LAUNCHED();
+    }
+    if (meta) { meta[0] = w.px0; meta[1] = w.py0; meta[2] = w.pw; meta[3] = w.ph; meta[4] = 0; meta[5] = 0; }
+    return;
+  }
+  SplatRec* recs = static_cast<SplatRec*>(ctx->recs.get((size_t)V * sizeof(SplatRec), st));
+  int32_t* nt = static_cast<int32_t*>(ctx->ntiles.get((size_t)(V + 1) * 4, st));
+  int32_t* offs = static_cast<int32_t*>(ctx->offsets.get((size_t)(V + 1) * 4, st));
+  preprocess_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(s, ctx->cam, w, V, recs, nt);
+  GSS_LAUNCHED();
+  GSS_CUDA(cudaMemsetAsync(nt + V, 0, 4, st));
+  size_t tb = 0;
+  GSS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, nt, offs, (int)(V + 1), st));
+  void* tmp = ctx->cub_tmp.get(tb, st);
+  GSS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nt, offs, (int)(V + 1), st));
+  count_launch();
+  GSS_CUDA(cudaMemcpyAsync(ctx->pinned + 1, offs + V, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  GSS_CUDA(cudaStreamSynchronize(st));
+  const int64_t I = (int64_t)(reinterpret_cast<int32_t*>(ctx->pinned + 1)[0]);
+  require(I >= 0, "rasterize_forward: tile instance count overflow");
+  ctx->I = I;
+  const int ntile = w.tw * w.th;
+  int2* ranges = static_cast<int2*>(ctx->ranges.get((size_t)ntile * sizeof(int2), st));
+  GSS_CUDA(cudaMemsetAsync(ranges, 0, (size_t)ntile * sizeof(int2), st));
+  int32_t* vals_sorted = nullptr;
+  if (I > 0) {
+    auto* ka = static_cast<unsigned long long*>(ctx->keys_a.get((size_t)I * 8, st));
+    auto* kb = static_cast<unsigned long long*>(ctx->keys_b.get((size_t)I * 8, st));
+    auto* va = static_cast<int32_t*>(ctx->vals_a.get((size_t)I * 4, st));
+    auto* vb = static_cast<int32_t*>(ctx->vals_b.get((size_t)I * 4, st));
+    duplicate_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(recs, offs, w, V, ka, va, recs);
+    GSS_LAUNCHED();
+    int tile_bits = 1;
+    while ((1ll << tile_bits) < ntile) ++tile_bits;
+    cub::DoubleBuffer<unsigned long long> dk(ka, kb);
+    cub::DoubleBuffer<int32_t> dv(va, vb);
+    size_t sb = 0;
+    GSS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sb, dk, dv, (int)I, 0, 32 + tile_bits, st));
+    void* stmp = ctx->cub_tmp.get(std::max(sb, tb), st);
+    GSS_CUDA(cub::DeviceRadixSort::SortPairs(stmp, sb, dk, dv, (int)I, 0, 32 + tile_bits, st));
+    count_launch();
+    vals_sorted = dv.Current();
+    // keep the sorted arrays addressable for backward
+    if (dk.Current() != ka) std::swap(ctx->keys_a, ctx->keys_b);
+    if (dv.Current() != va) std::swap(ctx->vals_a, ctx->vals_b);
+    ranges_kernel<<<(unsigned)ceil_div(I, 256), 256, 0, st>>>(dk.Current(), I, ranges);
+    GSS_LAUNCHED();
+  } else {
+    vals_sorted = static_cast<int32_t*>(ctx->vals_a.get(16, st));
+  }
+  double* lp = gt ? static_cast<double*>(ctx->lossp.get((size_t)ntile * 8, st)) : nullptr;
+  forward_kernel<<<ntile, kTilePix, 0, st>>>(recs, vals_sorted, ranges, w, s.bg[0], s.bg[1], s.bg[2], image, fT, last,
+                                             ncontrib_opt, gt, cam->width, inv, d_img, lp);
+  GSS_LAUNCHED();
+  if (gt) {
+    loss_final_kernel<<<1, 1024, 0, st>>>(lp, ntile, inv, loss_dev);
+    GSS_LAUNCHED();
+  }
+  if (final_T_opt) GSS_CUDA(cudaMemcpyAsync(final_T_opt, fT, npix * 4, cudaMemcpyDeviceToDevice, st));
+  if (meta) {
+    meta[0] = w.px0; meta[1] = w.py0; meta[2] = w.pw; meta[3] = w.ph; meta[4] = V; meta[5] = I;
+  }
+}
+
+void loss_l1(const float* image, const float* gt, int64_t elems, int64_t normalizer, float* d_img, float* loss_dev,
+             cudaStream_t st) {
+  require(elems >= 0 && (elems == 0 || (image && gt && d_img)) && loss_dev, "compute_loss_l1: null argument");
+  if (normalizer == 0) normalizer = elems;
+  const float inv = 1.0f / (float)(double)normalizer;
+  if (elems == 0) {
+    GSS_CUDA(cudaMemsetAsync(loss_dev, 0, sizeof(float), st));
+    return;
+  }
+  const int blocks = (int)std::min<int64_t>(ceil_div(elems, 256), 1024);
+  double* lp = nullptr;
+  GSS_CUDA(cudaMallocAsync((void**)&lp, (size_t)blocks * 8, st));
+  loss_partial_kernel<<<blocks, 256, 0, st>>>(image, gt, elems, inv, d_img, lp);
+  GSS_LAUNCHED();
+  loss_final_kernel<<<1, 1024, 0, st>>>(lp, blocks, inv, loss_dev);
+  GSS_LAUNCHED();
+  GSS_CUDA(cudaFreeAsync(lp, st));
+}
+
+void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int64_t gstride, float* gn,
+                        int64_t nstride, float* mean2d, cudaStream_t st) {
+  require(ctx && ctx->have_forward, "rasterize_backward: no forward result in this context");
+  require(gg && gn && gstride >= 10 && nstride >= 49, "rasterize_backward: bad gradient buffers");
+  const Win& w = ctx->win;
+  const int64_t V = ctx->V, I = ctx->I;
+  if (V == 0) return;
+  const int64_t npix = (int64_t)w.pw * w.ph;
+  require(npix == 0 || d_img, "rasterize_backward: null d_img");
+  const SplatRec* recs = static_cast<const SplatRec*>(ctx->recs.p);
+  const int32_t* offs = static_cast<const int32_t*>(ctx->offsets.p);
+  float* partials = static_cast<float*>(ctx->partials.get((size_t)std::max<int64_t>(I, 1) * 9 * 4, st));
+  if (I > 0 && npix > 0) {
+    GSS_CUDA(cudaMemsetAsync(partials, 0, (size_t)I * 9 * 4, st));
+    const int ntile = w.tw * w.th;
+    backward_kernel<<<ntile, kTilePix, 0, st>>>(recs, static_cast<const int32_t*>(ctx->vals_a.p),
+                                                static_cast<const int2*>(ctx->ranges.p), w, ctx->sc.bg[0],
+                                                ctx->sc.bg[1], ctx->sc.bg[2], static_cast<const float*>(ctx->fT.p),
+                                                static_cast<const int32_t*>(ctx->last.p), d_img, partials);
+    GSS_LAUNCHED();
+  } else if (I > 0) {
+    GSS_CUDA(cudaMemsetAsync(partials, 0, (size_t)I * 9 * 4, st));
+  }
+  chain_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(ctx->sc, ctx->cam, w, V, recs, offs, partials, gg, gstride,
+                                                          gn, nstride, mean2d);
+  GSS_LAUNCHED();
+}
+
+gss_render_ctx* render_ctx_create() { return new gss_render_ctx(); }
+
+void render_ctx_destroy(gss_render_ctx* ctx) {
+  if (!ctx) return;
+  cudaStream_t st = ctx->last_stream;
+  for (DBuf* b : {&ctx->recs, &ctx->ntiles, &ctx->offsets, &ctx->keys_a, &ctx->keys_b, &ctx->vals_a, &ctx->vals_b,
+                  &ctx->cub_tmp, &ctx->ranges, &ctx->last, &ctx->fT, &ctx->partials, &ctx->lossp, &ctx->hostcnt})
+    b->release(st);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  delete ctx;
+}
+
+}  // namespace gssd
