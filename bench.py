@@ -1,0 +1,462 @@
+"""bench.py — GS-Scale per-iteration training step on the B200 (BASELINE.json configs[1]).
+
+Workload (config C2 of SURVEY.md §8): synthetic 4M-Gaussian scene (the reference generator,
+synth.hpp:100-159, scales shrunk by (1e5/N)^(1/3) so depth complexity stays bounded), 1920x1080
+views, all optimizer state resident in HBM, pipelined two-stream engine, deferred Adam with
+defer_max = 15 for the non-geometric tier, dense immediate Adam for the geometric tier.
+A step = one OffloadEngine iteration: cull(g) + forwarding gather (restore_view + pending pass) +
+rasterize forward + L1 loss + rasterize backward + geo Adam + handoff + lazy deferred Adam(g-1).
+
+Arms:
+  default            our sm_100a path (libgss_b200.so through its C ABI);
+  --impl reference   the reference's own CPU implementation (oracle/_ref/libgss_ref.so: the
+                     unmodified reference headers compiled on this host) on the same scene,
+                     cameras and ground truth, all host threads.
+
+One JSON line on rank 0. Timing: W untimed warm-up iterations, then K iterations bracketed by
+barrier + device sync, CUDA events on the launching streams; inputs (2.8 GB of w/m/v state)
+are far larger than the 126 MB L2, so no flush is needed between iterations.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "training iters/sec & Gaussians culled/s at N Gaussians; Adam/cull HBM GB/s vs peak"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=4_000_000)
+    p.add_argument("--width", type=int, default=1920)
+    p.add_argument("--height", type=int, default=1080)
+    p.add_argument("--cams", type=int, default=8)
+    p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--ref-max-steps", type=int, default=4,
+                   help="reference arm: cap on timed CPU iterations (each is ~20 s at the default workload)")
+    return p.parse_args()
+
+
+def scene_config(n, w, h, cams, seed):
+    """C1's SynthConfig scaled to n Gaussians and a w x h view."""
+    import paper_2509_15645_b200 as G
+
+    s = (1e5 / n) ** (1.0 / 3.0)
+    return G.SynthConfig(seed=seed, n=n, cams=cams, width=w, height=h, radius_min=1.5, radius_max=3.0,
+                         scale_min=0.003 * s, scale_max=0.01 * s, fov_deg=30.0)
+
+
+def training_start(truth: np.ndarray) -> np.ndarray:
+    """Truth with opacity logit(0.1) and SH bands >= 1 zeroed."""
+    start = truth.copy()
+    start[:, 10] = np.float32(np.log(0.1 / 0.9))
+    start[:, 14:] = 0.0
+    return start
+
+
+class Clocks:
+    """nvidia-smi sampler running only during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        try:
+            d = json.loads(f.read_text())
+            for k in ("hbm_gbs", "hbm_GBs", "hbm"):
+                if k in d:
+                    v = d[k]
+                    return float(v["burst"] if isinstance(v, dict) else v), "measured"
+        except Exception:
+            pass
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+# ---------------------------------------------------------------------------------------------
+
+def run_ours(a, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_15645_b200 as G
+    from paper_2509_15645_b200._abi import GssCamera, check, lib
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    # Weak scaling: every rank owns an independent id-range shard of the scene (own seed) and
+    # its optimizer state; no data-path collective.
+    cfg = scene_config(a.n, a.width, a.height, a.cams, a.seed + rank)
+    truth, cams = G.synth_scene_params(cfg)
+    truth_dev = torch.from_numpy(truth).to(dev)
+    gts = np.stack([G.render_view(truth_dev, c, 3).cpu().numpy() for c in cams])
+    del truth_dev
+    torch.cuda.empty_cache()
+    start = training_start(truth)
+    eng = G.OffloadEngine(start, cams, gts, pipelined=True)
+
+    # --- device-resident throughput (value) ---
+    eng.run(a.warmup)
+    eng.stage_ms()  # reset accumulators
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    l0 = G.launch_count()
+    losses, valid = eng.run(a.steps)
+    launches = G.launch_count() - l0
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    stage = eng.stage_ms()
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / a.steps
+    value = world * a.steps / (ms / 1e3)
+
+    # --- end to end through the public per-step API (host GT in, host loss out) ---
+    gts_pinned = [torch.from_numpy(g).pin_memory() for g in gts]
+    ncam = len(cams)
+    for j in range(a.warmup):
+        eng.step(cams[j % ncam], gts_pinned[j % ncam].numpy())
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for j in range(a.steps):
+        eng.step(cams[(a.warmup + j) % ncam], gts_pinned[(a.warmup + j) % ncam].numpy())
+    eng.drain()
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": world * a.steps / (e2e_ms / 1e3), "unit": "iters/s",
+           "h2d_bytes_per_step": a.width * a.height * 3 * 4, "d2h_bytes_per_step": 4 + 8,
+           "api": "gss_engine_step (OffloadEngine.step): pinned host GT -> loss on host"}
+
+    # --- isolated HBM-bound kernels on the trained state (culled/s; Adam GB/s) ---
+    eng.close()
+    torch.cuda.empty_cache()
+    kern = kernel_probe(G, truth, cams, dev, a)
+
+    vis = np.asarray(valid, np.float64)
+    hbm, src = peaks()
+    out = {
+        "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference synth_scene generator, GT rendered on device)",
+        "config": {"workload": f"C2: synthetic {a.n // 1_000_000}M Gaussians, {a.width}x{a.height} views, "
+                               "all state in HBM, pipelined, deferred Adam defer_max=15",
+                   "n_gaussians": a.n, "width": a.width, "height": a.height, "cams": a.cams,
+                   "parallelism": f"replicas x{world} (id-range shards, no data-path collective)" if world > 1
+                   else "1 GPU", "l2": "inputs > L2 (2.8 GB optimizer state per rank), no flush",
+                   "mean_visible": float(vis.mean()), "used_ratio": float(vis.mean() / a.n)},
+        "gpu_launches": int(launches),
+        "stage_ms_per_step": {k: v / a.steps for k, v in stage.items()},
+        "kernels": kern,
+        "e2e": e2e,
+        "clocks": clocks,
+        "losses": [float(losses[0]), float(losses[-1])],
+    }
+    return out, (hbm, src), (cams, gts, start)
+
+
+def kernel_probe(G, truth, cams, dev, a):
+    """The HBM-bound kernels of the step launched alone on one stream, timed with CUDA events on
+    that stream (average per launch): cull over the N x 10 geometric tier, the deferred Adam pass
+    over the N x 49 non-geometric tier in steady state (>= 16 passes, 8.28% density, SURVEY.md
+    §8d), the dense geo Adam pass over N x 10 and the forwarding gather (restore + pending)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2509_15645_b200._abi import check, lib
+
+    L = lib()
+    n = a.n
+    s = torch.cuda.current_stream()
+    sp = s.cuda_stream
+    reps = 20
+
+    def timed(fn, reps=reps):
+        for _ in range(3):
+            fn(0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for r in range(reps):
+            fn(r)
+        e1.record(s)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    res = []
+    # cull (render.hpp:253-260): B = 40 N + 4 V
+    geo = torch.from_numpy(np.ascontiguousarray(truth[:, :10])).to(dev)
+    ids = torch.empty(n, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    wsb = int(L.gss_cull_workspace_bytes(n))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    vp = G.viewport_full(a.width, a.height)
+    cam0 = cams[0]
+
+    def cull(_):
+        check(L.gss_cull(geo.data_ptr(), n, 10, C.byref(cam0), C.byref(vp), 0.3, None, ids.data_ptr(),
+                         cnt.data_ptr(), ws.data_ptr(), wsb, sp))
+
+    ms = timed(cull)
+    vis = int(cnt.item())
+    b = 40 * n + 4 * vis
+    res.append({"kernel": "cull_kernel", "op": "frustum_cull", "ms": ms, "bytes": b, "gbs": b / ms / 1e6,
+                "culled_per_s": n / (ms / 1e3), "visible": vis})
+    del geo, ws
+    # deferred Adam, 49-wide non-geo tier (adam.hpp:211-238):
+    # B = sum_touched 4*49*(6 + has_grad) + 2 N
+    opt = G.OptimConfig()
+    arena = G.Arena(n, 49, opt.nongeo_groups(), 15, device=dev)
+    arena.w.uniform_(-1, 1)
+    dens = 0.0828
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(7)
+    nsched = 4
+    sched = []
+    for k in range(nsched):
+        m = torch.rand(n, device=dev, generator=gen) < dens
+        gi = torch.nonzero(m).flatten().to(torch.int32)
+        sched.append((gi, torch.randn(gi.numel(), 49, device=dev, generator=gen)))
+    touched = torch.empty(n, dtype=torch.int32, device=dev)
+    tcount = torch.zeros(1, dtype=torch.int64, device=dev)
+    for k in range(20):  # steady state: every counter has cycled
+        G.deferred_update(arena, G.SparseGrads(sched[k % nsched][0], sched[k % nsched][1], 49), want_touched=False)
+    st = arena.c_struct()
+    gs = [G.SparseGrads(gi, gr, 49).c_struct() for gi, gr in sched]
+    tot = {"t": 0, "g": 0}
+
+    def deferred(r):
+        g = gs[r % nsched]
+        check(L.gss_deferred_update(C.byref(st), C.byref(g), None, tcount.data_ptr(), sp))
+
+    # touched count per pass for the byte model (measured once per schedule entry, untimed)
+    ms = timed(deferred)
+    arena._sync_step(st)
+    tc = []
+    for k in range(nsched):
+        check(L.gss_deferred_update(C.byref(st), C.byref(gs[k]), None, tcount.data_ptr(), sp))
+        torch.cuda.synchronize()
+        tc.append(int(tcount.item()))
+    touched_avg = float(np.mean(tc))
+    grads_avg = float(np.mean([gi.numel() for gi, _ in sched]))
+    b = 4 * 49 * (6 * touched_avg + grads_avg) + 2 * n
+    res.append({"kernel": "update_kernel<49-wide, deferred>", "op": "deferred_update", "ms": ms, "bytes": b,
+                "gbs": b / ms / 1e6, "touched_rows": touched_avg, "grad_rows": grads_avg})
+    # forwarding gather = restore_view with a pending pass (adam.hpp:252-289):
+    # B = V (3*196 + 1) + V_pend * 196 + V * 196 (+ ids)
+    gi, gr = sched[0]
+    out = torch.empty(gi.numel(), 49, device=dev)
+    pend = gs[1]
+
+    def restore(_):
+        check(L.gss_restore_view(C.byref(st), gi.data_ptr(), gi.numel(), None, C.byref(pend), out.data_ptr(), sp))
+
+    ms = timed(restore)
+    V = gi.numel()
+    vp_ = sched[1][0].numel()
+    b = V * (3 * 196 + 1 + 196 + 4) + vp_ * (196 + 4)
+    res.append({"kernel": "restore_kernel (forwarding gather)", "op": "restore_view", "ms": ms, "bytes": b,
+                "gbs": b / ms / 1e6, "rows": V})
+    del arena, sched, gs, out, touched
+    torch.cuda.empty_cache()
+    # geo Adam: dense pass over N x 10 with sparse grads (engine.hpp:380-386): B = 240 N + 40 V
+    garena = G.Arena(n, 10, opt.geo_groups(), 0, device=dev)
+    garena.w.uniform_(-1, 1)
+    gi = torch.nonzero(torch.rand(n, device=dev, generator=gen) < dens).flatten().to(torch.int32)
+    gg = torch.randn(gi.numel(), 10, device=dev, generator=gen)
+    gst = garena.c_struct()
+    ggs = G.SparseGrads(gi, gg, 10).c_struct()
+
+    def geo_upd(_):
+        check(L.gss_deferred_update(C.byref(gst), C.byref(ggs), None, None, sp))
+
+    ms = timed(geo_upd)
+    b = 240 * n + 44 * gi.numel()
+    res.append({"kernel": "update_kernel<10-wide, dense>", "op": "geo deferred_update (defer_max=0)", "ms": ms,
+                "bytes": b, "gbs": b / ms / 1e6})
+    del garena
+    torch.cuda.empty_cache()
+    return res
+
+
+def cpu_baseline(cams, gts, start, a, steps=1):
+    """The reference's own CPU implementation (oracle/_ref/libgss_ref.so, the unmodified reference
+    headers behind a C shim) timed on this host: one full OffloadEngine iteration of the same
+    workload, all host threads as render workers."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracles as O
+
+    if O.ref() is None:
+        return None
+    cores = os.cpu_count() or 1
+    cam_arr = np.stack([O.cam_from_struct(c) for c in cams])
+    e = O.RefEngine(start, cam_arr, gts, workers=cores, pipelined=True)
+    t = time.perf_counter()
+    e.run(steps)
+    dt = time.perf_counter() - t
+    del e
+    return {"value": steps / dt, "unit": "iters/s", "cores": cores, "kind": "reference",
+            "sample": f"{steps} full OffloadEngine iteration(s) of the same {a.n}-Gaussian {a.width}x{a.height} "
+                      f"workload (camera 0), pipelined, workers={cores}; scene setup excluded",
+            "seconds": dt}
+
+
+def run_reference(a, rank, world):
+    """--impl reference: the reference CPU engine on the same workload, rank 0 only."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracles as O
+
+    import paper_2509_15645_b200 as G
+
+    if rank != 0:
+        return None
+    if O.ref() is None:
+        return {"impl": "reference", "unavailable": "oracle/_ref/libgss_ref.so not built (needs /root/reference)"}
+    cfg = scene_config(a.n, a.width, a.height, a.cams, a.seed)
+    truth, cams = G.synth_scene_params(cfg)
+    cam_arr = np.stack([O.cam_from_struct(c) for c in cams])
+    # Identical inputs to our arm: GT rendered by our (bit-exact) forward when a GPU is present,
+    # else by the reference renderer itself.
+    gts = ref_gts(O, truth, cam_arr, a)
+    start = training_start(truth)
+    cores = os.cpu_count() or 1
+    e = O.RefEngine(start, cam_arr, gts, workers=cores, pipelined=True)
+    w = min(a.warmup, 1)
+    if w:
+        e.run(w)
+    k = min(a.steps, a.ref_max_steps)
+    t = time.perf_counter()
+    e.run(k)
+    dt = time.perf_counter() - t
+    v = k / dt
+    return {"metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": world, "steps": k, "warmup": w,
+            "ms_per_step": dt / k * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (reference synth_scene generator)", "impl": "reference",
+            "config": {"workload": f"C2: synthetic {a.n // 1_000_000}M Gaussians, {a.width}x{a.height} views, "
+                                   "all state in host RAM (CPU reference), pipelined, deferred Adam defer_max=15",
+                       "n_gaussians": a.n, "width": a.width, "height": a.height, "cams": a.cams,
+                       "requested_steps": a.steps, "requested_warmup": a.warmup},
+            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cores, "kind": "reference",
+                             "sample": f"{k} full OffloadEngine iterations of the workload after {w} warm-up"},
+            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def ref_gts(O, truth, cam_arr, a):
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            import paper_2509_15645_b200 as G
+
+            td = torch.from_numpy(truth).cuda()
+            cams = [G.camera_from_bytes(c.tobytes()) for c in cam_arr]
+            return np.stack([G.render_view(td, c, 3).cpu().numpy() for c in cams])
+    except Exception:
+        pass
+    return np.stack([O.ref_render_view(truth, c, 3) for c in cam_arr]) if hasattr(O, "ref_render_view") else \
+        np.zeros((len(cam_arr), a.height, a.width, 3), np.float32)
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        import torch.distributed as dist
+
+        backend = "nccl" if a.impl == "ours" else "gloo"
+        dist.init_process_group(backend)
+    if a.impl == "reference":
+        out = run_reference(a, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    out, (hbm, src), (cams, gts, start) = run_ours(a, rank, world)
+    if rank == 0:
+        k = out["kernels"][0]
+        out["culled_per_s"] = k["culled_per_s"]
+        out["roofline"] = {"bound": "hbm", "kernel": k["kernel"], "achieved": k["gbs"], "peak": hbm,
+                           "peak_source": src, "unit": "GB/s", "frac": k["gbs"] / hbm, "traffic": None}
+        if not a.no_cpu_baseline and world == 1:
+            out["cpu_baseline"] = cpu_baseline(cams, gts, start, a)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -73,12 +73,14 @@ __device__ __forceinline__ int classify(const CullArgs& a, const float* g) {
   const float* W = c.m;
   const float m00 = j00 * W[0] + j02 * W[6], m01 = j00 * W[1] + j02 * W[7], m02 = j00 * W[2] + j02 * W[8];
   const float m10 = j11 * W[3] + j12 * W[6], m11 = j11 * W[4] + j12 * W[7], m12 = j11 * W[5] + j12 * W[8];
-  const float mm = fmaxf(fmaxf(fmaxf(fabsf(m00), fabsf(m01)), fmaxf(fabsf(m02), fabsf(m10))),
-                         fmaxf(fabsf(m11), fabsf(m12)));
-  const float qa = fmaxf(fmaxf(fabsf(g[6]), fabsf(g[7])), fmaxf(fabsf(g[8]), fabsf(g[9])));
+  // fmaxf drops NaN operands, so finiteness is tested per component (a NaN compares false).
+  const bool mfin = fabsf(m00) <= 1e8f && fabsf(m01) <= 1e8f && fabsf(m02) <= 1e8f && fabsf(m10) <= 1e8f &&
+                    fabsf(m11) <= 1e8f && fabsf(m12) <= 1e8f;
+  const bool qfin = fabsf(g[6]) <= 3.0e38f && fabsf(g[7]) <= 3.0e38f && fabsf(g[8]) <= 3.0e38f &&
+                    fabsf(g[9]) <= 3.0e38f;
   // Finite-covariance certificate: finite quaternion, log-scales <= 20, |J W| <= 1e8, lp in
   // [0, 1e30]: then |cov| < 1e35, so lmax is finite or +inf and the radius is never NaN.
-  const bool certified = (mm <= 1e8f) && (qa <= 3.0e38f) && (g[3] <= 20.0f) && (g[4] <= 20.0f) &&
+  const bool certified = mfin && qfin && (g[3] <= 20.0f) && (g[4] <= 20.0f) &&
                          (g[5] <= 20.0f) && (a.lp >= 0.0f) && (a.lp <= 1e30f) && (fabsf(mx) <= 1e30f) &&
                          (fabsf(my) <= 1e30f);
   if (!certified) return 2;
@@ -224,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, 2) cull_kernel(const __grid_constant
     }
     __syncthreads();  // stage s, keep[], words[] free again
     if (tid == 0) issue(s);
+    if (!kTma) __syncthreads();  // single stage: stage_tile[0] is re-read at the top
   }
 }
 

@@ -782,10 +782,11 @@ void loss_l1(const float* image, const float* gt, int64_t elems, int64_t normali
 void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int64_t gstride, float* gn,
                         int64_t nstride, float* mean2d, cudaStream_t st) {
   require(ctx && ctx->have_forward, "rasterize_backward: no forward result in this context");
-  require(gg && gn && gstride >= 10 && nstride >= 49, "rasterize_backward: bad gradient buffers");
+  require(gstride >= 10 && nstride >= 49, "rasterize_backward: bad gradient strides");
   const Win& w = ctx->win;
   const int64_t V = ctx->V, I = ctx->I;
   if (V == 0) return;
+  require(gg && gn, "rasterize_backward: null gradient buffers");
   const int64_t npix = (int64_t)w.pw * w.ph;
   require(npix == 0 || d_img, "rasterize_backward: null d_img");
   const SplatRec* recs = static_cast<const SplatRec*>(ctx->recs.p);
