@@ -260,7 +260,7 @@ def kernel_probe(G, truth, cams, dev, a):
     ids = torch.empty(n, dtype=torch.int32, device=dev)
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
     wsb = int(L.gss_cull_workspace_bytes(n))
-    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
     vp = G.viewport_full(a.width, a.height)
     cam0 = cams[0]
 

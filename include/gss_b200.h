@@ -87,7 +87,9 @@ int64_t gss_launch_count(void);
 int gss_expf_device(const float* x, float* y, int64_t n, gss_stream_t stream);
 
 /* ---- frustum cull (render.hpp:243-260 cull_keep / frustum_cull) ---------------------------- */
-/* Workspace for n Gaussians (look-back tile states + ticket). */
+/* Workspace for n Gaussians (per-tile look-back states). It must be zero-filled once
+ * before its first use; every call leaves it ready for the next one (no per-call memset). One
+ * workspace must not be used by two calls in flight at the same time. */
 size_t gss_cull_workspace_bytes(int64_t n);
 /* ids_out: capacity n, receives the kept ids ascending (bit-exact with frustum_cull);
  * mask_opt: optional bit mask, ceil(n/32) words, bit i of word i/32 = kept(i);

@@ -469,6 +469,7 @@ gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss
   GSS_CUDA(cudaHostAlloc((void**)&e->count_host, 3 * sizeof(int64_t), cudaHostAllocDefault));
   e->cull_ws_bytes = cull_workspace_bytes(n);
   e->cull_ws = dmalloc<char>(e->cull_ws_bytes);
+  GSS_CUDA(cudaMemsetAsync(e->cull_ws, 0, e->cull_ws_bytes, e->sD));  // zero once (gss_cull contract)
   e->accum_norm = dmalloc<double>(nn);
   e->accum_cnt = dmalloc<int32_t>(nn);
   GSS_CUDA(cudaMemsetAsync(e->accum_norm, 0, nn * 8, e->sD));

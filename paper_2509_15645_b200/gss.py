@@ -94,7 +94,7 @@ def frustum_cull(geo: torch.Tensor, count: int, cam: GssCamera, vp: GssViewport,
     dev = geo.device
     ids = torch.empty(max(count, 1), dtype=torch.int32, device=dev)
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-    ws = torch.empty(cull_workspace_bytes(count), dtype=torch.uint8, device=dev)
+    ws = torch.zeros(cull_workspace_bytes(count), dtype=torch.uint8, device=dev)
     mask = torch.empty(max((count + 31) // 32, 1), dtype=torch.int32, device=dev) if want_mask else None
     check(lib().gss_cull(_ptr(geo), int(count), int(stride), C.byref(cam), C.byref(vp), float(low_pass), _ptr(mask),
                          _ptr(ids), _ptr(cnt), _ptr(ws), ws.numel(), _stream(stream)))

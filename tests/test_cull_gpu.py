@@ -128,3 +128,38 @@ def test_synth_c1_scene_bit_exact(ref):
         ca = O.cam_from_struct(c)
         ids, _, _ = gpu_cull(geo, ca, [0, 256, 0, 256])
         assert np.array_equal(ids, O.ref_cull(geo, ca, [0, 256, 0, 256]))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_border_stress_bit_exact(ref, seed):
+    """Centres placed within a few ulps..pixels of the viewport borders (where the fast
+    classifier's error margins decide), scales spanning the radius bound, random cameras
+    including non-orthonormal rotations and low-pass values 0 / 0.3 / 10."""
+    rng = np.random.default_rng(100 + seed)
+    n = 200_000
+    W_, H_ = 640, 360
+    cam = O.look_at(list(rng.uniform(-3, 3, 3)), list(rng.uniform(-0.5, 0.5, 3)), float(rng.uniform(200, 900)),
+                    float(rng.uniform(200, 900)), W_, H_, 0.05, 30.0)
+    if seed % 2 == 1:  # perturb the rotation (no longer orthonormal)
+        cam = cam.copy()
+        cam[:9] = cam[:9] * rng.uniform(0.7, 1.3, 9).astype(np.float32)
+    rot = cam[:9].reshape(3, 3).astype(np.float64)
+    t = cam[9:12].astype(np.float64)
+    fx, fy, cx, cy = [float(v) for v in cam[12:16]]
+    # sample pixel targets near the borders, then back-project at random depths
+    u = np.where(rng.random(n) < 0.5, rng.choice([0.0, W_], n) + rng.normal(0, 3, n), rng.uniform(-50, W_ + 50, n))
+    v = np.where(rng.random(n) < 0.5, rng.choice([0.0, H_], n) + rng.normal(0, 3, n), rng.uniform(-50, H_ + 50, n))
+    z = rng.uniform(0.1, 20.0, n)
+    pc = np.stack([(u - cx) / fx * z, (v - cy) / fy * z, z], 1)
+    pw = np.linalg.solve(rot, (pc - t).T).T
+    rows = np.zeros((n, 10), np.float32)
+    rows[:, 0:3] = pw
+    rows[:, 3:6] = rng.uniform(-9, -1, (n, 3))
+    q = rng.normal(size=(n, 4))
+    rows[:, 6:10] = q / np.linalg.norm(q, axis=1, keepdims=True) * rng.choice([1.0, 1e-13, 7.0], (n, 1))
+    for lp in (0.3, 0.0, 10.0):
+        for vp in ([0, W_, 0, H_], [0.25, W_ - 0.5, 1.0, H_ * 0.5]):
+            ids, mask, _ = gpu_cull(rows, cam, vp, low_pass=lp)
+            want = O.ref_cull(rows, cam, vp, low_pass=lp)
+            assert np.array_equal(ids, want), (lp, vp, np.setxor1d(ids, want)[:10])
+            assert np.array_equal(mask, mask_from_ids(want, n))
