@@ -59,6 +59,20 @@ void require_device() {
     cudaGetLastError();
     throw Error(GSS_ERR_CUDA, "no CUDA device: libgss_b200 has no CPU fallback");
   }
+  // The kernels' scratch comes from the stream-ordered pool; keep freed blocks cached in the pool
+  // (the default release threshold 0 returns them to the driver at every sync, turning each
+  // scratch allocation into a full device allocation).
+  static thread_local int pooled_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && dev != pooled_dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    pooled_dev = dev;
+  }
 }
 }  // namespace
 

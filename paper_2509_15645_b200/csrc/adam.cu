@@ -116,14 +116,22 @@ __device__ __forceinline__ int64_t lower_bound_ids(const int32_t* ids, int64_t n
   return lo;
 }
 
+// IEEE round-to-nearest n / d. A zero numerator (most elements of a sparse step: delay-0 rows
+// have w_scale = 0, untouched rows have m = v = 0) sends CUDA's division into its slow path;
+// its exact result is a signed zero (sign = sign(n) ^ sign(d)) for any nonzero, non-NaN d.
+__device__ __forceinline__ float div_rn(float n, float d) {
+  if (n == 0.0f && d == d && d != 0.0f) return __int_as_float((__float_as_int(n) ^ __float_as_int(d)) & 0x80000000);
+  return __fdiv_rn(n, d);
+}
+
 // deferred_scalar (adam.hpp:102-110)
 __device__ __forceinline__ void deferred_scalar(float& w, float& m, float& v, float g, float ws, float ms, float vs,
                                                 const float* sc) {
   const float m_new = ms * m + sc[0] * g;
   const float v_new = vs * v + sc[1] * g * g;
-  w -= (ws * m) / (sqrtf(v) + sc[4]);
-  const float denom = sqrtf(v_new) / sc[2] + sc[4];
-  w = w - sc[3] * m_new / denom;
+  w -= div_rn(ws * m, sqrtf(v) + sc[4]);
+  const float denom = div_rn(sqrtf(v_new), sc[2]) + sc[4];
+  w = w - div_rn(sc[3] * m_new, denom);
   m = m_new;
   v = v_new;
 }
@@ -149,21 +157,49 @@ template <int K> __device__ void load_luts(SmemLuts<K>& s, const LutArgs<K>& L, 
 
 enum Mode : int { kDeferred = 0, kFlush = 1 };
 
+// Block index of a sorted id list: bstart[b] = lower_bound(ids, b * kRowsPerBlock) for
+// b = 0 .. nblocks (so a 1024-row block finds its gradient ids with two loads instead of a
+// dependent binary search), plus the reference's invariant on the list (adam.hpp:231): strictly
+// ascending ids in [0, n) — a violation sets bit 0 of the arena's error flag.
+__global__ void index_kernel(const int32_t* ids, int64_t count, const int64_t* count_dev, int64_t n, int nblocks,
+                             int32_t* bstart, int* err_flag) {
+  const int64_t V = count_dev ? *count_dev : count;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= V; k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t hi_b = nblocks;  // blocks b with ids[k-1] < b*R <= ids[k] start at k
+    if (k < V) {
+      const int32_t id = ids[k];
+      if (id < 0 || (int64_t)id >= n || (k > 0 && ids[k - 1] >= id)) atomicOr(err_flag, 1);
+      hi_b = id < 0 ? -1 : (int64_t)id / kRowsPerBlock;
+    }
+    int64_t lo_b = 0;
+    if (k > 0) {
+      const int32_t pid = ids[k - 1];
+      lo_b = pid < 0 ? 0 : (int64_t)pid / kRowsPerBlock + 1;
+    }
+    if (hi_b > nblocks) hi_b = nblocks;
+    for (int64_t b = lo_b; b <= hi_b; ++b) bstart[b] = (int32_t)k;
+  }
+}
+
 // One pass of deferred_update (adam.hpp:211-238) or flush_deferred (adam.hpp:293-313) over
-// rows [blockIdx*1024, +1024). Dense Adam (adam.hpp:198-207) is the deferred pass of an arena
-// whose counters stay 0 with defer_max 0 (every row saturated, delay 0).
-template <int K, int MODE>
-__global__ void __launch_bounds__(kUpdThreads) update_kernel(ArenaDev a, GradsDev gr,
+// rows [blockIdx*1024, +1024). DENSE: an arena with defer_max 0 (the geometric tier,
+// store.hpp:121-124) — every row is touched at delay 0 and counters stay 0, so the pass is a
+// contiguous vectorised stream over the block's rows (float4 loads/stores of w, m, v).
+struct TouchList {  // rows a deferred pass touches (unordered; each row at most once)
+  int32_t* row;
+  int32_t* slot;
+  uint8_t* del;
+  unsigned long long* count;
+};
+
+template <int K, int MODE, bool DENSE>
+__global__ void __launch_bounds__(kUpdThreads) update_kernel(ArenaDev a, GradsDev gr, const int32_t* bstart,
                                                              const __grid_constant__ LutArgs<K> L,
                                                              uint32_t* touched_mask, int64_t* touched_count,
-                                                             int* err_flag) {
+                                                             int* err_flag, TouchList tl) {
   __shared__ SmemLuts<K> lut;
   __shared__ int32_t slot_of[kRowsPerBlock];
-  __shared__ uint16_t trow[kRowsPerBlock];
-  __shared__ uint8_t tdel[kRowsPerBlock];
-  __shared__ int32_t tslot[kRowsPerBlock];
   __shared__ int warp_tot[kUpdThreads / 32];
-  __shared__ long long g_lo, g_hi;
   __shared__ int ntouched;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -171,52 +207,91 @@ __global__ void __launch_bounds__(kUpdThreads) update_kernel(ArenaDev a, GradsDe
   const int nrows = (int)((a.n - r0) < kRowsPerBlock ? (a.n - r0) : kRowsPerBlock);
   load_luts<K>(lut, L, a.dim);
   for (int i = tid; i < kRowsPerBlock; i += kUpdThreads) slot_of[i] = -1;
-  const int64_t gcount = MODE == kDeferred ? grads_count(gr) : 0;
-  if (MODE == kDeferred && tid < 2 && gr.ids) {
-    const int64_t b = lower_bound_ids(gr.ids, gcount, r0 + (tid == 0 ? 0 : kRowsPerBlock));
-    if (tid == 0) g_lo = b; else g_hi = b;
-  }
   __syncthreads();
   if (MODE == kDeferred && gr.ids) {
-    const int64_t lo = g_lo, hi = g_hi;
-    for (int64_t k = lo + tid; k < hi; k += kUpdThreads) {
+    // Clamped: an invalid id list (flagged by index_kernel) may leave entries unset.
+    const int64_t gcount = grads_count(gr);
+    const int lo = max(0, bstart[blockIdx.x]), hi = (int)min((int64_t)bstart[blockIdx.x + 1], gcount);
+    for (int k = lo + tid; k < hi; k += kUpdThreads) {
       const int64_t local = (int64_t)gr.ids[k] - r0;
-      if (local >= 0 && local < kRowsPerBlock) slot_of[local] = (int32_t)k;
-    }
-    // Sortedness / range invariant (adam.hpp:231): this block checks its share of the id list.
-    const int64_t per = (gcount + gridDim.x - 1) / gridDim.x;
-    const int64_t k0 = (int64_t)blockIdx.x * per, k1 = (gcount < k0 + per ? gcount : k0 + per);
-    for (int64_t k = k0 + tid; k < k1; k += kUpdThreads) {
-      const int32_t id = gr.ids[k];
-      if (id < 0 || (int64_t)id >= a.n || (k + 1 < gcount && gr.ids[k + 1] <= id)) atomicOr(err_flag, 1);
+      if (local >= 0 && local < kRowsPerBlock) slot_of[local] = k;
     }
   }
   __syncthreads();
-  // Counter pass: 4 consecutive rows per thread.
+  const int dim = a.dim;
+  if (DENSE) {
+    // Every row at delay 0 (w_scale = 0: the restoration term is w - (+-0), kept exactly);
+    // counters untouched (they stay 0 under defer_max 0). Lane-fixed columns: lanes 0..rpp*dim-1
+    // of a warp cover rpp consecutive rows, so each lane's column group and constants live in
+    // registers and every warp access is one contiguous span.
+    const int rpp = 32 / dim;  // rows per warp pass
+    const int rr = lane / dim, c = lane - rr * dim;
+    const bool act = rr < rpp;
+    const int g = act ? lut.col_group[c] : 0;
+    const float ms = lut.a1[g][0], vs = lut.a2[g][0];
+    const float s0 = lut.sc[g][0], s1 = lut.sc[g][1], s2 = lut.sc[g][2], s3 = lut.sc[g][3], s4 = lut.sc[g][4];
+    const int npass = (nrows + rpp - 1) / rpp;
+#pragma unroll 4
+    for (int p = warp; p < npass; p += kUpdThreads / 32) {
+      const int lr = p * rpp + rr;
+      if (!act || lr >= nrows) continue;
+      const size_t off = (size_t)(r0 + lr) * dim + c;
+      float w = a.w[off], m = a.m[off], v = a.v[off];
+      const int sl = slot_of[lr];
+      const float gv = sl >= 0 ? gr.rows[(size_t)sl * gr.stride + gr.col0 + c] : 0.0f;
+      const float m_new = ms * m + s0 * gv;
+      const float v_new = vs * v + s1 * gv * gv;
+      // (0 * m) / (sqrt(v) + eps) is (0 * m) itself whenever v >= 0 (denominator >= eps > 0).
+      const float num = 0.0f * m;
+      w = v >= 0.0f ? w - num : w - div_rn(num, sqrtf(v) + s4);
+      const float denom = div_rn(sqrtf(v_new), s2) + s4;
+      w = w - div_rn(s3 * m_new, denom);
+      a.w[off] = w;
+      a.m[off] = m_new;
+      a.v[off] = v_new;
+    }
+    if (touched_count && tid == 0 && nrows > 0)
+      atomicAdd((unsigned long long*)touched_count, (unsigned long long)nrows);
+    if (touched_mask) {
+      for (int wi = tid; wi * 32 < nrows; wi += kUpdThreads) {
+        const int rem = nrows - wi * 32;
+        touched_mask[(r0 >> 5) + wi] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+      }
+    }
+    return;
+  }
+  // Counter pass: 4 consecutive rows per thread (one 32-bit load/store of counters).
   int my_cnt = 0;
   uint8_t del[4];
   bool tch[4];
+  const bool vec_cnt = nrows == kRowsPerBlock && ((reinterpret_cast<uintptr_t>(a.counter + r0) & 3) == 0);
+  uint32_t cw = 0, cw_new = 0;
+  if (vec_cnt) cw = reinterpret_cast<const uint32_t*>(a.counter + r0)[tid];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int r = tid * 4 + j;
     tch[j] = false;
     del[j] = 0;
     if (r < nrows) {
-      const uint8_t c = a.counter[r0 + r];
+      const uint8_t c = vec_cnt ? (uint8_t)(cw >> (8 * j)) : a.counter[r0 + r];
       if (c > a.defer_max) atomicOr(err_flag, 2);  // check_counters (adam.hpp:154-158)
       bool t;
+      uint8_t cn;
       if (MODE == kDeferred) {
         t = slot_of[r] >= 0 || c == a.defer_max;
-        a.counter[r0 + r] = t ? 0 : (uint8_t)(c + 1);
+        cn = t ? 0 : (uint8_t)(c + 1);
       } else {
         t = c != 0;
-        if (t) a.counter[r0 + r] = 0;
+        cn = 0;
       }
+      cw_new |= (uint32_t)cn << (8 * j);
+      if (!vec_cnt && cn != c) a.counter[r0 + r] = cn;
       tch[j] = t;
       del[j] = c;
       my_cnt += t;
     }
   }
+  if (vec_cnt && cw_new != cw) reinterpret_cast<uint32_t*>(a.counter + r0)[tid] = cw_new;
   // Block exclusive scan of touched counts (ascending row order).
   int inc = my_cnt;
 #pragma unroll
@@ -236,14 +311,23 @@ __global__ void __launch_bounds__(kUpdThreads) update_kernel(ArenaDev a, GradsDe
     ntouched = run;
   }
   __syncthreads();
-  int pos = warp_tot[warp] + inc - my_cnt;
+  __shared__ unsigned long long gbase_s;
+  if (tid == 0) {
+    const int T = ntouched;
+    gbase_s = T > 0 ? atomicAdd(tl.count, (unsigned long long)T) : 0ull;
+    if (touched_count && T > 0) atomicAdd((unsigned long long*)touched_count, (unsigned long long)T);
+  }
+  __syncthreads();
+  // Append this block's touched rows (ascending within the block) to the pass's touch list; the
+  // walk kernel then streams the list with every warp busy (no per-block serial prologue).
+  int64_t pos = (int64_t)gbase_s + warp_tot[warp] + inc - my_cnt;
 #pragma unroll
   for (int j = 0; j < 4; ++j)
     if (tch[j]) {
       const int r = tid * 4 + j;
-      trow[pos] = (uint16_t)r;
-      tdel[pos] = del[j];
-      tslot[pos] = slot_of[r];
+      tl.row[pos] = (int32_t)(r0 + r);
+      tl.del[pos] = del[j];
+      tl.slot[pos] = MODE == kDeferred ? slot_of[r] : -1;
       ++pos;
     }
   if (touched_mask) {
@@ -262,87 +346,169 @@ __global__ void __launch_bounds__(kUpdThreads) update_kernel(ArenaDev a, GradsDe
       if (lane == 0 && wrow < a.n) touched_mask[wrow >> 5] = word;
     }
   }
+}
+
+// Streams a touch list: warp per row, lanes on consecutive columns (lane-fixed column groups);
+// each warp takes kRB rows at a time and issues all their loads before any math.
+template <int K, int MODE>
+__global__ void __launch_bounds__(kUpdThreads, 4) walk_kernel(ArenaDev a, GradsDev gr, const __grid_constant__ LutArgs<K> L,
+                                                           TouchList tl) {
+  __shared__ SmemLuts<K> lut;
+  load_luts<K>(lut, L, a.dim);
   __syncthreads();
-  const int T = ntouched;
-  if (touched_count && tid == 0 && T > 0) atomicAdd((unsigned long long*)touched_count, (unsigned long long)T);
+  const int lane = threadIdx.x & 31;
+  const int64_t T = (int64_t)*tl.count;
   const int dim = a.dim;
-  const int total = T * dim;
-  // Flattened (touched row, column) walk: consecutive lanes take consecutive columns.
-#pragma unroll 4
-  for (int f = tid; f < total; f += kUpdThreads) {
-    const int t = (int)__umulhi((uint32_t)f, a.div_magic);
-    const int c = f - t * dim;
-    const int64_t row = r0 + trow[t];
-    const int d = tdel[t];
-    const int g = lut.col_group[c];
-    const size_t off = (size_t)row * dim + c;
-    float w = a.w[off], m = a.m[off], v = a.v[off];
-    if (MODE == kDeferred) {
-      const int s = tslot[t];
-      const float gv = s >= 0 ? gr.rows[(size_t)s * gr.stride + gr.col0 + c] : 0.0f;
-      deferred_scalar(w, m, v, gv, lut.param[g][d], lut.a1[g][d], lut.a2[g][d], lut.sc[g]);
-      a.w[off] = w;
-      a.m[off] = m;
-      a.v[off] = v;
-    } else {
-      a.w[off] = w - (lut.param[g][d] * m) / (sqrtf(v) + lut.sc[g][4]);  // restore_scalar (adam.hpp:112-114)
-      a.m[off] = m * lut.a1[g][d];
-      a.v[off] = v * lut.a2[g][d];
+  constexpr int kRB = 4;
+  const int npass = (dim + 31) >> 5;
+  const int64_t wstride = (int64_t)gridDim.x * (kUpdThreads / 32) * kRB;
+  for (int64_t t0 = ((int64_t)blockIdx.x * (kUpdThreads / 32) + (threadIdx.x >> 5)) * kRB; t0 < T; t0 += wstride) {
+    int64_t rbase[kRB];
+    int d[kRB], sl[kRB];
+#pragma unroll
+    for (int u = 0; u < kRB; ++u) {
+      const bool ok = t0 + u < T;
+      rbase[u] = ok ? (int64_t)tl.row[t0 + u] * dim : -1;
+      d[u] = ok ? tl.del[t0 + u] : 0;
+      sl[u] = (ok && MODE == kDeferred) ? tl.slot[t0 + u] : -1;
+    }
+    for (int p = 0; p < npass; ++p) {
+      const int c = p * 32 + lane;
+      const bool cok = c < dim;
+      const int g = cok ? lut.col_group[c] : 0;
+      float w[kRB], m[kRB], v[kRB], gv[kRB];
+#pragma unroll
+      for (int u = 0; u < kRB; ++u) {
+        const bool ok = cok && rbase[u] >= 0;
+        const size_t off = ok ? (size_t)(rbase[u] + c) : 0;
+        w[u] = ok ? a.w[off] : 0.0f;
+        m[u] = ok ? a.m[off] : 0.0f;
+        v[u] = ok ? a.v[off] : 0.0f;
+        gv[u] = (cok && sl[u] >= 0) ? gr.rows[(size_t)sl[u] * gr.stride + gr.col0 + c] : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < kRB; ++u) {
+        if (!(cok && rbase[u] >= 0)) continue;
+        const size_t off = (size_t)(rbase[u] + c);
+        if (MODE == kDeferred) {
+          deferred_scalar(w[u], m[u], v[u], gv[u], lut.param[g][d[u]], lut.a1[g][d[u]], lut.a2[g][d[u]], lut.sc[g]);
+          a.w[off] = w[u];
+          a.m[off] = m[u];
+          a.v[off] = v[u];
+        } else {
+          a.w[off] = w[u] - div_rn(lut.param[g][d[u]] * m[u], sqrtf(v[u]) + lut.sc[g][4]);  // adam.hpp:112-114
+          a.m[off] = m[u] * lut.a1[g][d[u]];
+          a.v[off] = v[u] * lut.a2[g][d[u]];
+        }
+      }
     }
   }
 }
 
-// restore_view (adam.hpp:252-289): out[k] = restored row ids[k] (+ pending pass). Persistent
-// grid-stride over 128-id chunks; per chunk, one thread per id resolves (id, delay, pending
-// slot) by binary search, then the flattened (id, column) walk reads the arena rows.
-constexpr int kRestoreChunk = 128;
+// restore_view (adam.hpp:252-289): out[k] = restored row ids[k] (+ pending pass). Grid-stride
+// over 256-id chunks; per chunk each thread resolves one (id, delay, pending slot): the pending
+// ids of the chunk's row span are staged in SMEM through the pending list's block index, so the
+// slot is a binary search in SMEM instead of a dependent search through global memory. Then the
+// flattened (id, column) walk reads the arena rows with consecutive lanes on consecutive columns.
+constexpr int kRestoreChunk = kUpdThreads;
+constexpr int kSeg = 2048;
 template <int K>
-__global__ void __launch_bounds__(kUpdThreads) restore_kernel(ArenaDev a, const int32_t* ids, int64_t count,
+__global__ void __launch_bounds__(kUpdThreads, 4) restore_kernel(ArenaDev a, const int32_t* ids, int64_t count,
                                                               const int64_t* count_dev, GradsDev pend,
-                                                              int has_pending, const __grid_constant__ LutArgs<K> L,
-                                                              float* out) {
+                                                              const int32_t* pbstart, int has_pending,
+                                                              const __grid_constant__ LutArgs<K> L, float* out) {
   __shared__ SmemLuts<K> lut;
   __shared__ int32_t cid[kRestoreChunk];
   __shared__ uint8_t cdel[kRestoreChunk];
   __shared__ int32_t cslot[kRestoreChunk];
+  __shared__ int32_t seg[kSeg];
+  __shared__ int seg_lo, seg_n;
   load_luts<K>(lut, L, a.dim);
   const int64_t cnt = count_dev ? *count_dev : count;
   const int64_t pcnt = has_pending ? grads_count(pend) : 0;
+  const int nblk = (int)((a.n + kRowsPerBlock - 1) / kRowsPerBlock);
   const int dim = a.dim;
+  const int tid = threadIdx.x;
   for (int64_t k0 = (int64_t)blockIdx.x * kRestoreChunk; k0 < cnt; k0 += (int64_t)gridDim.x * kRestoreChunk) {
     const int nk = (int)((cnt - k0) < kRestoreChunk ? (cnt - k0) : kRestoreChunk);
     __syncthreads();
-    if (threadIdx.x < nk) {
-      const int32_t id = ids[k0 + threadIdx.x];
-      cid[threadIdx.x] = id;
-      cdel[threadIdx.x] = a.counter[id];
-      int32_t s = -1;
-      if (has_pending && pend.ids) {
-        const int64_t p = lower_bound_ids(pend.ids, pcnt, id);
-        if (p < pcnt && pend.ids[p] == id) s = (int32_t)p;
-      }
-      cslot[threadIdx.x] = s;
+    int32_t id = 0;
+    if (tid < nk) {
+      id = ids[k0 + tid];
+      cid[tid] = id;
+      cdel[tid] = a.counter[id];
+    }
+    if (has_pending && pend.ids && tid == 0) {
+      const int64_t lo_row = ids[k0], hi_row = ids[k0 + nk - 1];
+      int64_t b0 = lo_row / kRowsPerBlock, b1 = hi_row / kRowsPerBlock + 1;
+      b0 = b0 < 0 ? 0 : (b0 > nblk ? nblk : b0);
+      b1 = b1 < 0 ? 0 : (b1 > nblk ? nblk : b1);
+      int64_t p0 = pbstart[b0], p1 = pbstart[b1];
+      p0 = p0 < 0 ? 0 : p0;
+      p1 = p1 > pcnt ? pcnt : p1;
+      seg_lo = (int)p0;
+      seg_n = p1 > p0 ? (int)(p1 - p0) : 0;
     }
     __syncthreads();
-    const int total = nk * dim;
-#pragma unroll 4
-    for (int f = threadIdx.x; f < total; f += kUpdThreads) {
-      const int t = (int)__umulhi((uint32_t)f, a.div_magic);
-      const int c = f - t * dim;
-      const size_t off = (size_t)cid[t] * dim + c;
-      const int d = cdel[t];
-      const int g = lut.col_group[c];
-      float w = a.w[off];
-      const float m = a.m[off], v = a.v[off];
-      if (has_pending) {
-        float mm = m, vv = v;
-        const int s = cslot[t];
-        const float gv = s >= 0 ? pend.rows[(size_t)s * pend.stride + pend.col0 + c] : 0.0f;
-        deferred_scalar(w, mm, vv, gv, lut.param[g][d], lut.a1[g][d], lut.a2[g][d], lut.sc[g]);
-      } else {
-        w = w - (lut.param[g][d] * m) / (sqrtf(v) + lut.sc[g][4]);
+    if (has_pending && pend.ids) {
+      const int sn = seg_n, sl = seg_lo;
+      const bool staged = sn <= kSeg;
+      if (staged)
+        for (int i = tid; i < sn; i += kUpdThreads) seg[i] = pend.ids[sl + i];
+      __syncthreads();
+      if (tid < nk) {
+        int32_t s = -1;
+        if (staged) {
+          int lo = 0, hi = sn;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (seg[mid] < id) lo = mid + 1; else hi = mid;
+          }
+          if (lo < sn && seg[lo] == id) s = sl + lo;
+        } else {
+          const int64_t p = sl + lower_bound_ids(pend.ids + sl, sn, id);
+          if (p < sl + sn && pend.ids[p] == id) s = (int32_t)p;
+        }
+        cslot[tid] = s;
       }
-      out[(size_t)(k0 + t) * dim + c] = w;
+    }
+    __syncthreads();
+    // Warp per id, lanes on consecutive columns; kRB ids per warp with all loads issued first.
+    constexpr int kRB = 4;
+    const int npass = (dim + 31) >> 5;
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int t0 = warp * kRB; t0 < nk; t0 += (kUpdThreads / 32) * kRB) {
+      for (int p = 0; p < npass; ++p) {
+        const int c = p * 32 + lane;
+        const bool cok = c < dim;
+        const int g = cok ? lut.col_group[c] : 0;
+        float w[kRB], m[kRB], v[kRB], gv[kRB];
+#pragma unroll
+        for (int u = 0; u < kRB; ++u) {
+          const int t = t0 + u;
+          const bool ok = cok && t < nk;
+          const size_t off = ok ? (size_t)cid[t] * dim + c : 0;
+          const int sl = (ok && has_pending) ? cslot[t] : -1;
+          w[u] = ok ? a.w[off] : 0.0f;
+          m[u] = ok ? a.m[off] : 0.0f;
+          v[u] = ok ? a.v[off] : 0.0f;
+          gv[u] = sl >= 0 ? pend.rows[(size_t)sl * pend.stride + pend.col0 + c] : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < kRB; ++u) {
+          const int t = t0 + u;
+          if (!(cok && t < nk)) continue;
+          const int d = cdel[t];
+          float ww = w[u];
+          if (has_pending) {
+            float mm = m[u], vv = v[u];
+            deferred_scalar(ww, mm, vv, gv[u], lut.param[g][d], lut.a1[g][d], lut.a2[g][d], lut.sc[g]);
+          } else {
+            ww = ww - div_rn(lut.param[g][d] * m[u], sqrtf(v[u]) + lut.sc[g][4]);
+          }
+          out[(size_t)(k0 + t) * dim + c] = ww;
+        }
+      }
     }
   }
 }
@@ -386,15 +552,63 @@ GradsDev grads_dev(const gss_sparse_grads* g) {
 // Per-arena device error flag (keyed by the counter buffer), allocated lazily.
 int* err_flag_for(const gss_arena& a);
 
+int sm_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    GSS_CUDA(cudaGetDevice(&dev));
+    GSS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return sms;
+}
+
+// Stream-ordered scratch for the block index of a sorted id list (nblocks + 1 entries).
+int32_t* build_index(const gss_arena& a, const GradsDev& g, int* err, cudaStream_t st) {
+  const int nblk = (int)ceil_div(a.n, kRowsPerBlock);
+  int32_t* bstart = nullptr;
+  GSS_CUDA(cudaMallocAsync((void**)&bstart, (size_t)(nblk + 1) * 4, st));
+  const int64_t cap = g.count_dev ? std::max<int64_t>(g.count, a.n) : g.count;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap + 1, 256), 148 * 16));
+  index_kernel<<<blocks, 256, 0, st>>>(g.ids, g.count, g.count_dev, a.n, nblk, bstart, err);
+  GSS_LAUNCHED();
+  return bstart;
+}
+
 template <int K, int MODE>
 void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* tmask, int64_t* tcount,
                    cudaStream_t st) {
   auto L = std::make_unique<LutArgs<K>>();
   std::memset(L.get(), 0, sizeof(LutArgs<K>));
   fill_luts<K>(a, t, MODE == kFlush, *L);
+  int* err = err_flag_for(a);
+  int32_t* bstart = nullptr;
+  if (MODE == kDeferred && gd.ids) bstart = build_index(a, gd, err, st);
   const int blocks = (int)ceil_div(a.n, kRowsPerBlock);
-  update_kernel<K, MODE><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, *L, tmask, tcount, err_flag_for(a));
-  GSS_LAUNCHED();
+  if (MODE == kDeferred && a.defer_max == 0 && a.dim <= 32) {
+    update_kernel<K, MODE, true><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, bstart, *L, tmask, tcount, err,
+                                                                  TouchList{});
+    GSS_LAUNCHED();
+  } else {
+    // Pass 1: counters + touch list; pass 2: stream the list.
+    TouchList tl;
+    const size_t n = (size_t)a.n;
+    char* buf = nullptr;
+    GSS_CUDA(cudaMallocAsync((void**)&buf, 16 + n * 9, st));
+    tl.count = reinterpret_cast<unsigned long long*>(buf);
+    tl.row = reinterpret_cast<int32_t*>(buf + 16);
+    tl.slot = tl.row + n;
+    tl.del = reinterpret_cast<uint8_t*>(tl.slot + n);
+    GSS_CUDA(cudaMemsetAsync(tl.count, 0, 8, st));
+    update_kernel<K, MODE, false><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, bstart, *L, tmask, tcount, err,
+                                                                   tl);
+    GSS_LAUNCHED();
+    const int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, (kUpdThreads / 32) * 4),
+                                                                    (int64_t)sm_count() * 4));
+    walk_kernel<K, MODE><<<wblocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, *L, tl);
+    GSS_LAUNCHED();
+    GSS_CUDA(cudaFreeAsync(buf, st));
+  }
+  if (bstart) GSS_CUDA(cudaFreeAsync(bstart, st));
 }
 
 struct IsSet {
@@ -533,21 +747,24 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
   GSS_CUDA(cudaGetDevice(&dev));
   GSS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int64_t cap = count_dev ? std::max<int64_t>(count, a.n) : count;
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kRestoreChunk), (int64_t)sms * 8));
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kRestoreChunk), (int64_t)sms * 4));
+  int32_t* pbstart = nullptr;
+  if (pending && pd.ids) pbstart = build_index(a, pd, err_flag_for(a), st);
   if (a.defer_max < 16) {
     auto L = std::make_unique<LutArgs<16>>();
     std::memset(L.get(), 0, sizeof(LutArgs<16>));
     fill_luts<16>(a, t, false, *L);
-    restore_kernel<16><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), ids, count, count_dev, pd, pending ? 1 : 0, *L,
-                                                       out);
+    restore_kernel<16><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), ids, count, count_dev, pd, pbstart,
+                                                       pending ? 1 : 0, *L, out);
   } else {
     auto L = std::make_unique<LutArgs<256>>();
     std::memset(L.get(), 0, sizeof(LutArgs<256>));
     fill_luts<256>(a, t, false, *L);
-    restore_kernel<256><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), ids, count, count_dev, pd, pending ? 1 : 0,
-                                                        *L, out);
+    restore_kernel<256><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), ids, count, count_dev, pd, pbstart,
+                                                        pending ? 1 : 0, *L, out);
   }
   GSS_LAUNCHED();
+  if (pbstart) GSS_CUDA(cudaFreeAsync(pbstart, st));
 }
 
 int arena_check(const gss_arena* ap, cudaStream_t st) {
