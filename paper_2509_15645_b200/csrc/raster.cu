@@ -326,43 +326,120 @@ __global__ void loss_final_kernel(const double* partials, int n, float inv, floa
   }
 }
 
-// Reverse sweep (render.hpp:542-589) per tile; one partial SlotAcc per (splat, tile) instance.
-// partial layout: [instance][9] = rgb3, m2d2, cov3, ab.
-__global__ void __launch_bounds__(kTilePix) backward_kernel(const SplatRec* __restrict__ recs,
-                                                            const int32_t* __restrict__ vals,
-                                                            const int2* __restrict__ ranges, Win w, float bg0,
-                                                            float bg1, float bg2, const float* __restrict__ fT_in,
-                                                            const int32_t* __restrict__ last_in,
-                                                            const float* __restrict__ d_img, float* partials) {
+// Reverse sweep state of one pixel (render.hpp:542-589).
+struct PixB {
+  float cx, cy, T, g0, g1, g2, s0, s1, s2;
+  int x, y, L;
+};
+
+// One contribution of splat r (sweep position jpos) to pixel p: accumulates its 9 screen-space
+// gradient terms into v and steps the pixel's reverse state. Returns whether it contributed.
+__device__ __forceinline__ bool bwd_contrib(const SplatRec& r, int jpos, PixB& p, float v[9]) {
+  if (!(jpos < p.L && p.x >= r.bx0 && p.x < r.bx1 && p.y >= r.by0 && p.y < r.by1)) return false;
+  const EvalOut ev = contrib_eval(r, p.cx, p.cy);
+  const float alpha = ev.alpha;
+  const float inv1m = 1.0f / (1.0f - alpha);
+  const float Tb = p.T * inv1m;  // transmittance before this contribution
+  const float w_rgb = alpha * Tb;
+  v[0] += w_rgb * p.g0;
+  v[1] += w_rgb * p.g1;
+  v[2] += w_rgb * p.g2;
+  const float dot_c = r.r * p.g0 + r.g * p.g1 + r.bl * p.g2;
+  const float dot_suf = p.s0 * p.g0 + p.s1 * p.g1 + p.s2 * p.g2;
+  const float d_alpha = Tb * dot_c - dot_suf * inv1m;
+  p.s0 += r.r * w_rgb;
+  p.s1 += r.g * w_rgb;
+  p.s2 += r.bl * w_rgb;
+  p.T = Tb;
+  if (!ev.clamped) {  // render.hpp:572-586
+    v[8] += ev.weight * d_alpha;
+    const float d_q = -0.5f * alpha * d_alpha;
+    const float det = r.a * r.c - r.b * r.b;
+    const float inv_det = 1.0f / det;
+    const float dx = p.cx - r.mx, dy = p.cy - r.my;
+    const float dqi = d_q * inv_det;
+    v[5] += dqi * (dy * dy - ev.q * r.c);
+    v[6] += dqi * (-2.0f * dx * dy + 2.0f * ev.q * r.b);
+    v[7] += dqi * (dx * dx - ev.q * r.a);
+    v[3] += dqi * (-2.0f * r.c * dx + 2.0f * r.b * dy);
+    v[4] += dqi * (2.0f * r.b * dx - 2.0f * r.a * dy);
+  }
+  return true;
+}
+
+// Warp reduce-scatter of 9 values (padded to 16): 16 shuffles instead of 9 x 5 butterflies.
+// Afterwards lane l holds the warp total of value index ((l>>4)&1)*8 + ((l>>3)&1)*4 +
+// ((l>>2)&1)*2 + ((l>>1)&1) (lanes 2k and 2k+1 hold the same total). Fixed order: deterministic.
+__device__ __forceinline__ float warp_reduce_scatter9(const float v[9], int lane) {
+  float x[16];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) x[i] = v[i];
+#pragma unroll
+  for (int i = 9; i < 16; ++i) x[i] = 0.0f;
+#pragma unroll
+  for (int o = 16, n = 16; o >= 2; o >>= 1, n >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const float send = up ? x[i] : x[i + n / 2];
+      const float keep = up ? x[i + n / 2] : x[i];
+      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return x[0] + __shfl_xor_sync(0xffffffffu, x[0], 1);
+}
+
+// Reverse sweep (render.hpp:542-589) per 16x16 tile: 128 threads, 2 pixels each (rows ly and
+// ly + 2 of a 4-row warp band), so a splat's 9 gradient terms are pre-summed per lane and
+// reduced once per warp. One partial SlotAcc per (splat, tile) instance, fixed-order sums (no
+// float atomics, deterministic). partial layout: [instance][9] = rgb3, m2d2, cov3, ab.
+constexpr int kBwdThreads = kTilePix / 2;
+__global__ void __launch_bounds__(kBwdThreads) backward_kernel(const SplatRec* __restrict__ recs,
+                                                               const int32_t* __restrict__ vals,
+                                                               const int2* __restrict__ ranges, Win w, float bg0,
+                                                               float bg1, float bg2, const float* __restrict__ fT_in,
+                                                               const int32_t* __restrict__ last_in,
+                                                               const float* __restrict__ d_img, float* partials) {
   __shared__ SplatRec sh[kBwdBatch];
-  __shared__ float red[kBwdBatch][kTilePix / 32][9];
+  __shared__ float red[kBwdBatch][kBwdThreads / 32][9];
   __shared__ int smax;
   const int tile = blockIdx.x;
   const int tx = tile % w.tw, ty = tile / w.tw;
-  const int lx = threadIdx.x % kTileSize, ly = threadIdx.x / kTileSize;
-  const int x = w.px0 + tx * kTileSize + lx, y = w.py0 + ty * kTileSize + ly;
-  const bool inside = x < w.px0 + w.pw && y < w.py0 + w.ph;
-  const float cx = (float)x + 0.5f, cy = (float)y + 0.5f;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lx = lane & 15, ly = warp * 4 + (lane >> 4);
   const int2 rg = ranges[tile];
-  int L = 0;
-  float T = 1.0f, g0 = 0.0f, g1 = 0.0f, g2 = 0.0f;
-  if (inside) {
-    const int64_t pix = (int64_t)(y - w.py0) * w.pw + (x - w.px0);
-    L = last_in[pix];
-    T = fT_in[pix];
-    g0 = d_img[pix * 3];
-    g1 = d_img[pix * 3 + 1];
-    g2 = d_img[pix * 3 + 2];
-    if (g0 == 0.0f && g1 == 0.0f && g2 == 0.0f) L = 0;  // render.hpp:551
+  PixB px[2];
+  int lmax = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    PixB& p = px[h];
+    p.x = w.px0 + tx * kTileSize + lx;
+    p.y = w.py0 + ty * kTileSize + ly + 2 * h;
+    p.cx = (float)p.x + 0.5f;
+    p.cy = (float)p.y + 0.5f;
+    p.L = 0;
+    p.T = 1.0f;
+    p.g0 = p.g1 = p.g2 = 0.0f;
+    if (p.x < w.px0 + w.pw && p.y < w.py0 + w.ph) {
+      const int64_t pix = (int64_t)(p.y - w.py0) * w.pw + (p.x - w.px0);
+      p.L = last_in[pix];
+      p.T = fT_in[pix];
+      p.g0 = d_img[pix * 3];
+      p.g1 = d_img[pix * 3 + 1];
+      p.g2 = d_img[pix * 3 + 2];
+      if (p.g0 == 0.0f && p.g1 == 0.0f && p.g2 == 0.0f) p.L = 0;  // render.hpp:551
+    }
+    p.s0 = p.T * bg0;
+    p.s1 = p.T * bg1;
+    p.s2 = p.T * bg2;
+    lmax = max(lmax, p.L);
   }
-  float s0 = T * bg0, s1 = T * bg1, s2 = T * bg2;
   if (threadIdx.x == 0) smax = 0;
   __syncthreads();
-  if (L > 0) atomicMax(&smax, L);
+  if (lmax > 0) atomicMax(&smax, lmax);
   __syncthreads();
   const int Lmax = smax;
-  const int txi = tx, tyi = ty;
+  const int vidx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
   for (int bend = Lmax; bend > 0; bend -= kBwdBatch) {
     const int bstart = max(0, bend - kBwdBatch);
     const int nb = bend - bstart;
@@ -374,62 +451,26 @@ __global__ void __launch_bounds__(kTilePix) backward_kernel(const SplatRec* __re
       float v[9];
 #pragma unroll
       for (int i = 0; i < 9; ++i) v[i] = 0.0f;
-      const bool act = (bstart + jj) < L && x >= r.bx0 && x < r.bx1 && y >= r.by0 && y < r.by1;
-      if (act) {
-        const EvalOut ev = contrib_eval(r, cx, cy);
-        const float alpha = ev.alpha;
-        const float Tb = T / (1.0f - alpha);  // transmittance before this contribution
-        const float w_rgb = alpha * Tb;
-        v[0] = w_rgb * g0;
-        v[1] = w_rgb * g1;
-        v[2] = w_rgb * g2;
-        const float dot_c = r.r * g0 + r.g * g1 + r.bl * g2;
-        const float dot_suf = s0 * g0 + s1 * g1 + s2 * g2;
-        const float d_alpha = Tb * dot_c - dot_suf / (1.0f - alpha);
-        s0 += r.r * alpha * Tb;
-        s1 += r.g * alpha * Tb;
-        s2 += r.bl * alpha * Tb;
-        T = Tb;
-        if (!ev.clamped) {
-          v[8] = ev.weight * d_alpha;
-          const float d_q = -0.5f * alpha * d_alpha;
-          const float det = r.a * r.c - r.b * r.b;
-          const float inv_det = 1.0f / det;
-          const float dx = cx - r.mx, dy = cy - r.my;
-          v[5] = d_q * (dy * dy - ev.q * r.c) * inv_det;
-          v[6] = d_q * (-2.0f * dx * dy + 2.0f * ev.q * r.b) * inv_det;
-          v[7] = d_q * (dx * dx - ev.q * r.a) * inv_det;
-          const float dq_dmx = (-2.0f * r.c * dx + 2.0f * r.b * dy) * inv_det;
-          const float dq_dmy = (2.0f * r.b * dx - 2.0f * r.a * dy) * inv_det;
-          v[3] = d_q * dq_dmx;
-          v[4] = d_q * dq_dmy;
-        }
-      }
+      bool act = bwd_contrib(r, bstart + jj, px[0], v);
+      act |= bwd_contrib(r, bstart + jj, px[1], v);
       if (__any_sync(0xffffffffu, act)) {
-#pragma unroll
-        for (int i = 0; i < 9; ++i) {
-          float s = v[i];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          v[i] = s;
-        }
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int i = 0; i < 9; ++i) red[jj][warp][i] = v[i];
+        const float tot = warp_reduce_scatter9(v, lane);
+        if ((lane & 1) == 0 && vidx < 9) red[jj][warp][vidx] = tot;
+      } else if (lane < 9) {
+        red[jj][warp][lane] = 0.0f;
       }
     }
     __syncthreads();
     // Fixed-order cross-warp sum, one instance partial per splat of the batch.
-    for (int e = threadIdx.x; e < nb * 9; e += kTilePix) {
+    for (int e = threadIdx.x; e < nb * 9; e += kBwdThreads) {
       const int jj = e / 9, i = e - jj * 9;
       float s = 0.0f;
 #pragma unroll
-      for (int q = 0; q < kTilePix / 32; ++q) s += red[jj][q][i];
+      for (int q = 0; q < kBwdThreads / 32; ++q) s += red[jj][q][i];
       const SplatRec& r = sh[jj];
       int tx0, ty0, ntx, nty;
       tile_box(r, w, tx0, ty0, ntx, nty);
-      const int64_t inst = (int64_t)r.off + (int64_t)(tyi - ty0) * ntx + (txi - tx0);
+      const int64_t inst = (int64_t)r.off + (int64_t)(ty - ty0) * ntx + (tx - tx0);
       partials[inst * 9 + i] = s;
     }
   }
@@ -795,7 +836,7 @@ void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int6
   if (I > 0 && npix > 0) {
     GSS_CUDA(cudaMemsetAsync(partials, 0, (size_t)I * 9 * 4, st));
     const int ntile = w.tw * w.th;
-    backward_kernel<<<ntile, kTilePix, 0, st>>>(recs, static_cast<const int32_t*>(ctx->vals_a.p),
+    backward_kernel<<<ntile, kBwdThreads, 0, st>>>(recs, static_cast<const int32_t*>(ctx->vals_a.p),
                                                 static_cast<const int2*>(ctx->ranges.p), w, ctx->sc.bg[0],
                                                 ctx->sc.bg[1], ctx->sc.bg[2], static_cast<const float*>(ctx->fT.p),
                                                 static_cast<const int32_t*>(ctx->last.p), d_img, partials);
