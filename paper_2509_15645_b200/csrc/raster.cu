@@ -332,13 +332,41 @@ struct PixB {
   int x, y, L;
 };
 
+// Per-splat constants of the backward sweep, computed once per batch: the conic (inverse 2D
+// covariance) so the per-pixel exponent needs no division.
+struct BwdConic {
+  float ia, ib, ic;  // c/det, b/det, a/det
+  float inv_det;
+};
+
+__device__ __forceinline__ float ex2_fast(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rcp_fast(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // One contribution of splat r (sweep position jpos) to pixel p: accumulates its 9 screen-space
 // gradient terms into v and steps the pixel's reverse state. Returns whether it contributed.
-__device__ __forceinline__ bool bwd_contrib(const SplatRec& r, int jpos, PixB& p, float v[9]) {
+// The gradient arithmetic runs on fast math (tolerance-checked); the 0.999 clamp
+// decision, which selects the reference's branch (render.hpp:560-573), is recomputed with the
+// forward's exact arithmetic whenever the fast alpha is within 1e-4 of the threshold, so both
+// passes always take the same branch.
+__device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k, int jpos, PixB& p, float v[9]) {
   if (!(jpos < p.L && p.x >= r.bx0 && p.x < r.bx1 && p.y >= r.by0 && p.y < r.by1)) return false;
-  const EvalOut ev = contrib_eval(r, p.cx, p.cy);
-  const float alpha = ev.alpha;
-  const float inv1m = 1.0f / (1.0f - alpha);
+  const float dx = p.cx - r.mx, dy = p.cy - r.my;
+  float q = __fmaf_rn(k.ia * dx, dx, __fmaf_rn(k.ic * dy, dy, -2.0f * k.ib * dx * dy));
+  q = q < 0.0f ? 0.0f : q;
+  const float weight = ex2_fast(-0.72134752f * q);  // exp(-q/2)
+  float raw = r.ab * weight;
+  if (fabsf(raw - 0.999f) < 1e-4f) raw = contrib_eval(r, p.cx, p.cy).clamped ? 1.0f : 0.0f;
+  const bool clamped = raw > 0.999f;
+  const float alpha = clamped ? 0.999f : r.ab * weight;
+  const float inv1m = rcp_fast(1.0f - alpha);
   const float Tb = p.T * inv1m;  // transmittance before this contribution
   const float w_rgb = alpha * Tb;
   v[0] += w_rgb * p.g0;
@@ -351,16 +379,12 @@ __device__ __forceinline__ bool bwd_contrib(const SplatRec& r, int jpos, PixB& p
   p.s1 += r.g * w_rgb;
   p.s2 += r.bl * w_rgb;
   p.T = Tb;
-  if (!ev.clamped) {  // render.hpp:572-586
-    v[8] += ev.weight * d_alpha;
-    const float d_q = -0.5f * alpha * d_alpha;
-    const float det = r.a * r.c - r.b * r.b;
-    const float inv_det = 1.0f / det;
-    const float dx = p.cx - r.mx, dy = p.cy - r.my;
-    const float dqi = d_q * inv_det;
-    v[5] += dqi * (dy * dy - ev.q * r.c);
-    v[6] += dqi * (-2.0f * dx * dy + 2.0f * ev.q * r.b);
-    v[7] += dqi * (dx * dx - ev.q * r.a);
+  if (!clamped) {  // render.hpp:572-586
+    v[8] += weight * d_alpha;
+    const float dqi = -0.5f * alpha * d_alpha * k.inv_det;
+    v[5] += dqi * (dy * dy - q * r.c);
+    v[6] += dqi * (-2.0f * dx * dy + 2.0f * q * r.b);
+    v[7] += dqi * (dx * dx - q * r.a);
     v[3] += dqi * (-2.0f * r.c * dx + 2.0f * r.b * dy);
     v[4] += dqi * (2.0f * r.b * dx - 2.0f * r.a * dy);
   }
@@ -401,6 +425,7 @@ __global__ void __launch_bounds__(kBwdThreads) backward_kernel(const SplatRec* _
                                                                const int32_t* __restrict__ last_in,
                                                                const float* __restrict__ d_img, float* partials) {
   __shared__ SplatRec sh[kBwdBatch];
+  __shared__ BwdConic shk[kBwdBatch];
   __shared__ float red[kBwdBatch][kBwdThreads / 32][9];
   __shared__ int smax;
   const int tile = blockIdx.x;
@@ -444,15 +469,21 @@ __global__ void __launch_bounds__(kBwdThreads) backward_kernel(const SplatRec* _
     const int bstart = max(0, bend - kBwdBatch);
     const int nb = bend - bstart;
     __syncthreads();
-    if ((int)threadIdx.x < nb) load_rec(&sh[threadIdx.x], recs, vals[rg.x + bstart + threadIdx.x]);
+    if ((int)threadIdx.x < nb) {
+      load_rec(&sh[threadIdx.x], recs, vals[rg.x + bstart + threadIdx.x]);
+      const SplatRec& r = sh[threadIdx.x];
+      const float inv = 1.0f / (r.a * r.c - r.b * r.b);  // det > 0 for every binned splat
+      shk[threadIdx.x] = BwdConic{r.c * inv, r.b * inv, r.a * inv, inv};
+    }
     __syncthreads();
     for (int jj = nb - 1; jj >= 0; --jj) {
-      const SplatRec& r = sh[jj];
+      const SplatRec r = sh[jj];
+      const BwdConic k = shk[jj];
       float v[9];
 #pragma unroll
       for (int i = 0; i < 9; ++i) v[i] = 0.0f;
-      bool act = bwd_contrib(r, bstart + jj, px[0], v);
-      act |= bwd_contrib(r, bstart + jj, px[1], v);
+      bool act = bwd_contrib(r, k, bstart + jj, px[0], v);
+      act |= bwd_contrib(r, k, bstart + jj, px[1], v);
       if (__any_sync(0xffffffffu, act)) {
         const float tot = warp_reduce_scatter9(v, lane);
         if ((lane & 1) == 0 && vidx < 9) red[jj][warp][vidx] = tot;
