@@ -18,7 +18,9 @@ namespace gssd {
 // render.hpp:105, 348, 374 call std::exp(float)). Evaluated in fp64 exactly like the host:
 // kd = fma(x, 32/ln2, 2^52*1.5), r = fma(x, 32/ln2, -kd), s = 2^(k/32) from the table, cubic in r.
 // Exhaustively equal to host expf over all 2^32 inputs (oracle/gss_oracle.c: orc_expf).
-__constant__ static const unsigned long long kExp2Tab[32] = {
+// Global (not __constant__) table: the index differs per lane, and indexed constant-bank loads
+// serialise across distinct addresses; an L1-resident global load does not.
+__device__ static const unsigned long long kExp2Tab[32] = {
     0x3ff0000000000000ULL, 0x3fefd9b0d3158574ULL, 0x3fefb5586cf9890fULL, 0x3fef9301d0125b51ULL,
     0x3fef72b83c7d517bULL, 0x3fef54873168b9aaULL, 0x3fef387a6e756238ULL, 0x3fef1e9df51fdee1ULL,
     0x3fef06fe0a31b715ULL, 0x3feef1a7373aa9cbULL, 0x3feedea64c123422ULL, 0x3feece086061892dULL,
@@ -40,7 +42,7 @@ __device__ __forceinline__ float gss_expf(float x) {
   const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
   kd = __dsub_rn(kd, shift);
   const double r = __fma_rn(inv_ln2_n, xd, -kd);
-  const unsigned long long t = kExp2Tab[ki & 31] + (ki << 47);
+  const unsigned long long t = __ldg(&kExp2Tab[ki & 31]) + (ki << 47);
   const double s = __longlong_as_double((long long)t);
   const double z = __fma_rn(0x1.c6af84b912394p-5 / (32.0 * 32 * 32), r, 0x1.ebfce50fac4f3p-3 / (32.0 * 32));
   const double r2 = __dmul_rn(r, r);
