@@ -231,24 +231,37 @@ __global__ void __launch_bounds__(kUpdThreads) update_kernel(ArenaDev a, GradsDe
     const float ms = lut.a1[g][0], vs = lut.a2[g][0];
     const float s0 = lut.sc[g][0], s1 = lut.sc[g][1], s2 = lut.sc[g][2], s3 = lut.sc[g][3], s4 = lut.sc[g][4];
     const int npass = (nrows + rpp - 1) / rpp;
-#pragma unroll 4
-    for (int p = warp; p < npass; p += kUpdThreads / 32) {
-      const int lr = p * rpp + rr;
-      if (!act || lr >= nrows) continue;
-      const size_t off = (size_t)(r0 + lr) * dim + c;
-      float w = a.w[off], m = a.m[off], v = a.v[off];
-      const int sl = slot_of[lr];
-      const float gv = sl >= 0 ? gr.rows[(size_t)sl * gr.stride + gr.col0 + c] : 0.0f;
-      const float m_new = ms * m + s0 * gv;
-      const float v_new = vs * v + s1 * gv * gv;
-      // (0 * m) / (sqrt(v) + eps) is (0 * m) itself whenever v >= 0 (denominator >= eps > 0).
-      const float num = 0.0f * m;
-      w = v >= 0.0f ? w - num : w - div_rn(num, sqrtf(v) + s4);
-      const float denom = div_rn(sqrtf(v_new), s2) + s4;
-      w = w - div_rn(s3 * m_new, denom);
-      a.w[off] = w;
-      a.m[off] = m_new;
-      a.v[off] = v_new;
+    constexpr int kU = 4;  // passes per warp in flight: all loads issued before any math
+    constexpr int kW = kUpdThreads / 32;
+    for (int p0 = warp; p0 < npass; p0 += kW * kU) {
+      float w[kU], m[kU], v[kU], gv[kU];
+      size_t off[kU];
+      bool ok[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int lr = (p0 + u * kW) * rpp + rr;
+        ok[u] = act && p0 + u * kW < npass && lr < nrows;
+        off[u] = ok[u] ? (size_t)(r0 + lr) * dim + c : 0;
+        const int sl = ok[u] ? slot_of[lr] : -1;
+        w[u] = ok[u] ? a.w[off[u]] : 0.0f;
+        m[u] = ok[u] ? a.m[off[u]] : 0.0f;
+        v[u] = ok[u] ? a.v[off[u]] : 0.0f;
+        gv[u] = sl >= 0 ? gr.rows[(size_t)sl * gr.stride + gr.col0 + c] : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (!ok[u]) continue;
+        const float m_new = ms * m[u] + s0 * gv[u];
+        const float v_new = vs * v[u] + s1 * gv[u] * gv[u];
+        // (0 * m) / (sqrt(v) + eps) is (0 * m) itself whenever v >= 0 (denominator >= eps > 0).
+        const float num = 0.0f * m[u];
+        float ww = v[u] >= 0.0f ? w[u] - num : w[u] - div_rn(num, sqrtf(v[u]) + s4);
+        const float denom = div_rn(sqrtf(v_new), s2) + s4;
+        ww = ww - div_rn(s3 * m_new, denom);
+        a.w[off[u]] = ww;
+        a.m[off[u]] = m_new;
+        a.v[off[u]] = v_new;
+      }
     }
     if (touched_count && tid == 0 && nrows > 0)
       atomicAdd((unsigned long long*)touched_count, (unsigned long long)nrows);

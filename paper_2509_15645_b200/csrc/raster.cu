@@ -82,7 +82,7 @@ struct DBuf {
 
 struct gss_render_ctx {
   gssd::DBuf recs, ntiles, offsets, keys_a, keys_b, vals_a, vals_b, cub_tmp, ranges, last, fT, partials, lossp,
-      hostcnt;
+      hostcnt, sums;
   gssd::Win win{};
   gssd::SceneDev sc{};
   gssd::Cam cam{};
@@ -508,31 +508,120 @@ __global__ void __launch_bounds__(kBwdThreads) backward_kernel(const SplatRec* _
 }
 
 // render.hpp:600-638 + project_geo_backward (render.hpp:152-237), per slot.
-__global__ void chain_kernel(SceneDev s, Cam cam, Win w, int64_t V, const SplatRec* recs, const int32_t* offsets,
-                             const float* partials, float* gg, int64_t gstride, float* gn, int64_t nstride,
-                             float* mean2d) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= V) return;
-  float* outg = gg + k * gstride;
-  float* outn = gn + k * nstride;
+// Per-slot sums of the backward's instance partials (CSR by slot: instances of slot k are
+// [offsets[k], offsets[k+1])), in a fixed order: each lane sums its own slot's first kHead
+// instances sequentially (2x unrolled so loads overlap), then the warp sums the tails of big
+// splats (near-camera Gaussians cover hundreds of tiles) cooperatively, 4x unrolled, with a
+// fixed butterfly. Light on registers, so many warps hide the load latency.
+constexpr int kSumThreads = 256;
+__global__ void __launch_bounds__(kSumThreads) slot_sum_kernel(int64_t V, const int32_t* offsets,
+                                                               const float* __restrict__ partials, float* sums) {
+  constexpr int kHead = 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (int64_t)blockIdx.x * kSumThreads + threadIdx.x;
+  const int64_t kw = k - lane;
+  if (kw >= V) return;
+  int32_t o0 = 0, o1 = 0;
+  if (k < V) {
+    o0 = offsets[k];
+    o1 = offsets[k + 1];
+  }
+  float acc[9];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) acc[c] = 0.0f;
+  const int32_t hend = min(o1, o0 + kHead);
+  int32_t i = o0;
+  for (; i + 1 < hend; i += 2) {
+    float a0[9], a1[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+      a0[c] = partials[(int64_t)i * 9 + c];
+      a1[c] = partials[(int64_t)(i + 1) * 9 + c];
+    }
+#pragma unroll
+    for (int c = 0; c < 9; ++c) acc[c] = (acc[c] + a0[c]) + a1[c];
+  }
+  if (i < hend)
+#pragma unroll
+    for (int c = 0; c < 9; ++c) acc[c] += partials[(int64_t)i * 9 + c];
+  unsigned big = __ballot_sync(0xffffffffu, o1 - o0 > kHead);
+  while (big) {
+    const int b = __ffs(big) - 1;
+    big &= big - 1;
+    const int32_t t0 = __shfl_sync(0xffffffffu, o0, b) + kHead, t1 = __shfl_sync(0xffffffffu, o1, b);
+    float tail[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) tail[c] = 0.0f;
+    int32_t j = t0 + lane;
+    for (; j + 96 < t1; j += 128) {
+      float x[4][9];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < 9; ++c) x[u][c] = partials[(int64_t)(j + 32 * u) * 9 + c];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < 9; ++c) tail[c] += x[u][c];
+    }
+    for (; j < t1; j += 32)
+#pragma unroll
+      for (int c = 0; c < 9; ++c) tail[c] += partials[(int64_t)j * 9 + c];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tail[c] += __shfl_xor_sync(0xffffffffu, tail[c], o);
+      if (lane == b) acc[c] += tail[c];
+    }
+  }
+  if (k < V)
+#pragma unroll
+    for (int c = 0; c < 9; ++c) sums[k * 9 + c] = acc[c];
+}
+
+constexpr int kChainThreads = 128;
+constexpr int kChainRow = 61;     // odd row pitch: conflict-free per-lane row access
+// Warp-cooperative: a warp owns 32 consecutive slots. It sums each slot's instance partials with
+// all lanes, stages the slots' 49-float non-geometric rows in SMEM with coalesced loads; each lane
+// then runs the reference chain for its slot, and the 59 outputs are written back through SMEM
+// with coalesced stores.
+template <int DEG>
+__global__ void __launch_bounds__(kChainThreads) chain_kernel(SceneDev s, Cam cam, Win w, int64_t V,
+                                                              const SplatRec* recs, const float* sums,
+                                                              float* gg, int64_t gstride,
+                                                              float* gn, int64_t nstride, float* mean2d) {
+  __shared__ float row_s[kChainThreads / 32][32][kChainRow];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t k0 = (int64_t)blockIdx.x * kChainThreads + warp * 32;
+  if (k0 >= V) return;
+  const int nk = (V - k0) < 32 ? (int)(V - k0) : 32;
+  float(*rows)[kChainRow] = row_s[warp];
+  {
+    // Row base pointers resolved once per lane, then 49 independent coalesced loads per lane.
+    const float* my_row = lane < nk ? ng_row(s, (int)(k0 + lane), s.ids[k0 + lane]) : s.nongeo;
+#pragma unroll 7
+    for (int e = lane; e < 32 * 49; e += 32) {
+      const int kk = e / 49, c = e - kk * 49;
+      const float* rp = (const float*)__shfl_sync(0xffffffffu, (unsigned long long)my_row, kk);
+      if (kk < nk) rows[kk][c] = rp[c];
+    }
+  }
+  __syncwarp();
+  const int64_t k = k0 + lane;
   float out[59];
 #pragma unroll
   for (int i = 0; i < 59; ++i) out[i] = 0.0f;
   float sa[9];
 #pragma unroll
-  for (int i = 0; i < 9; ++i) sa[i] = 0.0f;
-  const int id = s.ids[k];
+  for (int i = 0; i < 9; ++i) sa[i] = lane < nk ? sums[(k0 + lane) * 9 + i] : 0.0f;
+  const int id = lane < nk ? s.ids[k] : 0;
   const float* g = s.geo + (int64_t)id * s.geo_stride;
   Proj p;
   f3 t;
-  const bool valid = project_geo(cam, g, s.lp, p, t);
+  const bool valid = lane < nk && project_geo(cam, g, s.lp, p, t);
   if (valid) {
-    const int32_t o0 = offsets[k], o1 = offsets[k + 1];
-    for (int32_t i = o0; i < o1; ++i)
-#pragma unroll
-      for (int c = 0; c < 9; ++c) sa[c] += partials[(int64_t)i * 9 + c];
     const SplatRec r = recs[k];
-    const float* ng = ng_row(s, (int)k, id);
+    const float* ng = rows[lane];
     const float ab = r.ab;
     out[10] += sa[8] * ab * (1.0f - ab);
     const f3 cp = cam_position(cam);
@@ -544,17 +633,19 @@ __global__ void chain_kernel(SceneDev s, Cam cam, Win w, int64_t V, const SplatR
       const f3 u{dir.x * inv, dir.y * inv, dir.z * inv};
       float basis[16];
       f3 bgr[16];
-      sh_basis(u.x, u.y, u.z, s.sh_degree, basis);
-      sh_basis_grad(u.x, u.y, u.z, s.sh_degree, bgr);
-      const int nb = (s.sh_degree + 1) * (s.sh_degree + 1);
+      sh_basis(u.x, u.y, u.z, DEG, basis);
+      sh_basis_grad(u.x, u.y, u.z, DEG, bgr);
+      constexpr int nb = (DEG + 1) * (DEG + 1);
       float gc[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {  // eval_sh_clamp_mask (sh.hpp:114-125)
         float v = 0.5f;
+#pragma unroll
         for (int b = 0; b < nb; ++b) v += basis[b] * ng[1 + 3 * b + c];
         gc[c] = (v < 0.0f || v > 1.0f) ? 0.0f : sa[c];
       }
       f3 ddir{0.0f, 0.0f, 0.0f};
+#pragma unroll
       for (int b = 0; b < nb; ++b) {  // eval_sh_backward (sh.hpp:92-110)
         float coef_dot = 0.0f;
 #pragma unroll
@@ -672,13 +763,23 @@ __global__ void chain_kernel(SceneDev s, Cam cam, Win w, int64_t V, const SplatR
     out[1] += W[1] * dt.x + W[4] * dt.y + W[7] * dt.z;
     out[2] += W[2] * dt.x + W[5] * dt.y + W[8] * dt.z;
   }
+  __syncwarp();
+  if (lane < nk) {
 #pragma unroll
-  for (int i = 0; i < 10; ++i) outg[i] = out[i];
-#pragma unroll
-  for (int i = 0; i < 49; ++i) outn[i] = out[10 + i];
-  if (mean2d) {
-    mean2d[k * 2] = sa[3];
-    mean2d[k * 2 + 1] = sa[4];
+    for (int i = 0; i < 59; ++i) rows[lane][i] = out[i];
+    if (mean2d) {
+      mean2d[k * 2] = sa[3];
+      mean2d[k * 2 + 1] = sa[4];
+    }
+  }
+  __syncwarp();
+  for (int e = lane; e < nk * 10; e += 32) {
+    const int kk = e / 10, c = e - kk * 10;
+    gg[(k0 + kk) * gstride + c] = rows[kk][c];
+  }
+  for (int e = lane; e < nk * 49; e += 32) {
+    const int kk = e / 49, c = e - kk * 49;
+    gn[(k0 + kk) * nstride + c] = rows[kk][10 + c];
   }
 }
 
@@ -875,8 +976,18 @@ void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int6
   } else if (I > 0) {
     GSS_CUDA(cudaMemsetAsync(partials, 0, (size_t)I * 9 * 4, st));
   }
-  chain_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(ctx->sc, ctx->cam, w, V, recs, offs, partials, gg, gstride,
-                                                          gn, nstride, mean2d);
+  float* sums = static_cast<float*>(ctx->sums.get((size_t)V * 9 * 4, st));
+  slot_sum_kernel<<<(unsigned)ceil_div(V, kSumThreads), kSumThreads, 0, st>>>(V, offs, partials, sums);
+  GSS_LAUNCHED();
+  {
+    const unsigned cb = (unsigned)ceil_div(V, kChainThreads);
+    switch (ctx->sc.sh_degree) {
+      case 0: chain_kernel<0><<<cb, kChainThreads, 0, st>>>(ctx->sc, ctx->cam, w, V, recs, sums, gg, gstride, gn, nstride, mean2d); break;
+      case 1: chain_kernel<1><<<cb, kChainThreads, 0, st>>>(ctx->sc, ctx->cam, w, V, recs, sums, gg, gstride, gn, nstride, mean2d); break;
+      case 2: chain_kernel<2><<<cb, kChainThreads, 0, st>>>(ctx->sc, ctx->cam, w, V, recs, sums, gg, gstride, gn, nstride, mean2d); break;
+      default: chain_kernel<3><<<cb, kChainThreads, 0, st>>>(ctx->sc, ctx->cam, w, V, recs, sums, gg, gstride, gn, nstride, mean2d); break;
+    }
+  }
   GSS_LAUNCHED();
 }
 
@@ -886,7 +997,7 @@ void render_ctx_destroy(gss_render_ctx* ctx) {
   if (!ctx) return;
   cudaStream_t st = ctx->last_stream;
   for (DBuf* b : {&ctx->recs, &ctx->ntiles, &ctx->offsets, &ctx->keys_a, &ctx->keys_b, &ctx->vals_a, &ctx->vals_b,
-                  &ctx->cub_tmp, &ctx->ranges, &ctx->last, &ctx->fT, &ctx->partials, &ctx->lossp, &ctx->hostcnt})
+                  &ctx->cub_tmp, &ctx->ranges, &ctx->last, &ctx->fT, &ctx->partials, &ctx->lossp, &ctx->hostcnt, &ctx->sums})
     b->release(st);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
