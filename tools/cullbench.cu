@@ -1,0 +1,33 @@
+// Standalone timing harness for cull.cu variants (dev only).
+#include <atomic>
+#include <string>
+#include "../paper_2509_15645_b200/csrc/cull.cu"
+namespace gssd {
+void set_error(const std::string&) {}
+void count_launch() {}
+int64_t launches() { return 0; }
+}
+#include <cstdio>
+#include <vector>
+int main(int argc, char** argv) {
+  FILE* f = fopen(argv[1], "rb");
+  int64_t n; fread(&n, 8, 1, f);
+  gss_camera cam; fread(&cam, sizeof cam, 1, f);
+  std::vector<float> rows(n * 10); fread(rows.data(), 4, n * 10, f); fclose(f);
+  float *geo; int32_t* ids; int64_t* cnt; void* ws;
+  cudaMalloc(&geo, n * 40); cudaMemcpy(geo, rows.data(), n * 40, cudaMemcpyHostToDevice);
+  cudaMalloc(&ids, n * 4); cudaMalloc(&cnt, 8);
+  size_t wsb = gssd::cull_workspace_bytes(n); cudaMalloc(&ws, wsb); cudaMemset(ws, 0, wsb);
+  gss_viewport vp{0.f, (float)cam.width, 0.f, (float)cam.height};
+  cudaStream_t st; cudaStreamCreate(&st);
+  for (int i = 0; i < 5; ++i) gssd::cull(geo, n, 10, &cam, &vp, 0.3f, nullptr, ids, cnt, ws, wsb, st);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int reps = 50;
+  cudaEventRecord(e0, st);
+  for (int i = 0; i < reps; ++i) gssd::cull(geo, n, 10, &cam, &vp, 0.3f, nullptr, ids, cnt, ws, wsb, st);
+  cudaEventRecord(e1, st); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= reps;
+  int64_t v; cudaMemcpy(&v, cnt, 8, cudaMemcpyDeviceToHost);
+  printf("%s: %.2f us  visible %lld  %.0f GB/s\n", argv[2], ms * 1e3, (long long)v, (40.0 * n + 4.0 * v) / ms / 1e6);
+  return 0;
+}
