@@ -71,7 +71,7 @@ def build_oracle(with_ref: bool | None = None) -> None:
     if with_ref is None:
         with_ref = Path("/root/reference/proj/include/gss").is_dir()
     if with_ref:
-        targets.append("ref")
+        targets += ["ref", "dropin"]
     subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), *targets], check=True)
 
 

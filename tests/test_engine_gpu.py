@@ -104,3 +104,20 @@ def test_fresh_snapshot_equals_initial():
     start, cams, gts = scene(n=60, cams=3, img=16, seed=21)
     e = engine(start, cams, gts)
     assert np.array_equal(e.snapshot().view(np.uint32), start.view(np.uint32))
+
+
+@pytest.mark.parametrize("pipelined", [False, True])
+def test_host_offload_tier_equals_hbm_bitwise(pipelined):
+    """Selective offloading (store.hpp:149-192): the non-geometric tier in mapped pinned host
+    memory (gathered / lazily updated through the host link) gives the same trajectory, bit for
+    bit, as the tier resident in HBM."""
+    start, cams, gts = scene(n=150, cams=5, img=24, seed=41)
+    eh = engine(start, cams, gts, pipelined=pipelined, nongeo_on_host=True)
+    ed = engine(start, cams, gts, pipelined=pipelined, nongeo_on_host=False)
+    lh, vh = eh.run(25)
+    ld, vd = ed.run(25)
+    assert np.array_equal(lh.view(np.uint32), ld.view(np.uint32))
+    assert np.array_equal(vh, vd)
+    sh, sd = eh.state(), ed.state()
+    for k in ("geo_w", "ng_w", "ng_m", "ng_v", "ng_counter"):
+        assert np.array_equal(np.asarray(sh[k]).view(np.uint8), np.asarray(sd[k]).view(np.uint8)), k
