@@ -141,7 +141,9 @@ def run_ours(a, rank, world):
     dev = torch.device("cuda", local)
     # Weak scaling: every rank owns an independent id-range shard of the scene (own seed) and
     # its optimizer state; no data-path collective.
-    cfg = scene_config(a.n, a.width, a.height, a.cams, a.seed + rank)
+    from paper_2509_15645_b200 import dist as D
+
+    cfg = scene_config(a.n, a.width, a.height, a.cams, D.shard_seed(a.seed, rank))
     truth, cams = G.synth_scene_params(cfg)
     truth_dev = torch.from_numpy(truth).to(dev)
     gts = np.stack([G.render_view(truth_dev, c, 3).cpu().numpy() for c in cams])
@@ -165,12 +167,8 @@ def run_ours(a, rank, world):
     e1.record()
     torch.cuda.synchronize()
     clocks = clk.stop()
-    ms = e0.elapsed_time(e1)
+    ms = D.max_over_ranks(e0.elapsed_time(e1), dev)
     stage = eng.stage_ms()
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     ms_per_step = ms / a.steps
     value = world * a.steps / (ms / 1e3)
 
@@ -189,11 +187,7 @@ def run_ours(a, rank, world):
     eng.drain()
     f1.record()
     torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = D.max_over_ranks(f0.elapsed_time(f1), dev)
     e2e = {"value": world * a.steps / (e2e_ms / 1e3), "unit": "iters/s",
            "h2d_bytes_per_step": a.width * a.height * 3 * 4, "d2h_bytes_per_step": 4 + 8,
            "api": "gss_engine_step (OffloadEngine.step): pinned host GT -> loss on host"}
