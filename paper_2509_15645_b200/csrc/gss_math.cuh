@@ -30,12 +30,8 @@ __device__ static const unsigned long long kExp2Tab[32] = {
     0x3feee89f995ad3adULL, 0x3feeff76f2fb5e47ULL, 0x3fef199bdd85529cULL, 0x3fef3720dcef9069ULL,
     0x3fef5818dcfba487ULL, 0x3fef7c97337b9b5fULL, 0x3fefa4afa2a490daULL, 0x3fefd0765b6e4540ULL};
 
-__device__ __forceinline__ float gss_expf(float x) {
-  if (!(x <= 0x1.62e42ep6f)) {                 // > 88.72 (overflow), +inf or NaN
-    if (x != x) return x + x;
-    return __int_as_float(0x7f800000);
-  }
-  if (x < -0x1.9fe368p6f) return 0.0f;         // underflow and -inf
+// glibc 2.39 expf body (table-driven, FMA variant) for x in [-103.97, 88.72].
+__device__ __forceinline__ float gss_expf_core(float x) {
   const double inv_ln2_n = 0x1.71547652b82fep+0 * 32.0, shift = 0x1.8p+52;
   const double xd = (double)x;
   double kd = __fma_rn(inv_ln2_n, xd, shift);
@@ -50,6 +46,22 @@ __device__ __forceinline__ float gss_expf(float x) {
   y = __fma_rn(z, r2, y);
   y = __dmul_rn(y, s);
   return __double2float_rn(y);
+}
+
+__device__ __forceinline__ float gss_expf(float x) {
+  if (!(x <= 0x1.62e42ep6f)) {                 // > 88.72 (overflow), +inf or NaN
+    if (x != x) return x + x;
+    return __int_as_float(0x7f800000);
+  }
+  if (x < -0x1.9fe368p6f) return 0.0f;         // underflow and -inf
+  return gss_expf_core(x);
+}
+
+// gss_expf for x <= 0 or NaN (the compositing exponent -q/2, q >= 0): only the underflow and NaN
+// guards of expf can fire; the result is identical to gss_expf on that domain.
+__device__ __forceinline__ float gss_expf_nonpos(float x) {
+  if (!(x >= -0x1.9fe368p6f)) return (x != x) ? x + x : 0.0f;
+  return gss_expf_core(x);
 }
 
 // std::max(v, 0) as the reference evaluates it ((v < 0) ? 0 : v; NaN passes through).

@@ -36,7 +36,8 @@ struct __align__(16) SplatRec {
   float mx, my, a, b;
   float c, ab, r, g;
   float bl, depth;
-  int32_t off, pad;
+  int32_t off;
+  float det;  // a*c - b*b, evaluated once with the reference's operation order
   int32_t bx0, bx1, by0, by1;  // absolute pixels, half-open, clipped to the window
 };
 static_assert(sizeof(SplatRec) == 64, "record is 4 x 16 B");
@@ -135,7 +136,8 @@ __global__ void preprocess_kernel(SceneDev s, Cam cam, Win w, int64_t V, SplatRe
     r.mx = p.mx; r.my = p.my; r.a = p.a; r.b = p.b; r.c = p.c; r.ab = ab;
     r.r = clamp01(rgb0); r.g = clamp01(rgb1); r.bl = clamp01(rgb2);
     r.depth = t.z;
-    if (p.a * p.c - p.b * p.b > 0.0f) {
+    r.det = p.a * p.c - p.b * p.b;
+    if (r.det > 0.0f) {
       const double mx = (double)p.mx, my = (double)p.my, rad = (double)p.radius;
       const int a0 = d2i_x86(ceil(mx - rad - 0.5));
       const int a1 = (int)((unsigned)d2i_x86(floor(mx + rad - 0.5)) + 1u);
@@ -197,12 +199,12 @@ struct EvalOut {
 };
 
 // contrib_eval (render.hpp:342-358); det > 0 holds for every binned splat (render.hpp:418).
+// The exponent is -q/2 <= 0 (or NaN), so only the underflow / NaN guards of expf apply.
 __device__ __forceinline__ EvalOut contrib_eval(const SplatRec& r, float cx, float cy) {
   EvalOut o;
-  const float det = r.a * r.c - r.b * r.b;
   const float dx = cx - r.mx, dy = cy - r.my;
-  o.q = max0((r.c * dx * dx - 2.0f * r.b * dx * dy + r.a * dy * dy) / det);
-  o.weight = gss_expf(-0.5f * o.q);
+  o.q = max0((r.c * dx * dx - 2.0f * r.b * dx * dy + r.a * dy * dy) / r.det);
+  o.weight = gss_expf_nonpos(-0.5f * o.q);
   const float raw = r.ab * o.weight;
   o.clamped = raw > 0.999f;
   o.alpha = o.clamped ? 0.999f : raw;
@@ -216,6 +218,9 @@ __device__ __forceinline__ void load_rec(SplatRec* dst, const SplatRec* recs, in
 }
 
 // Forward composite (render.hpp:438-462) fused with the L1 loss (render.hpp:497-511).
+// Each warp owns an 8x4 pixel block of the 16x16 tile. After a batch of records is staged in
+// SMEM, the warp ballots which records' pixel boxes intersect its block and walks only those
+// (warp-uniform loop); the per-pixel box test then reproduces the CSR membership exactly.
 __global__ void __launch_bounds__(kTilePix) forward_kernel(const SplatRec* __restrict__ recs,
                                                            const int32_t* __restrict__ vals,
                                                            const int2* __restrict__ ranges, Win w, float bg0,
@@ -227,8 +232,10 @@ __global__ void __launch_bounds__(kTilePix) forward_kernel(const SplatRec* __res
   __shared__ double red[kTilePix / 32];
   const int tile = blockIdx.x;
   const int tx = tile % w.tw, ty = tile / w.tw;
-  const int lx = threadIdx.x % kTileSize, ly = threadIdx.x / kTileSize;
-  const int x = w.px0 + tx * kTileSize + lx, y = w.py0 + ty * kTileSize + ly;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 4;
+  const int fx0 = w.px0 + tx * kTileSize + wx0, fy0 = w.py0 + ty * kTileSize + wy0;  // warp block origin
+  const int x = fx0 + (lane & 7), y = fy0 + (lane >> 3);
   const bool inside = x < w.px0 + w.pw && y < w.py0 + w.ph;
   const float cx = (float)x + 0.5f, cy = (float)y + 0.5f;
   const int2 rg = ranges[tile];
@@ -240,13 +247,23 @@ __global__ void __launch_bounds__(kTilePix) forward_kernel(const SplatRec* __res
     const int nb = min(kFwdBatch, rg.y - b);
     if ((int)threadIdx.x < nb) load_rec(&sh[threadIdx.x], recs, vals[b + threadIdx.x]);
     __syncthreads();
-    if (!done) {
-      for (int j = 0; j < nb; ++j) {
+    for (int c0j = 0; c0j < nb && __any_sync(0xffffffffu, !done); c0j += 32) {
+      const int jl = c0j + lane;
+      bool hit = false;
+      if (jl < nb) {
+        const int4 bx = *reinterpret_cast<const int4*>(&sh[jl].bx0);
+        hit = bx.x <= fx0 + 7 && bx.y > fx0 && bx.z <= fy0 + 3 && bx.w > fy0;
+      }
+      unsigned m = __ballot_sync(0xffffffffu, hit);
+      while (m) {
+        const int j = c0j + __ffs(m) - 1;
+        m &= m - 1;
+        if (done) continue;
         const SplatRec& r = sh[j];
         if (x < r.bx0 || x >= r.bx1 || y < r.by0 || y >= r.by1) continue;
         if (T < 1e-4f) {
           done = true;
-          break;
+          continue;
         }
         const EvalOut ev = contrib_eval(r, cx, cy);
         c0 += r.r * ev.alpha * T;
@@ -282,7 +299,7 @@ __global__ void __launch_bounds__(kTilePix) forward_kernel(const SplatRec* __res
   }
   if (gt) {
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    if (lane == 0) red[warp] = acc;
     __syncthreads();
     if (threadIdx.x == 0) {
       double s = 0.0;
@@ -336,7 +353,7 @@ struct PixB {
 // covariance) so the per-pixel exponent needs no division.
 struct BwdConic {
   float ia, ib, ic;  // c/det, b/det, a/det
-  float inv_det;
+  float nh;          // -0.5/det
 };
 
 __device__ __forceinline__ float ex2_fast(float x) {
@@ -352,14 +369,15 @@ __device__ __forceinline__ float rcp_fast(float x) {
 
 // One contribution of splat r (sweep position jpos) to pixel p: accumulates its 9 screen-space
 // gradient terms into v and steps the pixel's reverse state. Returns whether it contributed.
-// The gradient arithmetic runs on fast math (tolerance-checked); the 0.999 clamp
-// decision, which selects the reference's branch (render.hpp:560-573), is recomputed with the
-// forward's exact arithmetic whenever the fast alpha is within 1e-4 of the threshold, so both
-// passes always take the same branch.
+// The gradient arithmetic runs on fast math with explicit FMAs (tolerance-checked);
+// the 0.999 clamp decision, which selects the reference's branch (render.hpp:560-573), is
+// recomputed with the forward's exact arithmetic whenever the fast alpha is within 1e-4 of the
+// threshold, so both passes always take the same branch.
 __device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k, int jpos, PixB& p, float v[9]) {
   if (!(jpos < p.L && p.x >= r.bx0 && p.x < r.bx1 && p.y >= r.by0 && p.y < r.by1)) return false;
   const float dx = p.cx - r.mx, dy = p.cy - r.my;
-  float q = __fmaf_rn(k.ia * dx, dx, __fmaf_rn(k.ic * dy, dy, -2.0f * k.ib * dx * dy));
+  const float mdxy2 = -2.0f * dx * dy;
+  float q = __fmaf_rn(k.ia * dx, dx, __fmaf_rn(k.ic * dy, dy, k.ib * mdxy2));
   q = q < 0.0f ? 0.0f : q;
   const float weight = ex2_fast(-0.72134752f * q);  // exp(-q/2)
   float raw = r.ab * weight;
@@ -369,24 +387,25 @@ __device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k
   const float inv1m = rcp_fast(1.0f - alpha);
   const float Tb = p.T * inv1m;  // transmittance before this contribution
   const float w_rgb = alpha * Tb;
-  v[0] += w_rgb * p.g0;
-  v[1] += w_rgb * p.g1;
-  v[2] += w_rgb * p.g2;
-  const float dot_c = r.r * p.g0 + r.g * p.g1 + r.bl * p.g2;
-  const float dot_suf = p.s0 * p.g0 + p.s1 * p.g1 + p.s2 * p.g2;
-  const float d_alpha = Tb * dot_c - dot_suf * inv1m;
-  p.s0 += r.r * w_rgb;
-  p.s1 += r.g * w_rgb;
-  p.s2 += r.bl * w_rgb;
+  v[0] = __fmaf_rn(w_rgb, p.g0, v[0]);
+  v[1] = __fmaf_rn(w_rgb, p.g1, v[1]);
+  v[2] = __fmaf_rn(w_rgb, p.g2, v[2]);
+  const float dot_c = __fmaf_rn(r.r, p.g0, __fmaf_rn(r.g, p.g1, r.bl * p.g2));
+  const float dot_suf = __fmaf_rn(p.s0, p.g0, __fmaf_rn(p.s1, p.g1, p.s2 * p.g2));
+  const float d_alpha = __fmaf_rn(Tb, dot_c, -dot_suf * inv1m);
+  p.s0 = __fmaf_rn(r.r, w_rgb, p.s0);
+  p.s1 = __fmaf_rn(r.g, w_rgb, p.s1);
+  p.s2 = __fmaf_rn(r.bl, w_rgb, p.s2);
   p.T = Tb;
   if (!clamped) {  // render.hpp:572-586
-    v[8] += weight * d_alpha;
-    const float dqi = -0.5f * alpha * d_alpha * k.inv_det;
-    v[5] += dqi * (dy * dy - q * r.c);
-    v[6] += dqi * (-2.0f * dx * dy + 2.0f * q * r.b);
-    v[7] += dqi * (dx * dx - q * r.a);
-    v[3] += dqi * (-2.0f * r.c * dx + 2.0f * r.b * dy);
-    v[4] += dqi * (2.0f * r.b * dx - 2.0f * r.a * dy);
+    v[8] = __fmaf_rn(weight, d_alpha, v[8]);
+    const float dqi = alpha * d_alpha * k.nh;
+    const float b2 = 2.0f * r.b;
+    v[5] = __fmaf_rn(dqi, __fmaf_rn(-q, r.c, dy * dy), v[5]);
+    v[6] = __fmaf_rn(dqi, __fmaf_rn(q, b2, mdxy2), v[6]);
+    v[7] = __fmaf_rn(dqi, __fmaf_rn(-q, r.a, dx * dx), v[7]);
+    v[3] = __fmaf_rn(dqi, __fmaf_rn(b2, dy, -2.0f * r.c * dx), v[3]);
+    v[4] = __fmaf_rn(dqi, __fmaf_rn(b2, dx, -2.0f * r.a * dy), v[4]);
   }
   return true;
 }
@@ -415,24 +434,30 @@ __device__ __forceinline__ float warp_reduce_scatter9(const float v[9], int lane
 
 // Reverse sweep (render.hpp:542-589) per 16x16 tile: 128 threads, 2 pixels each (rows ly and
 // ly + 2 of a 4-row warp band), so a splat's 9 gradient terms are pre-summed per lane and
-// reduced once per warp. One partial SlotAcc per (splat, tile) instance, fixed-order sums (no
-// float atomics, deterministic). partial layout: [instance][9] = rgb3, m2d2, cov3, ab.
+// reduced once per warp. Per batch, each warp ballots which records can reach its band (pixel
+// box intersects the band and sweep position < the band's largest last-contribution index) and
+// walks only those. One partial SlotAcc per (splat, tile) instance, fixed-order sums (no float
+// atomics, deterministic). partial layout: [instance][9] = rgb3, m2d2, cov3, ab.
 constexpr int kBwdThreads = kTilePix / 2;
+constexpr int kBwdWarps = kBwdThreads / 32;
 __global__ void __launch_bounds__(kBwdThreads) backward_kernel(const SplatRec* __restrict__ recs,
                                                                const int32_t* __restrict__ vals,
                                                                const int2* __restrict__ ranges, Win w, float bg0,
                                                                float bg1, float bg2, const float* __restrict__ fT_in,
                                                                const int32_t* __restrict__ last_in,
                                                                const float* __restrict__ d_img, float* partials) {
+  static_assert(kBwdBatch == 64, "one 64-bit record mask per warp");
   __shared__ SplatRec sh[kBwdBatch];
   __shared__ BwdConic shk[kBwdBatch];
-  __shared__ float red[kBwdBatch][kBwdThreads / 32][9];
+  __shared__ float red[kBwdBatch][kBwdWarps][9];
+  __shared__ unsigned long long wmask[kBwdWarps];
   __shared__ int smax;
   const int tile = blockIdx.x;
   const int tx = tile % w.tw, ty = tile / w.tw;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lx = lane & 15, ly = warp * 4 + (lane >> 4);
   const int2 rg = ranges[tile];
+  const int bx0w = w.px0 + tx * kTileSize, by0w = w.py0 + ty * kTileSize + warp * 4;  // warp band origin
   PixB px[2];
   int lmax = 0;
 #pragma unroll
@@ -460,8 +485,9 @@ __global__ void __launch_bounds__(kBwdThreads) backward_kernel(const SplatRec* _
     lmax = max(lmax, p.L);
   }
   if (threadIdx.x == 0) smax = 0;
+  const int wl = __reduce_max_sync(0xffffffffu, lmax);  // the band's largest last index
   __syncthreads();
-  if (lmax > 0) atomicMax(&smax, lmax);
+  if (lane == 0 && wl > 0) atomicMax(&smax, wl);
   __syncthreads();
   const int Lmax = smax;
   const int vidx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
@@ -472,11 +498,25 @@ __global__ void __launch_bounds__(kBwdThreads) backward_kernel(const SplatRec* _
     if ((int)threadIdx.x < nb) {
       load_rec(&sh[threadIdx.x], recs, vals[rg.x + bstart + threadIdx.x]);
       const SplatRec& r = sh[threadIdx.x];
-      const float inv = 1.0f / (r.a * r.c - r.b * r.b);  // det > 0 for every binned splat
-      shk[threadIdx.x] = BwdConic{r.c * inv, r.b * inv, r.a * inv, inv};
+      const float inv = 1.0f / r.det;  // det > 0 for every binned splat
+      shk[threadIdx.x] = BwdConic{r.c * inv, r.b * inv, r.a * inv, -0.5f * inv};
     }
     __syncthreads();
-    for (int jj = nb - 1; jj >= 0; --jj) {
+    unsigned long long m = 0;
+#pragma unroll
+    for (int h = 0; h < kBwdBatch / 32; ++h) {
+      const int jl = h * 32 + lane;
+      bool hit = false;
+      if (jl < nb && bstart + jl < wl) {
+        const int4 bx = *reinterpret_cast<const int4*>(&sh[jl].bx0);
+        hit = bx.x <= bx0w + 15 && bx.y > bx0w && bx.z <= by0w + 3 && bx.w > by0w;
+      }
+      m |= (unsigned long long)__ballot_sync(0xffffffffu, hit) << (32 * h);
+    }
+    if (lane == 0) wmask[warp] = m;
+    while (m) {
+      const int jj = 63 - __clzll(m);  // reverse order: back to front
+      m &= ~(1ull << jj);
       const SplatRec r = sh[jj];
       const BwdConic k = shk[jj];
       float v[9];
@@ -492,12 +532,14 @@ __global__ void __launch_bounds__(kBwdThreads) backward_kernel(const SplatRec* _
       }
     }
     __syncthreads();
-    // Fixed-order cross-warp sum, one instance partial per splat of the batch.
+    // Fixed-order cross-warp sum over the warps that walked the record: one instance partial per
+    // splat of the batch.
     for (int e = threadIdx.x; e < nb * 9; e += kBwdThreads) {
       const int jj = e / 9, i = e - jj * 9;
       float s = 0.0f;
 #pragma unroll
-      for (int q = 0; q < kBwdThreads / 32; ++q) s += red[jj][q][i];
+      for (int q = 0; q < kBwdWarps; ++q)
+        if ((wmask[q] >> jj) & 1ull) s += red[jj][q][i];
       const SplatRec& r = sh[jj];
       int tx0, ty0, ntx, nty;
       tile_box(r, w, tx0, ty0, ntx, nty);
