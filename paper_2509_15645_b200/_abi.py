@@ -6,9 +6,11 @@ fallback — on a machine without a GPU every compute entry point returns GSS_ER
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libgss_b200.so"
+# GSS_LIB overrides the library path (kernel-variant experiments built by tools/build_variant.py).
+LIB_PATH = Path(os.environ.get("GSS_LIB") or Path(__file__).resolve().parent / "libgss_b200.so")
 
 GSS_OK, GSS_ERR_CUDA, GSS_ERR_INVALID, GSS_ERR_INVARIANT = 0, 1, 2, 3
 

@@ -37,11 +37,11 @@ def _stale(obj: Path, src: Path) -> bool:
     return any(d.stat().st_mtime > obj.stat().st_mtime for d in deps)
 
 
-def _compile(src: str) -> Path:
+def _compile(src: str, build: Path = BUILD, defines: tuple = ()) -> Path:
     s = CSRC / src
-    o = BUILD / (src + ".o")
+    o = build / (src + ".o")
     if _stale(o, s):
-        cmd = [NVCC, *FLAGS, "-c", str(s), "-o", str(o)]
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", str(s), "-o", str(o)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
@@ -50,18 +50,22 @@ def _compile(src: str) -> Path:
     return o
 
 
-def build_lib(verbose: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build_lib(verbose: bool = False, variant: str = "", defines: tuple = ()) -> Path:
+    """Builds the product library; with `variant`, a copy compiled with extra -D `defines` into
+    _build/var_<variant>/libgss_b200.so (load it with GSS_LIB=...; experiments only)."""
+    build = BUILD / f"var_{variant}" if variant else BUILD
+    lib = build / "libgss_b200.so" if variant else LIB
+    build.mkdir(parents=True, exist_ok=True)
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(_compile, SOURCES))
-    if not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs)]
+        objs = list(ex.map(lambda src: _compile(src, build, defines), SOURCES))
+    if not lib.exists() or any(o.stat().st_mtime > lib.stat().st_mtime for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     if verbose:
-        print(f"built {LIB}")
-    return LIB
+        print(f"built {lib}")
+    return lib
 
 
 def build_oracle(with_ref: bool | None = None) -> None:

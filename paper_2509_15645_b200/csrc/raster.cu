@@ -18,6 +18,8 @@
 //   chain       thread per slot: fixed-order sum of its instance partials, then the reference's
 //               chain through sigmoid, SH and project_geo_backward (render.hpp:600-638).
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
 #include <cstring>
@@ -83,7 +85,7 @@ struct DBuf {
 
 struct gss_render_ctx {
   gssd::DBuf recs, ntiles, offsets, keys_a, keys_b, vals_a, vals_b, cub_tmp, ranges, last, fT, partials, lossp,
-      hostcnt, sums;
+      hostcnt, sums, dkeys_a, dkeys_b, order_a, order_b, slot_off;
   gssd::Win win{};
   gssd::SceneDev sc{};
   gssd::Cam cam{};
@@ -102,7 +104,8 @@ __device__ __forceinline__ const float* ng_row(const SceneDev& s, int k, int id)
 }
 
 // project_all (render.hpp:361-380) + CSR box (render.hpp:297-314, 418-419) + tile count.
-__global__ void preprocess_kernel(SceneDev s, Cam cam, Win w, int64_t V, SplatRec* recs, int32_t* ntiles) {
+__global__ void preprocess_kernel(SceneDev s, Cam cam, Win w, int64_t V, SplatRec* recs, int32_t* ntiles,
+                                  uint32_t* dkey, int32_t* dslot) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= V) return;
   const int id = s.ids[k];
@@ -156,6 +159,9 @@ __global__ void preprocess_kernel(SceneDev s, Cam cam, Win w, int64_t V, SplatRe
   if (nt == 0) r.bx0 = r.bx1 = r.by0 = r.by1 = 0;
   recs[k] = r;
   ntiles[k] = nt;
+  // Depth sort key: binned splats have depth >= near > 0, whose IEEE bits order like the values.
+  dkey[k] = nt > 0 ? __float_as_uint(r.depth) : 0xffffffffu;
+  dslot[k] = (int32_t)k;
 }
 
 __device__ __forceinline__ void tile_box(const SplatRec& r, const Win& w, int& tx0, int& ty0, int& ntx, int& nty) {
@@ -165,32 +171,46 @@ __device__ __forceinline__ void tile_box(const SplatRec& r, const Win& w, int& t
   nty = (r.by1 - 1 - w.py0) / kTileSize - ty0 + 1;
 }
 
-__global__ void duplicate_kernel(const SplatRec* recs, const int32_t* offsets, Win w, int64_t V,
-                                 unsigned long long* keys, int32_t* vals, SplatRec* recs_rw) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= V) return;
-  const SplatRec r = recs[k];
-  const int32_t off = offsets[k];
+// Tile instances in depth order: thread i takes the i-th splat of the stable (depth, slot) sort
+// and emits one (tile) key per touched tile; the stable tile sort that follows keeps depth order
+// (ties in slot = ascending id order) inside each tile, the reference's std::stable_sort order
+// (render.hpp:406-416). Instance numbering follows this order; slot_off[k] / ntiles[k] give slot
+// k's instance range for the backward's per-slot sums.
+__global__ void duplicate_kernel(const SplatRec* recs, const int32_t* order, const int32_t* ntiles,
+                                 const int32_t* offsets, Win w, int64_t V, uint32_t* keys, int32_t* vals,
+                                 SplatRec* recs_rw, int32_t* slot_off) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  const int32_t k = order[i];
+  const int32_t off = offsets[i];
   recs_rw[k].off = off;
-  if (r.bx1 <= r.bx0) return;
+  slot_off[k] = off;
+  if (ntiles[k] == 0) return;
+  const SplatRec r = recs[k];
   int tx0, ty0, ntx, nty;
   tile_box(r, w, tx0, ty0, ntx, nty);
-  const unsigned long long dbits = (unsigned long long)__float_as_uint(r.depth);
   int j = 0;
   for (int ty = ty0; ty < ty0 + nty; ++ty)
     for (int tx = tx0; tx < tx0 + ntx; ++tx, ++j) {
-      const unsigned long long tile = (unsigned long long)(ty * w.tw + tx);
-      keys[off + j] = (tile << 32) | dbits;
-      vals[off + j] = (int32_t)k;
+      keys[off + j] = (uint32_t)(ty * w.tw + tx);
+      vals[off + j] = k;
     }
 }
 
-__global__ void ranges_kernel(const unsigned long long* keys, int64_t I, int2* ranges) {
+// ntiles in sorted order (0 at position V), for the instance-offset scan: offsets[V] = I.
+struct SortedCount {
+  const int32_t* nt;
+  const int32_t* order;
+  int32_t V;
+  __host__ __device__ int32_t operator()(int32_t i) const { return i < V ? nt[order[i]] : 0; }
+};
+
+__global__ void ranges_kernel(const uint32_t* keys, int64_t I, int2* ranges) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= I) return;
-  const int tile = (int)(keys[i] >> 32);
-  if (i == 0 || (int)(keys[i - 1] >> 32) != tile) ranges[tile].x = (int)i;
-  if (i == I - 1 || (int)(keys[i + 1] >> 32) != tile) ranges[tile].y = (int)(i + 1);
+  const uint32_t tile = keys[i];
+  if (i == 0 || keys[i - 1] != tile) ranges[tile].x = (int)i;
+  if (i == I - 1 || keys[i + 1] != tile) ranges[tile].y = (int)(i + 1);
 }
 
 struct EvalOut {
@@ -438,8 +458,13 @@ __device__ __forceinline__ float warp_reduce_scatter9(const float v[9], int lane
 // box intersects the band and sweep position < the band's largest last-contribution index) and
 // walks only those. One partial SlotAcc per (splat, tile) instance, fixed-order sums (no float
 // atomics, deterministic). partial layout: [instance][9] = rgb3, m2d2, cov3, ab.
-constexpr int kBwdThreads = kTilePix / 2;
+#ifndef GSS_BWD_PPT
+#define GSS_BWD_PPT 2
+#endif
+constexpr int kBwdPPT = GSS_BWD_PPT;              // pixels per thread
+constexpr int kBwdThreads = kTilePix / kBwdPPT;
 constexpr int kBwdWarps = kBwdThreads / 32;
+constexpr int kBand = 2 * kBwdPPT;                // rows per warp band
 __global__ void __launch_bounds__(kBwdThreads) backward_kernel(const SplatRec* __restrict__ recs,
                                                                const int32_t* __restrict__ vals,
                                                                const int2* __restrict__ ranges, Win w, float bg0,
@@ -455,13 +480,13 @@ __global__ void __launch_bounds__(kBwdThreads) backward_kernel(const SplatRec* _
   const int tile = blockIdx.x;
   const int tx = tile % w.tw, ty = tile / w.tw;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int lx = lane & 15, ly = warp * 4 + (lane >> 4);
+  const int lx = lane & 15, ly = warp * kBand + (lane >> 4);
   const int2 rg = ranges[tile];
-  const int bx0w = w.px0 + tx * kTileSize, by0w = w.py0 + ty * kTileSize + warp * 4;  // warp band origin
-  PixB px[2];
+  const int bx0w = w.px0 + tx * kTileSize, by0w = w.py0 + ty * kTileSize + warp * kBand;  // warp band origin
+  PixB px[kBwdPPT];
   int lmax = 0;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < kBwdPPT; ++h) {
     PixB& p = px[h];
     p.x = w.px0 + tx * kTileSize + lx;
     p.y = w.py0 + ty * kTileSize + ly + 2 * h;
@@ -495,11 +520,11 @@ __global__ void __launch_bounds__(kBwdThreads) backward_kernel(const SplatRec* _
     const int bstart = max(0, bend - kBwdBatch);
     const int nb = bend - bstart;
     __syncthreads();
-    if ((int)threadIdx.x < nb) {
-      load_rec(&sh[threadIdx.x], recs, vals[rg.x + bstart + threadIdx.x]);
-      const SplatRec& r = sh[threadIdx.x];
+    for (int j = threadIdx.x; j < nb; j += kBwdThreads) {
+      load_rec(&sh[j], recs, vals[rg.x + bstart + j]);
+      const SplatRec& r = sh[j];
       const float inv = 1.0f / r.det;  // det > 0 for every binned splat
-      shk[threadIdx.x] = BwdConic{r.c * inv, r.b * inv, r.a * inv, -0.5f * inv};
+      shk[j] = BwdConic{r.c * inv, r.b * inv, r.a * inv, -0.5f * inv};
     }
     __syncthreads();
     unsigned long long m = 0;
@@ -509,7 +534,7 @@ __global__ void __launch_bounds__(kBwdThreads) backward_kernel(const SplatRec* _
       bool hit = false;
       if (jl < nb && bstart + jl < wl) {
         const int4 bx = *reinterpret_cast<const int4*>(&sh[jl].bx0);
-        hit = bx.x <= bx0w + 15 && bx.y > bx0w && bx.z <= by0w + 3 && bx.w > by0w;
+        hit = bx.x <= bx0w + 15 && bx.y > bx0w && bx.z <= by0w + kBand - 1 && bx.w > by0w;
       }
       m |= (unsigned long long)__ballot_sync(0xffffffffu, hit) << (32 * h);
     }
@@ -522,8 +547,9 @@ __global__ void __launch_bounds__(kBwdThreads) backward_kernel(const SplatRec* _
       float v[9];
 #pragma unroll
       for (int i = 0; i < 9; ++i) v[i] = 0.0f;
-      bool act = bwd_contrib(r, k, bstart + jj, px[0], v);
-      act |= bwd_contrib(r, k, bstart + jj, px[1], v);
+      bool act = false;
+#pragma unroll
+      for (int h = 0; h < kBwdPPT; ++h) act |= bwd_contrib(r, k, bstart + jj, px[h], v);
       if (__any_sync(0xffffffffu, act)) {
         const float tot = warp_reduce_scatter9(v, lane);
         if ((lane & 1) == 0 && vidx < 9) red[jj][warp][vidx] = tot;
@@ -556,7 +582,8 @@ __global__ void __launch_bounds__(kBwdThreads) backward_kernel(const SplatRec* _
 // splats (near-camera Gaussians cover hundreds of tiles) cooperatively, 4x unrolled, with a
 // fixed butterfly. Light on registers, so many warps hide the load latency.
 constexpr int kSumThreads = 256;
-__global__ void __launch_bounds__(kSumThreads) slot_sum_kernel(int64_t V, const int32_t* offsets,
+__global__ void __launch_bounds__(kSumThreads) slot_sum_kernel(int64_t V, const int32_t* slot_off,
+                                                               const int32_t* ntiles,
                                                                const float* __restrict__ partials, float* sums) {
   constexpr int kHead = 32;
   const int lane = threadIdx.x & 31;
@@ -565,8 +592,8 @@ __global__ void __launch_bounds__(kSumThreads) slot_sum_kernel(int64_t V, const 
   if (kw >= V) return;
   int32_t o0 = 0, o1 = 0;
   if (k < V) {
-    o0 = offsets[k];
-    o1 = offsets[k + 1];
+    o0 = slot_off[k];
+    o1 = o0 + ntiles[k];
   }
   float acc[9];
 #pragma unroll
@@ -919,47 +946,67 @@ void rasterize_forward(gss_render_ctx* ctx, const gss_render_scene* scene, const
   SplatRec* recs = static_cast<SplatRec*>(ctx->recs.get((size_t)V * sizeof(SplatRec), st));
   int32_t* nt = static_cast<int32_t*>(ctx->ntiles.get((size_t)(V + 1) * 4, st));
   int32_t* offs = static_cast<int32_t*>(ctx->offsets.get((size_t)(V + 1) * 4, st));
-  preprocess_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(s, ctx->cam, w, V, recs, nt);
+  int32_t* soff = static_cast<int32_t*>(ctx->slot_off.get((size_t)V * 4, st));
+  auto* dka = static_cast<uint32_t*>(ctx->dkeys_a.get((size_t)V * 4, st));
+  auto* dkb = static_cast<uint32_t*>(ctx->dkeys_b.get((size_t)V * 4, st));
+  auto* oa = static_cast<int32_t*>(ctx->order_a.get((size_t)V * 4, st));
+  auto* ob = static_cast<int32_t*>(ctx->order_b.get((size_t)V * 4, st));
+  preprocess_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(s, ctx->cam, w, V, recs, nt, dka, oa);
   GSS_LAUNCHED();
-  GSS_CUDA(cudaMemsetAsync(nt + V, 0, 4, st));
+  // 1. stable sort of the V splats by depth (slot order breaks ties = ascending id).
+  cub::DoubleBuffer<uint32_t> ddk(dka, dkb);
+  cub::DoubleBuffer<int32_t> ddv(oa, ob);
+  size_t db = 0;
+  GSS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, db, ddk, ddv, (int)V, 0, 32, st));
+  // 2. instance offsets in depth order; offs[V] = I.
+  using CountIt = thrust::transform_iterator<SortedCount, thrust::counting_iterator<int32_t>>;
   size_t tb = 0;
-  GSS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, nt, offs, (int)(V + 1), st));
-  void* tmp = ctx->cub_tmp.get(tb, st);
-  GSS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nt, offs, (int)(V + 1), st));
+  GSS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, CountIt(thrust::counting_iterator<int32_t>(0),
+                                                                  SortedCount{nt, nullptr, (int32_t)V}),
+                                         offs, (int)(V + 1), st));
+  void* tmp = ctx->cub_tmp.get(std::max(db, tb), st);
+  GSS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, db, ddk, ddv, (int)V, 0, 32, st));
+  count_launch();
+  const int32_t* order = ddv.Current();
+  GSS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, CountIt(thrust::counting_iterator<int32_t>(0),
+                                                              SortedCount{nt, order, (int32_t)V}),
+                                         offs, (int)(V + 1), st));
   count_launch();
   GSS_CUDA(cudaMemcpyAsync(ctx->pinned + 1, offs + V, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   GSS_CUDA(cudaStreamSynchronize(st));
   const int64_t I = (int64_t)(reinterpret_cast<int32_t*>(ctx->pinned + 1)[0]);
-  require(I >= 0, "rasterize_forward: tile instance count overflow");
+  require(I >= 0 && I <= INT32_MAX, "rasterize_forward: tile instance count overflow");
   ctx->I = I;
   const int ntile = w.tw * w.th;
   int2* ranges = static_cast<int2*>(ctx->ranges.get((size_t)ntile * sizeof(int2), st));
   GSS_CUDA(cudaMemsetAsync(ranges, 0, (size_t)ntile * sizeof(int2), st));
   int32_t* vals_sorted = nullptr;
-  if (I > 0) {
-    auto* ka = static_cast<unsigned long long*>(ctx->keys_a.get((size_t)I * 8, st));
-    auto* kb = static_cast<unsigned long long*>(ctx->keys_b.get((size_t)I * 8, st));
-    auto* va = static_cast<int32_t*>(ctx->vals_a.get((size_t)I * 4, st));
-    auto* vb = static_cast<int32_t*>(ctx->vals_b.get((size_t)I * 4, st));
-    duplicate_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(recs, offs, w, V, ka, va, recs);
+  {
+    auto* ka = static_cast<uint32_t*>(ctx->keys_a.get((size_t)std::max<int64_t>(I, 1) * 4, st));
+    auto* kb = static_cast<uint32_t*>(ctx->keys_b.get((size_t)std::max<int64_t>(I, 1) * 4, st));
+    auto* va = static_cast<int32_t*>(ctx->vals_a.get((size_t)std::max<int64_t>(I, 1) * 4, st));
+    auto* vb = static_cast<int32_t*>(ctx->vals_b.get((size_t)std::max<int64_t>(I, 1) * 4, st));
+    duplicate_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(recs, order, nt, offs, w, V, ka, va, recs, soff);
     GSS_LAUNCHED();
-    int tile_bits = 1;
-    while ((1ll << tile_bits) < ntile) ++tile_bits;
-    cub::DoubleBuffer<unsigned long long> dk(ka, kb);
-    cub::DoubleBuffer<int32_t> dv(va, vb);
-    size_t sb = 0;
-    GSS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sb, dk, dv, (int)I, 0, 32 + tile_bits, st));
-    void* stmp = ctx->cub_tmp.get(std::max(sb, tb), st);
-    GSS_CUDA(cub::DeviceRadixSort::SortPairs(stmp, sb, dk, dv, (int)I, 0, 32 + tile_bits, st));
-    count_launch();
-    vals_sorted = dv.Current();
-    // keep the sorted arrays addressable for backward
-    if (dk.Current() != ka) std::swap(ctx->keys_a, ctx->keys_b);
-    if (dv.Current() != va) std::swap(ctx->vals_a, ctx->vals_b);
-    ranges_kernel<<<(unsigned)ceil_div(I, 256), 256, 0, st>>>(dk.Current(), I, ranges);
-    GSS_LAUNCHED();
-  } else {
-    vals_sorted = static_cast<int32_t*>(ctx->vals_a.get(16, st));
+    vals_sorted = va;
+    if (I > 0) {
+      // 3. stable sort of the instances by tile (only the tile bits).
+      int tile_bits = 1;
+      while ((1ll << tile_bits) < ntile) ++tile_bits;
+      cub::DoubleBuffer<uint32_t> dk(ka, kb);
+      cub::DoubleBuffer<int32_t> dv(va, vb);
+      size_t sb = 0;
+      GSS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sb, dk, dv, (int)I, 0, tile_bits, st));
+      void* stmp = ctx->cub_tmp.get(std::max(sb, std::max(db, tb)), st);
+      GSS_CUDA(cub::DeviceRadixSort::SortPairs(stmp, sb, dk, dv, (int)I, 0, tile_bits, st));
+      count_launch();
+      vals_sorted = dv.Current();
+      // keep the sorted arrays addressable for backward
+      if (dk.Current() != ka) std::swap(ctx->keys_a, ctx->keys_b);
+      if (dv.Current() != va) std::swap(ctx->vals_a, ctx->vals_b);
+      ranges_kernel<<<(unsigned)ceil_div(I, 256), 256, 0, st>>>(dk.Current(), I, ranges);
+      GSS_LAUNCHED();
+    }
   }
   double* lp = gt ? static_cast<double*>(ctx->lossp.get((size_t)ntile * 8, st)) : nullptr;
   forward_kernel<<<ntile, kTilePix, 0, st>>>(recs, vals_sorted, ranges, w, s.bg[0], s.bg[1], s.bg[2], image, fT, last,
@@ -1005,7 +1052,8 @@ void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int6
   const int64_t npix = (int64_t)w.pw * w.ph;
   require(npix == 0 || d_img, "rasterize_backward: null d_img");
   const SplatRec* recs = static_cast<const SplatRec*>(ctx->recs.p);
-  const int32_t* offs = static_cast<const int32_t*>(ctx->offsets.p);
+  const int32_t* soff = static_cast<const int32_t*>(ctx->slot_off.p);
+  const int32_t* nts = static_cast<const int32_t*>(ctx->ntiles.p);
   float* partials = static_cast<float*>(ctx->partials.get((size_t)std::max<int64_t>(I, 1) * 9 * 4, st));
   if (I > 0 && npix > 0) {
     GSS_CUDA(cudaMemsetAsync(partials, 0, (size_t)I * 9 * 4, st));
@@ -1019,7 +1067,7 @@ void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int6
     GSS_CUDA(cudaMemsetAsync(partials, 0, (size_t)I * 9 * 4, st));
   }
   float* sums = static_cast<float*>(ctx->sums.get((size_t)V * 9 * 4, st));
-  slot_sum_kernel<<<(unsigned)ceil_div(V, kSumThreads), kSumThreads, 0, st>>>(V, offs, partials, sums);
+  slot_sum_kernel<<<(unsigned)ceil_div(V, kSumThreads), kSumThreads, 0, st>>>(V, soff, nts, partials, sums);
   GSS_LAUNCHED();
   {
     const unsigned cb = (unsigned)ceil_div(V, kChainThreads);
@@ -1039,7 +1087,8 @@ void render_ctx_destroy(gss_render_ctx* ctx) {
   if (!ctx) return;
   cudaStream_t st = ctx->last_stream;
   for (DBuf* b : {&ctx->recs, &ctx->ntiles, &ctx->offsets, &ctx->keys_a, &ctx->keys_b, &ctx->vals_a, &ctx->vals_b,
-                  &ctx->cub_tmp, &ctx->ranges, &ctx->last, &ctx->fT, &ctx->partials, &ctx->lossp, &ctx->hostcnt, &ctx->sums})
+                  &ctx->cub_tmp, &ctx->ranges, &ctx->last, &ctx->fT, &ctx->partials, &ctx->lossp, &ctx->hostcnt, &ctx->sums, &ctx->dkeys_a, &ctx->dkeys_b, &ctx->order_a, &ctx->order_b,
+                  &ctx->slot_off})
     b->release(st);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
