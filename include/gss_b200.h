@@ -171,6 +171,50 @@ int gss_loss_l1(const float* image, const float* gt, int64_t elems, int64_t norm
 int gss_rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* grad_geo, int64_t geo_stride,
                            float* grad_nongeo, int64_t ng_stride, float* mean2d_opt, gss_stream_t stream);
 
+/* ---- split-phase rasterizer: image-parallel rendering over N GPUs --------- */
+/* The reference renders a view on one process (render.hpp:384-640) and splits it only into two
+ * viewports (engine.hpp:266-273, splitter.hpp:31-123). Across GPUs the view is cut into column
+ * strips: each GPU projects ITS Gaussians (a contiguous id shard) into splat records, ships every
+ * record to the owner of each strip its pixel box touches, the strip owner composites the records
+ * it received from all GPUs in (shard, slot) order = ascending global id, and the 9-float
+ * screen-space gradient sums (the SlotAcc cut, render.hpp:538) travel back to the record owner,
+ * which sums them in strip order and runs the chain (render.hpp:600-638) locally. Per-pixel
+ * contribution lists equal the single-GPU ones, so strip images are bit-identical to the
+ * unsplit image. */
+#define GSS_SPLAT_RECORD_BYTES 64
+/* project_all (render.hpp:361-380) of the scene's visible slots: records[k] (64 B each, device)
+ * for slot k, pixel box clipped to vp. Host-known count only. */
+int gss_project(const gss_render_scene* scene, const gss_camera* cam, const gss_viewport* vp, void* records,
+                gss_stream_t stream);
+/* Strip routing: strip k = pixel columns [strip_x[k], strip_x[k+1]) (strip_x: host, nstrips+1
+ * ascending). dest_slots (device, nstrips*count) row k receives the ascending slots whose box
+ * touches strip k; dest_counts (device int64[nstrips]) their numbers. */
+int gss_route_strips(const void* records, int64_t count, const int32_t* strip_x, int32_t nstrips,
+                     int32_t* dest_slots, int64_t* dest_counts, gss_stream_t stream);
+/* out[i] = records[slots[i]] (packing a send buffer). */
+int gss_gather_records(const void* records, const int32_t* slots, int64_t n, void* out, gss_stream_t stream);
+/* dst[slots[j]*width + c] += src[j*width + c]; each slot at most once per call (call in strip
+ * order for a fixed-order sum). */
+int gss_scatter_add_rows(const float* src, const int32_t* slots, int64_t n, int32_t width, float* dst,
+                         gss_stream_t stream);
+/* Composite received records (ties in depth broken by record order) on window vp, as
+ * gss_rasterize_forward does after projection; background[3] (host). loss_sum_dev (optional
+ * device double) receives the fp64 sum of |image - gt| of the window, so strip losses add up to the
+ * unsplit fp64 sum before the single float cast (render.hpp:510). */
+int gss_rasterize_records_forward(gss_render_ctx* ctx, const void* records, int64_t count, const gss_camera* cam,
+                                  const gss_viewport* vp, const float* background, float* image, const float* gt,
+                                  int64_t normalizer, float* d_img, float* loss_dev, double* loss_sum_dev,
+                                  float* final_T_opt, int32_t* n_contrib_opt, int64_t* meta_host,
+                                  gss_stream_t stream);
+/* Per-record 9-float screen-space gradient sums (rgb3, mean2d2, cov3, alpha_base; device
+ * count*9) of the ctx's last records forward. */
+int gss_rasterize_records_backward(gss_render_ctx* ctx, const float* d_img, float* sums, gss_stream_t stream);
+/* The per-Gaussian chain (render.hpp:600-638): sums (device V*9, per slot of scene, summed over
+ * strips) + the records gss_project produced -> gradient rows as gss_rasterize_backward. */
+int gss_chain_backward(const gss_render_scene* scene, const gss_camera* cam, const void* records, const float* sums,
+                       float* grad_geo, int64_t geo_stride, float* grad_nongeo, int64_t ng_stride, float* mean2d_opt,
+                       gss_stream_t stream);
+
 /* ---- offload engine (engine.hpp:55-522) ------------------------------------------------- */
 /* OptimConfig (store.hpp:110-145) + EngineConfig (engine.hpp:30-49). */
 typedef struct {

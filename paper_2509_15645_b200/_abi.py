@@ -137,6 +137,14 @@ SIGNATURES = {
                                         C.POINTER(GssViewport), P, P, I64, P, P, P, P, P, P]),
     "gss_loss_l1": (C.c_int, [P, P, I64, I64, P, P, P]),
     "gss_rasterize_backward": (C.c_int, [P, P, P, I64, P, I64, P, P]),
+    "gss_project": (C.c_int, [C.POINTER(GssRenderScene), C.POINTER(GssCamera), C.POINTER(GssViewport), P, P]),
+    "gss_route_strips": (C.c_int, [P, I64, P, I32, P, P, P]),
+    "gss_gather_records": (C.c_int, [P, P, I64, P, P]),
+    "gss_scatter_add_rows": (C.c_int, [P, P, I64, I32, P, P]),
+    "gss_rasterize_records_forward": (C.c_int, [P, P, I64, C.POINTER(GssCamera), C.POINTER(GssViewport), P, P, P,
+                                                I64, P, P, P, P, P, P, P]),
+    "gss_rasterize_records_backward": (C.c_int, [P, P, P, P]),
+    "gss_chain_backward": (C.c_int, [C.POINTER(GssRenderScene), C.POINTER(GssCamera), P, P, P, I64, P, I64, P, P]),
     "gss_engine_config_default": (None, [C.POINTER(GssEngineConfig)]),
     "gss_engine_create": (P, [I64, P, I32, P, P, C.POINTER(GssEngineConfig)]),
     "gss_engine_destroy": (None, [P]),

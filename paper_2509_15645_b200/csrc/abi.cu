@@ -33,6 +33,19 @@ void loss_l1(const float* image, const float* gt, int64_t elems, int64_t normali
              cudaStream_t st);
 void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int64_t gstride, float* gn,
                         int64_t nstride, float* mean2d, cudaStream_t st);
+void project(const gss_render_scene* scene, const gss_camera* cam, const gss_viewport* vp, void* records,
+             cudaStream_t st);
+void route_strips(const void* records, int64_t count, const int32_t* strip_x, int nstrips, int32_t* dest_slots,
+                  int64_t* dest_counts, cudaStream_t st);
+void gather_records(const void* records, const int32_t* slots, int64_t n, void* out, cudaStream_t st);
+void scatter_add_rows(const float* src, const int32_t* slots, int64_t n, int width, float* dst, cudaStream_t st);
+void rasterize_records_forward(gss_render_ctx* ctx, const void* records, int64_t count, const gss_camera* cam,
+                               const gss_viewport* vp, const float* background, float* image, const float* gt,
+                               int64_t normalizer, float* d_img, float* loss_dev, double* loss_sum_dev,
+                               float* final_T_opt, int32_t* ncontrib_opt, int64_t* meta, cudaStream_t st);
+void rasterize_records_backward(gss_render_ctx* ctx, const float* d_img, float* sums, cudaStream_t st);
+void chain_backward(const gss_render_scene* scene, const gss_camera* cam, const void* records, const float* sums,
+                    float* gg, int64_t gstride, float* gn, int64_t nstride, float* mean2d, cudaStream_t st);
 // engine.cu
 void engine_config_default(gss_engine_config* c);
 gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss_camera* cams, const float* gts,
@@ -87,7 +100,7 @@ using namespace gssd;
 #define GSS_API extern "C" __attribute__((visibility("default")))
 
 GSS_API const char* gss_last_error(void) { return t_err.c_str(); }
-GSS_API int32_t gss_abi_version(void) { return 1; }
+GSS_API int32_t gss_abi_version(void) { return 2; }
 GSS_API int32_t gss_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) {
@@ -196,6 +209,67 @@ GSS_API int gss_rasterize_backward(gss_render_ctx* ctx, const float* d_img, floa
   return guarded([&] {
     require_device();
     rasterize_backward(ctx, d_img, grad_geo, geo_stride, grad_nongeo, ng_stride, mean2d_opt, as_stream(stream));
+  });
+}
+
+GSS_API int gss_project(const gss_render_scene* scene, const gss_camera* cam, const gss_viewport* vp,
+                        void* records, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    project(scene, cam, vp, records, as_stream(stream));
+  });
+}
+
+GSS_API int gss_route_strips(const void* records, int64_t count, const int32_t* strip_x, int32_t nstrips,
+                             int32_t* dest_slots, int64_t* dest_counts, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    route_strips(records, count, strip_x, nstrips, dest_slots, dest_counts, as_stream(stream));
+  });
+}
+
+GSS_API int gss_gather_records(const void* records, const int32_t* slots, int64_t n, void* out, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    gather_records(records, slots, n, out, as_stream(stream));
+  });
+}
+
+GSS_API int gss_scatter_add_rows(const float* src, const int32_t* slots, int64_t n, int32_t width, float* dst,
+                                 gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    scatter_add_rows(src, slots, n, width, dst, as_stream(stream));
+  });
+}
+
+GSS_API int gss_rasterize_records_forward(gss_render_ctx* ctx, const void* records, int64_t count,
+                                          const gss_camera* cam, const gss_viewport* vp, const float* background,
+                                          float* image, const float* gt, int64_t normalizer, float* d_img,
+                                          float* loss_dev, double* loss_sum_dev, float* final_T_opt,
+                                          int32_t* n_contrib_opt, int64_t* meta_host, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    rasterize_records_forward(ctx, records, count, cam, vp, background, image, gt, normalizer, d_img, loss_dev,
+                              loss_sum_dev, final_T_opt, n_contrib_opt, meta_host, as_stream(stream));
+  });
+}
+
+GSS_API int gss_rasterize_records_backward(gss_render_ctx* ctx, const float* d_img, float* sums,
+                                           gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    rasterize_records_backward(ctx, d_img, sums, as_stream(stream));
+  });
+}
+
+GSS_API int gss_chain_backward(const gss_render_scene* scene, const gss_camera* cam, const void* records,
+                               const float* sums, float* grad_geo, int64_t geo_stride, float* grad_nongeo,
+                               int64_t ng_stride, float* mean2d_opt, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    chain_backward(scene, cam, records, sums, grad_geo, geo_stride, grad_nongeo, ng_stride, mean2d_opt,
+                   as_stream(stream));
   });
 }
 

@@ -158,10 +158,62 @@ __global__ void preprocess_kernel(SceneDev s, Cam cam, Win w, int64_t V, SplatRe
   }
   if (nt == 0) r.bx0 = r.bx1 = r.by0 = r.by1 = 0;
   recs[k] = r;
+  if (!ntiles) return;  // projection only (gss_project)
   ntiles[k] = nt;
   // Depth sort key: binned splats have depth >= near > 0, whose IEEE bits order like the values.
   dkey[k] = nt > 0 ? __float_as_uint(r.depth) : 0xffffffffu;
   dslot[k] = (int32_t)k;
+}
+
+// Records projected against a larger window (another GPU's projection of the whole view),
+// re-clipped to this window w (an image strip): the reference box of a splat is the same for
+// every window, only its clip differs, so per-pixel contribution lists are unchanged.
+__global__ void clip_kernel(const SplatRec* in, int64_t V, Win w, SplatRec* recs, int32_t* ntiles, uint32_t* dkey,
+                            int32_t* dslot) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= V) return;
+  SplatRec r = in[k];
+  int nt = 0;
+  if (r.bx1 > r.bx0 && r.by1 > r.by0) {
+    const int wx1 = w.px0 + w.pw, wy1 = w.py0 + w.ph;
+    r.bx0 = max(w.px0, r.bx0); r.bx1 = min(wx1, r.bx1);
+    r.by0 = max(w.py0, r.by0); r.by1 = min(wy1, r.by1);
+    if (r.bx0 < r.bx1 && r.by0 < r.by1) {
+      const int tx0 = (r.bx0 - w.px0) / kTileSize, tx1 = (r.bx1 - 1 - w.px0) / kTileSize;
+      const int ty0 = (r.by0 - w.py0) / kTileSize, ty1 = (r.by1 - 1 - w.py0) / kTileSize;
+      nt = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+    }
+  }
+  if (nt == 0) r.bx0 = r.bx1 = r.by0 = r.by1 = 0;
+  recs[k] = r;
+  ntiles[k] = nt;
+  dkey[k] = nt > 0 ? __float_as_uint(r.depth) : 0xffffffffu;
+  dslot[k] = (int32_t)k;
+}
+
+// Image-strip routing: does record k's pixel box touch columns [x0, x1)?
+struct StripHit {
+  const SplatRec* recs;
+  int x0, x1;
+  __host__ __device__ bool operator()(int32_t k) const {
+    const SplatRec& r = recs[k];
+    return r.bx1 > r.bx0 && r.by1 > r.by0 && r.bx0 < x1 && r.bx1 > x0;
+  }
+};
+
+__global__ void gather_records_kernel(const SplatRec* recs, const int32_t* slots, int64_t n, SplatRec* out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = recs[slots[i]];
+}
+
+// dst[slots[j]][c] += src[j][c]: one strip's returned partials; each slot appears at most once per
+// call, so calls in strip order give a fixed-order (deterministic) sum.
+__global__ void scatter_add_rows_kernel(const float* src, const int32_t* slots, int64_t n, int width, float* dst) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n * width) return;
+  const int64_t j = e / width;
+  const int c = (int)(e - j * width);
+  dst[(int64_t)slots[j] * width + c] += src[e];
 }
 
 __device__ __forceinline__ void tile_box(const SplatRec& r, const Win& w, int& tx0, int& ty0, int& ntx, int& nty) {
@@ -349,7 +401,7 @@ __global__ void loss_partial_kernel(const float* img, const float* gt, int64_t n
 }
 
 // Fixed-order final reduction: loss = float(sum) * inv (render.hpp:510).
-__global__ void loss_final_kernel(const double* partials, int n, float inv, float* loss) {
+__global__ void loss_final_kernel(const double* partials, int n, float inv, float* loss, double* sum_out) {
   __shared__ double red[32];
   double acc = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partials[i];
@@ -360,6 +412,7 @@ __global__ void loss_final_kernel(const double* partials, int n, float inv, floa
     double s = 0.0;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
     *loss = (float)s * inv;
+    if (sum_out) *sum_out = s;
   }
 }
 
@@ -852,18 +905,6 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(SceneDev s, Cam ca
   }
 }
 
-__global__ void fill_bg_kernel(float* image, float* fT, int32_t* last, int32_t* nc, int64_t npix, float b0, float b1,
-                               float b2) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= npix) return;
-  image[i * 3] = b0;
-  image[i * 3 + 1] = b1;
-  image[i * 3 + 2] = b2;
-  fT[i] = 1.0f;
-  last[i] = 0;
-  if (nc) nc[i] = 0;
-}
-
 Win make_window(const gss_viewport& vp) {
   // viewport_pixels (render.hpp:297-304)
   auto cvt = [](double d) -> int {
@@ -886,18 +927,19 @@ Win make_window(const gss_viewport& vp) {
 
 }  // namespace
 
-void rasterize_forward(gss_render_ctx* ctx, const gss_render_scene* scene, const gss_camera* cam,
-                       const gss_viewport* vp, float* image, const float* gt, int64_t normalizer, float* d_img,
-                       float* loss_dev, float* final_T_opt, int32_t* ncontrib_opt, int64_t* meta, cudaStream_t st) {
-  require(ctx && scene && cam && vp && image, "rasterize_forward: null argument");
+namespace {
+
+void set_scene(gss_render_ctx* ctx, const gss_render_scene* scene) {
   require(scene->sh_degree >= 0 && scene->sh_degree <= 3, "rasterize_forward: sh_degree must be in [0,3]");
-  require(!gt || (d_img && loss_dev), "rasterize_forward: gt needs d_img and loss_dev");
   require(scene->geo_stride >= 10 && scene->nongeo_stride >= 49, "rasterize_forward: bad strides");
-  ctx->last_stream = st;
-  if (!ctx->pinned) GSS_CUDA(cudaMallocHost(&ctx->pinned, 4 * sizeof(int64_t)));
-  const Win w = make_window(*vp);
-  require(!gt || (w.px0 + w.pw <= cam->width && w.py0 + w.ph <= cam->height),
-          "compute_loss_l1: image and ground-truth shapes differ");
+  SceneDev& s = ctx->sc;
+  s.ids = scene->ids; s.geo = scene->geo; s.geo_stride = scene->geo_stride; s.nongeo = scene->nongeo;
+  s.ng_stride = scene->nongeo_stride; s.compact = scene->nongeo_compact; s.slot_map = scene->slot_map;
+  s.sh_degree = scene->sh_degree; s.lp = scene->low_pass;
+  for (int c = 0; c < 3; ++c) s.bg[c] = scene->background[c];
+}
+
+int64_t scene_count(gss_render_ctx* ctx, const gss_render_scene* scene, cudaStream_t st) {
   int64_t V = scene->count;
   if (scene->count_dev) {
     GSS_CUDA(cudaMemcpyAsync(ctx->pinned, scene->count_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -905,83 +947,78 @@ void rasterize_forward(gss_render_ctx* ctx, const gss_render_scene* scene, const
     V = ctx->pinned[0];
   }
   require(V >= 0 && V <= INT32_MAX, "rasterize_forward: visible count out of range");
-  SceneDev& s = ctx->sc;
-  s.ids = scene->ids; s.geo = scene->geo; s.geo_stride = scene->geo_stride; s.nongeo = scene->nongeo;
-  s.ng_stride = scene->nongeo_stride; s.compact = scene->nongeo_compact; s.slot_map = scene->slot_map;
-  s.sh_degree = scene->sh_degree; s.lp = scene->low_pass;
-  for (int c = 0; c < 3; ++c) s.bg[c] = scene->background[c];
-  std::memcpy(&ctx->cam, cam, sizeof(Cam));
-  ctx->win = w;
-  ctx->V = V;
-  ctx->I = 0;
-  ctx->have_forward = 1;
+  return V;
+}
+
+struct FwdOut {
+  float* image;
+  const float* gt;
+  int gt_width;
+  float inv;
+  float* d_img;
+  float* loss_dev;
+  double* loss_sum;
+  float* final_T;
+  int32_t* ncontrib;
+  int64_t* meta;
+};
+
+// Everything after the records exist: common to rasterize_forward (records from preprocess) and
+// the image-parallel strip forward (records received from other GPUs, re-clipped). Expects
+// ctx->recs / ntiles / dkeys_a / order_a filled for V records, boxes clipped to w.
+void bin_and_composite(gss_render_ctx* ctx, const Win& w, int64_t V, const FwdOut& o, cudaStream_t st) {
+  const SceneDev& s = ctx->sc;
   const int64_t npix = (int64_t)w.pw * w.ph;
   float* fT = static_cast<float*>(ctx->fT.get((size_t)std::max<int64_t>(npix, 1) * 4, st));
   int32_t* last = static_cast<int32_t*>(ctx->last.get((size_t)std::max<int64_t>(npix, 1) * 4, st));
-  const float inv = gt ? 1.0f / (float)(double)(normalizer > 0 ? normalizer : npix * 3) : 0.0f;
-  if (npix == 0) {
-    if (gt) GSS_CUDA(cudaMemsetAsync(loss_dev, 0, sizeof(float), st));
-    if (meta) { meta[0] = w.px0; meta[1] = w.py0; meta[2] = w.pw; meta[3] = w.ph; meta[4] = V; meta[5] = 0; }
-    return;
-  }
-  if (V == 0) {
-    fill_bg_kernel<<<(unsigned)ceil_div(npix, 256), 256, 0, st>>>(image, fT, last, ncontrib_opt, npix, s.bg[0],
-                                                                  s.bg[1], s.bg[2]);
-    GSS_LAUNCHED();
-    if (final_T_opt) GSS_CUDA(cudaMemcpyAsync(final_T_opt, fT, npix * 4, cudaMemcpyDeviceToDevice, st));
-    if (gt) {
-      const int blocks = (int)std::min<int64_t>(ceil_div(npix * 3, 256), 1024);
-      double* lp = static_cast<double*>(ctx->lossp.get((size_t)blocks * 8, st));
-      // gt window == full image only when the window covers it; extract rows for a sub-window.
-      require(w.pw == cam->width && w.px0 == 0, "loss on an empty scene needs a full-width window");
-      loss_partial_kernel<<<blocks, 256, 0, st>>>(image, gt + (int64_t)w.py0 * cam->width * 3, npix * 3, inv, d_img,
-                                                  lp);
-      GSS_LAUNCHED();
-      loss_final_kernel<<<1, 1024, 0, st>>>(lp, blocks, inv, loss_dev);
-      GSS_LAUNCHED();
+  auto write_meta = [&](int64_t I) {
+    if (o.meta) {
+      o.meta[0] = w.px0; o.meta[1] = w.py0; o.meta[2] = w.pw; o.meta[3] = w.ph; o.meta[4] = V; o.meta[5] = I;
     }
-    if (meta) { meta[0] = w.px0; meta[1] = w.py0; meta[2] = w.pw; meta[3] = w.ph; meta[4] = 0; meta[5] = 0; }
+  };
+  if (npix == 0) {
+    if (o.gt) GSS_CUDA(cudaMemsetAsync(o.loss_dev, 0, sizeof(float), st));
+    if (o.gt && o.loss_sum) GSS_CUDA(cudaMemsetAsync(o.loss_sum, 0, sizeof(double), st));
+    write_meta(0);
     return;
   }
-  SplatRec* recs = static_cast<SplatRec*>(ctx->recs.get((size_t)V * sizeof(SplatRec), st));
-  int32_t* nt = static_cast<int32_t*>(ctx->ntiles.get((size_t)(V + 1) * 4, st));
+  SplatRec* recs = static_cast<SplatRec*>(ctx->recs.p);
+  int32_t* nt = static_cast<int32_t*>(ctx->ntiles.p);
   int32_t* offs = static_cast<int32_t*>(ctx->offsets.get((size_t)(V + 1) * 4, st));
-  int32_t* soff = static_cast<int32_t*>(ctx->slot_off.get((size_t)V * 4, st));
-  auto* dka = static_cast<uint32_t*>(ctx->dkeys_a.get((size_t)V * 4, st));
-  auto* dkb = static_cast<uint32_t*>(ctx->dkeys_b.get((size_t)V * 4, st));
-  auto* oa = static_cast<int32_t*>(ctx->order_a.get((size_t)V * 4, st));
-  auto* ob = static_cast<int32_t*>(ctx->order_b.get((size_t)V * 4, st));
-  preprocess_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(s, ctx->cam, w, V, recs, nt, dka, oa);
-  GSS_LAUNCHED();
-  // 1. stable sort of the V splats by depth (slot order breaks ties = ascending id).
-  cub::DoubleBuffer<uint32_t> ddk(dka, dkb);
-  cub::DoubleBuffer<int32_t> ddv(oa, ob);
-  size_t db = 0;
-  GSS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, db, ddk, ddv, (int)V, 0, 32, st));
-  // 2. instance offsets in depth order; offs[V] = I.
-  using CountIt = thrust::transform_iterator<SortedCount, thrust::counting_iterator<int32_t>>;
-  size_t tb = 0;
-  GSS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, CountIt(thrust::counting_iterator<int32_t>(0),
-                                                                  SortedCount{nt, nullptr, (int32_t)V}),
-                                         offs, (int)(V + 1), st));
-  void* tmp = ctx->cub_tmp.get(std::max(db, tb), st);
-  GSS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, db, ddk, ddv, (int)V, 0, 32, st));
-  count_launch();
-  const int32_t* order = ddv.Current();
-  GSS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, CountIt(thrust::counting_iterator<int32_t>(0),
-                                                              SortedCount{nt, order, (int32_t)V}),
-                                         offs, (int)(V + 1), st));
-  count_launch();
-  GSS_CUDA(cudaMemcpyAsync(ctx->pinned + 1, offs + V, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  GSS_CUDA(cudaStreamSynchronize(st));
-  const int64_t I = (int64_t)(reinterpret_cast<int32_t*>(ctx->pinned + 1)[0]);
-  require(I >= 0 && I <= INT32_MAX, "rasterize_forward: tile instance count overflow");
-  ctx->I = I;
+  int32_t* soff = static_cast<int32_t*>(ctx->slot_off.get((size_t)std::max<int64_t>(V, 1) * 4, st));
+  int64_t I = 0;
   const int ntile = w.tw * w.th;
   int2* ranges = static_cast<int2*>(ctx->ranges.get((size_t)ntile * sizeof(int2), st));
   GSS_CUDA(cudaMemsetAsync(ranges, 0, (size_t)ntile * sizeof(int2), st));
-  int32_t* vals_sorted = nullptr;
-  {
+  int32_t* vals_sorted = static_cast<int32_t*>(ctx->vals_a.get(16, st));
+  if (V > 0) {
+    auto* dka = static_cast<uint32_t*>(ctx->dkeys_a.p);
+    auto* dkb = static_cast<uint32_t*>(ctx->dkeys_b.get((size_t)V * 4, st));
+    auto* oa = static_cast<int32_t*>(ctx->order_a.p);
+    auto* ob = static_cast<int32_t*>(ctx->order_b.get((size_t)V * 4, st));
+    // 1. stable sort of the V splats by depth (record order breaks ties: ascending id).
+    cub::DoubleBuffer<uint32_t> ddk(dka, dkb);
+    cub::DoubleBuffer<int32_t> ddv(oa, ob);
+    size_t db = 0;
+    GSS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, db, ddk, ddv, (int)V, 0, 32, st));
+    // 2. instance offsets in depth order; offs[V] = I.
+    using CountIt = thrust::transform_iterator<SortedCount, thrust::counting_iterator<int32_t>>;
+    size_t tb = 0;
+    GSS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, CountIt(thrust::counting_iterator<int32_t>(0),
+                                                                    SortedCount{nt, nullptr, (int32_t)V}),
+                                           offs, (int)(V + 1), st));
+    void* tmp = ctx->cub_tmp.get(std::max(db, tb), st);
+    GSS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, db, ddk, ddv, (int)V, 0, 32, st));
+    count_launch();
+    const int32_t* order = ddv.Current();
+    GSS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, CountIt(thrust::counting_iterator<int32_t>(0),
+                                                                SortedCount{nt, order, (int32_t)V}),
+                                           offs, (int)(V + 1), st));
+    count_launch();
+    GSS_CUDA(cudaMemcpyAsync(ctx->pinned + 1, offs + V, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    GSS_CUDA(cudaStreamSynchronize(st));
+    I = (int64_t)(reinterpret_cast<int32_t*>(ctx->pinned + 1)[0]);
+    require(I >= 0 && I <= INT32_MAX, "rasterize_forward: tile instance count overflow");
     auto* ka = static_cast<uint32_t*>(ctx->keys_a.get((size_t)std::max<int64_t>(I, 1) * 4, st));
     auto* kb = static_cast<uint32_t*>(ctx->keys_b.get((size_t)std::max<int64_t>(I, 1) * 4, st));
     auto* va = static_cast<int32_t*>(ctx->vals_a.get((size_t)std::max<int64_t>(I, 1) * 4, st));
@@ -1008,18 +1045,99 @@ void rasterize_forward(gss_render_ctx* ctx, const gss_render_scene* scene, const
       GSS_LAUNCHED();
     }
   }
-  double* lp = gt ? static_cast<double*>(ctx->lossp.get((size_t)ntile * 8, st)) : nullptr;
-  forward_kernel<<<ntile, kTilePix, 0, st>>>(recs, vals_sorted, ranges, w, s.bg[0], s.bg[1], s.bg[2], image, fT, last,
-                                             ncontrib_opt, gt, cam->width, inv, d_img, lp);
+  ctx->I = I;
+  double* lp = o.gt ? static_cast<double*>(ctx->lossp.get((size_t)ntile * 8, st)) : nullptr;
+  forward_kernel<<<ntile, kTilePix, 0, st>>>(recs, vals_sorted, ranges, w, s.bg[0], s.bg[1], s.bg[2], o.image, fT,
+                                             last, o.ncontrib, o.gt, o.gt_width, o.inv, o.d_img, lp);
   GSS_LAUNCHED();
-  if (gt) {
-    loss_final_kernel<<<1, 1024, 0, st>>>(lp, ntile, inv, loss_dev);
+  if (o.gt) {
+    loss_final_kernel<<<1, 1024, 0, st>>>(lp, ntile, o.inv, o.loss_dev, o.loss_sum);
     GSS_LAUNCHED();
   }
-  if (final_T_opt) GSS_CUDA(cudaMemcpyAsync(final_T_opt, fT, npix * 4, cudaMemcpyDeviceToDevice, st));
-  if (meta) {
-    meta[0] = w.px0; meta[1] = w.py0; meta[2] = w.pw; meta[3] = w.ph; meta[4] = V; meta[5] = I;
+  if (o.final_T) GSS_CUDA(cudaMemcpyAsync(o.final_T, fT, npix * 4, cudaMemcpyDeviceToDevice, st));
+  write_meta(I);
+}
+
+void begin_forward(gss_render_ctx* ctx, const gss_camera* cam, const Win& w, int64_t V, cudaStream_t st) {
+  ctx->last_stream = st;
+  std::memcpy(&ctx->cam, cam, sizeof(Cam));
+  ctx->win = w;
+  ctx->V = V;
+  ctx->I = 0;
+  ctx->have_forward = 1;
+}
+
+void alloc_records(gss_render_ctx* ctx, int64_t V, cudaStream_t st) {
+  const size_t n = (size_t)std::max<int64_t>(V, 1);
+  ctx->recs.get(n * sizeof(SplatRec), st);
+  ctx->ntiles.get((n + 1) * 4, st);
+  ctx->dkeys_a.get(n * 4, st);
+  ctx->order_a.get(n * 4, st);
+}
+
+void per_slot_sums(gss_render_ctx* ctx, const float* d_img, float* sums, cudaStream_t st) {
+  const Win& w = ctx->win;
+  const int64_t V = ctx->V, I = ctx->I;
+  const int64_t npix = (int64_t)w.pw * w.ph;
+  require(npix == 0 || d_img, "rasterize_backward: null d_img");
+  if (I == 0 || npix == 0) {  // no tile instances: every per-slot sum is zero
+    GSS_CUDA(cudaMemsetAsync(sums, 0, (size_t)V * 9 * 4, st));
+    return;
   }
+  const SplatRec* recs = static_cast<const SplatRec*>(ctx->recs.p);
+  const int32_t* soff = static_cast<const int32_t*>(ctx->slot_off.p);
+  const int32_t* nts = static_cast<const int32_t*>(ctx->ntiles.p);
+  float* partials = static_cast<float*>(ctx->partials.get((size_t)std::max<int64_t>(I, 1) * 9 * 4, st));
+  GSS_CUDA(cudaMemsetAsync(partials, 0, (size_t)I * 9 * 4, st));
+  {
+    const int ntile = w.tw * w.th;
+    backward_kernel<<<ntile, kBwdThreads, 0, st>>>(recs, static_cast<const int32_t*>(ctx->vals_a.p),
+                                                static_cast<const int2*>(ctx->ranges.p), w, ctx->sc.bg[0],
+                                                ctx->sc.bg[1], ctx->sc.bg[2], static_cast<const float*>(ctx->fT.p),
+                                                static_cast<const int32_t*>(ctx->last.p), d_img, partials);
+    GSS_LAUNCHED();
+  }
+  slot_sum_kernel<<<(unsigned)ceil_div(V, kSumThreads), kSumThreads, 0, st>>>(V, soff, nts, partials, sums);
+  GSS_LAUNCHED();
+}
+
+void launch_chain(const SceneDev& sc, const Cam& cam, const Win& w, int64_t V, const SplatRec* recs, const float* sums,
+                  float* gg, int64_t gstride, float* gn, int64_t nstride, float* mean2d, cudaStream_t st) {
+  const unsigned cb = (unsigned)ceil_div(V, kChainThreads);
+  switch (sc.sh_degree) {
+    case 0: chain_kernel<0><<<cb, kChainThreads, 0, st>>>(sc, cam, w, V, recs, sums, gg, gstride, gn, nstride, mean2d); break;
+    case 1: chain_kernel<1><<<cb, kChainThreads, 0, st>>>(sc, cam, w, V, recs, sums, gg, gstride, gn, nstride, mean2d); break;
+    case 2: chain_kernel<2><<<cb, kChainThreads, 0, st>>>(sc, cam, w, V, recs, sums, gg, gstride, gn, nstride, mean2d); break;
+    default: chain_kernel<3><<<cb, kChainThreads, 0, st>>>(sc, cam, w, V, recs, sums, gg, gstride, gn, nstride, mean2d); break;
+  }
+  GSS_LAUNCHED();
+}
+
+}  // namespace
+
+void rasterize_forward(gss_render_ctx* ctx, const gss_render_scene* scene, const gss_camera* cam,
+                       const gss_viewport* vp, float* image, const float* gt, int64_t normalizer, float* d_img,
+                       float* loss_dev, float* final_T_opt, int32_t* ncontrib_opt, int64_t* meta, cudaStream_t st) {
+  require(ctx && scene && cam && vp && image, "rasterize_forward: null argument");
+  require(!gt || (d_img && loss_dev), "rasterize_forward: gt needs d_img and loss_dev");
+  set_scene(ctx, scene);
+  if (!ctx->pinned) GSS_CUDA(cudaMallocHost(&ctx->pinned, 4 * sizeof(int64_t)));
+  const Win w = make_window(*vp);
+  require(!gt || (w.px0 + w.pw <= cam->width && w.py0 + w.ph <= cam->height),
+          "compute_loss_l1: image and ground-truth shapes differ");
+  const int64_t V = scene_count(ctx, scene, st);
+  begin_forward(ctx, cam, w, V, st);
+  const int64_t npix = (int64_t)w.pw * w.ph;
+  const float inv = gt ? 1.0f / (float)(double)(normalizer > 0 ? normalizer : npix * 3) : 0.0f;
+  alloc_records(ctx, V, st);
+  if (V > 0 && npix > 0) {
+    preprocess_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(
+        ctx->sc, ctx->cam, w, V, static_cast<SplatRec*>(ctx->recs.p), static_cast<int32_t*>(ctx->ntiles.p),
+        static_cast<uint32_t*>(ctx->dkeys_a.p), static_cast<int32_t*>(ctx->order_a.p));
+    GSS_LAUNCHED();
+  }
+  bin_and_composite(ctx, w, V, FwdOut{image, gt, cam->width, inv, d_img, loss_dev, nullptr, final_T_opt, ncontrib_opt,
+                                      meta}, st);
 }
 
 void loss_l1(const float* image, const float* gt, int64_t elems, int64_t normalizer, float* d_img, float* loss_dev,
@@ -1036,7 +1154,7 @@ void loss_l1(const float* image, const float* gt, int64_t elems, int64_t normali
   GSS_CUDA(cudaMallocAsync((void**)&lp, (size_t)blocks * 8, st));
   loss_partial_kernel<<<blocks, 256, 0, st>>>(image, gt, elems, inv, d_img, lp);
   GSS_LAUNCHED();
-  loss_final_kernel<<<1, 1024, 0, st>>>(lp, blocks, inv, loss_dev);
+  loss_final_kernel<<<1, 1024, 0, st>>>(lp, blocks, inv, loss_dev, nullptr);
   GSS_LAUNCHED();
   GSS_CUDA(cudaFreeAsync(lp, st));
 }
@@ -1045,40 +1163,122 @@ void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int6
                         int64_t nstride, float* mean2d, cudaStream_t st) {
   require(ctx && ctx->have_forward, "rasterize_backward: no forward result in this context");
   require(gstride >= 10 && nstride >= 49, "rasterize_backward: bad gradient strides");
-  const Win& w = ctx->win;
-  const int64_t V = ctx->V, I = ctx->I;
+  const int64_t V = ctx->V;
   if (V == 0) return;
   require(gg && gn, "rasterize_backward: null gradient buffers");
-  const int64_t npix = (int64_t)w.pw * w.ph;
-  require(npix == 0 || d_img, "rasterize_backward: null d_img");
-  const SplatRec* recs = static_cast<const SplatRec*>(ctx->recs.p);
-  const int32_t* soff = static_cast<const int32_t*>(ctx->slot_off.p);
-  const int32_t* nts = static_cast<const int32_t*>(ctx->ntiles.p);
-  float* partials = static_cast<float*>(ctx->partials.get((size_t)std::max<int64_t>(I, 1) * 9 * 4, st));
-  if (I > 0 && npix > 0) {
-    GSS_CUDA(cudaMemsetAsync(partials, 0, (size_t)I * 9 * 4, st));
-    const int ntile = w.tw * w.th;
-    backward_kernel<<<ntile, kBwdThreads, 0, st>>>(recs, static_cast<const int32_t*>(ctx->vals_a.p),
-                                                static_cast<const int2*>(ctx->ranges.p), w, ctx->sc.bg[0],
-                                                ctx->sc.bg[1], ctx->sc.bg[2], static_cast<const float*>(ctx->fT.p),
-                                                static_cast<const int32_t*>(ctx->last.p), d_img, partials);
-    GSS_LAUNCHED();
-  } else if (I > 0) {
-    GSS_CUDA(cudaMemsetAsync(partials, 0, (size_t)I * 9 * 4, st));
-  }
   float* sums = static_cast<float*>(ctx->sums.get((size_t)V * 9 * 4, st));
-  slot_sum_kernel<<<(unsigned)ceil_div(V, kSumThreads), kSumThreads, 0, st>>>(V, soff, nts, partials, sums);
+  per_slot_sums(ctx, d_img, sums, st);
+  launch_chain(ctx->sc, ctx->cam, ctx->win, V, static_cast<const SplatRec*>(ctx->recs.p), sums, gg, gstride, gn,
+               nstride, mean2d, st);
+}
+
+// ---- split-phase rasterizer for image-parallel rendering ----------------------
+
+void project(const gss_render_scene* scene, const gss_camera* cam, const gss_viewport* vp, void* records,
+             cudaStream_t st) {
+  require(scene && cam && vp && (scene->count == 0 || records), "project: null argument");
+  require(!scene->count_dev, "project: needs a host-known count");
+  gss_render_ctx tmp;
+  set_scene(&tmp, scene);
+  const int64_t V = scene->count;
+  require(V >= 0 && V <= INT32_MAX, "project: visible count out of range");
+  if (V == 0) return;
+  Cam c;
+  std::memcpy(&c, cam, sizeof(Cam));
+  preprocess_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(tmp.sc, c, make_window(*vp), V,
+                                                                static_cast<SplatRec*>(records), nullptr, nullptr,
+                                                                nullptr);
   GSS_LAUNCHED();
-  {
-    const unsigned cb = (unsigned)ceil_div(V, kChainThreads);
-    switch (ctx->sc.sh_degree) {
-      case 0: chain_kernel<0><<<cb, kChainThreads, 0, st>>>(ctx->sc, ctx->cam, w, V, recs, sums, gg, gstride, gn, nstride, mean2d); break;
-      case 1: chain_kernel<1><<<cb, kChainThreads, 0, st>>>(ctx->sc, ctx->cam, w, V, recs, sums, gg, gstride, gn, nstride, mean2d); break;
-      case 2: chain_kernel<2><<<cb, kChainThreads, 0, st>>>(ctx->sc, ctx->cam, w, V, recs, sums, gg, gstride, gn, nstride, mean2d); break;
-      default: chain_kernel<3><<<cb, kChainThreads, 0, st>>>(ctx->sc, ctx->cam, w, V, recs, sums, gg, gstride, gn, nstride, mean2d); break;
-    }
+}
+
+void route_strips(const void* records, int64_t count, const int32_t* strip_x, int nstrips, int32_t* dest_slots,
+                  int64_t* dest_counts, cudaStream_t st) {
+  require(count >= 0 && count <= INT32_MAX && nstrips >= 1, "route_strips: bad sizes");
+  require(strip_x && dest_counts && (count == 0 || (records && dest_slots)), "route_strips: null argument");
+  for (int k = 0; k < nstrips; ++k) require(strip_x[k] <= strip_x[k + 1], "route_strips: strips must ascend");
+  if (count == 0) {
+    GSS_CUDA(cudaMemsetAsync(dest_counts, 0, (size_t)nstrips * 8, st));
+    return;
   }
+  const SplatRec* recs = static_cast<const SplatRec*>(records);
+  size_t tb = 0;
+  thrust::counting_iterator<int32_t> it(0);
+  GSS_CUDA(cub::DeviceSelect::If(nullptr, tb, it, dest_slots, dest_counts, (int)count,
+                                 StripHit{recs, strip_x[0], strip_x[1]}, st));
+  void* tmp = nullptr;
+  GSS_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tb, 16), st));
+  for (int k = 0; k < nstrips; ++k) {
+    GSS_CUDA(cub::DeviceSelect::If(tmp, tb, it, dest_slots + (size_t)k * count, dest_counts + k, (int)count,
+                                   StripHit{recs, strip_x[k], strip_x[k + 1]}, st));
+    count_launch();
+  }
+  GSS_CUDA(cudaFreeAsync(tmp, st));
+}
+
+void gather_records(const void* records, const int32_t* slots, int64_t n, void* out, cudaStream_t st) {
+  require(n >= 0 && (n == 0 || (records && slots && out)), "gather_records: null argument");
+  if (n == 0) return;
+  gather_records_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(static_cast<const SplatRec*>(records), slots, n,
+                                                                    static_cast<SplatRec*>(out));
   GSS_LAUNCHED();
+}
+
+void scatter_add_rows(const float* src, const int32_t* slots, int64_t n, int width, float* dst, cudaStream_t st) {
+  require(n >= 0 && width > 0 && (n == 0 || (src && slots && dst)), "scatter_add_rows: null argument");
+  if (n == 0) return;
+  scatter_add_rows_kernel<<<(unsigned)ceil_div(n * width, 256), 256, 0, st>>>(src, slots, n, width, dst);
+  GSS_LAUNCHED();
+}
+
+void rasterize_records_forward(gss_render_ctx* ctx, const void* records, int64_t count, const gss_camera* cam,
+                               const gss_viewport* vp, const float* background, float* image, const float* gt,
+                               int64_t normalizer, float* d_img, float* loss_dev, double* loss_sum_dev,
+                               float* final_T_opt, int32_t* ncontrib_opt, int64_t* meta, cudaStream_t st) {
+  require(ctx && cam && vp && background && (count == 0 || records), "rasterize_records_forward: null argument");
+  require(count >= 0 && count <= INT32_MAX, "rasterize_records_forward: count out of range");
+  if (!ctx->pinned) GSS_CUDA(cudaMallocHost(&ctx->pinned, 4 * sizeof(int64_t)));
+  const Win w = make_window(*vp);
+  const bool empty = (int64_t)w.pw * w.ph == 0;  // an empty strip: no pixel buffers needed
+  require(empty || image, "rasterize_records_forward: null image");
+  require(!gt || ((empty || d_img) && loss_dev), "rasterize_records_forward: gt needs d_img and loss_dev");
+  require(!gt || (w.px0 + w.pw <= cam->width && w.py0 + w.ph <= cam->height),
+          "compute_loss_l1: image and ground-truth shapes differ");
+  ctx->sc = SceneDev{};
+  for (int c = 0; c < 3; ++c) ctx->sc.bg[c] = background[c];
+  begin_forward(ctx, cam, w, count, st);
+  const int64_t npix = (int64_t)w.pw * w.ph;
+  const float inv = gt ? 1.0f / (float)(double)(normalizer > 0 ? normalizer : npix * 3) : 0.0f;
+  alloc_records(ctx, count, st);
+  if (count > 0 && npix > 0) {
+    clip_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, st>>>(
+        static_cast<const SplatRec*>(records), count, w, static_cast<SplatRec*>(ctx->recs.p),
+        static_cast<int32_t*>(ctx->ntiles.p), static_cast<uint32_t*>(ctx->dkeys_a.p),
+        static_cast<int32_t*>(ctx->order_a.p));
+    GSS_LAUNCHED();
+  }
+  bin_and_composite(ctx, w, count, FwdOut{image, gt, cam->width, inv, d_img, loss_dev, loss_sum_dev, final_T_opt,
+                                          ncontrib_opt, meta}, st);
+}
+
+void rasterize_records_backward(gss_render_ctx* ctx, const float* d_img, float* sums, cudaStream_t st) {
+  require(ctx && ctx->have_forward, "rasterize_records_backward: no forward result in this context");
+  if (ctx->V == 0) return;
+  require(sums, "rasterize_records_backward: null sums");
+  per_slot_sums(ctx, d_img, sums, st);
+}
+
+void chain_backward(const gss_render_scene* scene, const gss_camera* cam, const void* records, const float* sums,
+                    float* gg, int64_t gstride, float* gn, int64_t nstride, float* mean2d, cudaStream_t st) {
+  require(scene && cam && (scene->count == 0 || (records && sums && gg && gn)), "chain_backward: null argument");
+  require(!scene->count_dev, "chain_backward: needs a host-known count");
+  require(gstride >= 10 && nstride >= 49, "chain_backward: bad gradient strides");
+  gss_render_ctx tmp;
+  set_scene(&tmp, scene);
+  if (scene->count == 0) return;
+  Cam c;
+  std::memcpy(&c, cam, sizeof(Cam));
+  launch_chain(tmp.sc, c, Win{}, scene->count, static_cast<const SplatRec*>(records), sums, gg, gstride, gn, nstride,
+               mean2d, st);
 }
 
 gss_render_ctx* render_ctx_create() { return new gss_render_ctx(); }

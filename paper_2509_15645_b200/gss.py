@@ -386,6 +386,109 @@ def rasterize_backward(sc: RenderScene, cam: GssCamera, fw: RenderResult, d_img:
 
 
 # ---------------------------------------------------------------------------------------------
+# Split-phase rasterizer (image-parallel rendering across GPUs; include/gss_b200.h)
+
+SPLAT_RECORD_BYTES = 64
+
+
+def project(sc: RenderScene, cam: GssCamera, vp: GssViewport, stream=None) -> torch.Tensor:
+    """project_all (render.hpp:361-380): one 64-byte splat record per visible slot (uint8 [V, 64])."""
+    V = int(sc.ids.numel())
+    recs = torch.empty((max(V, 1), SPLAT_RECORD_BYTES), dtype=torch.uint8, device=sc.geo.device)[:V]
+    s = sc.c_struct()
+    check(lib().gss_project(C.byref(s), C.byref(cam), C.byref(vp), _ptr(recs) if V else None, _stream(stream)))
+    return recs
+
+
+def route_strips(recs: torch.Tensor, strip_x: Sequence[int], stream=None):
+    """Slots (ascending) whose pixel box touches each column strip [strip_x[k], strip_x[k+1]).
+    Returns (dest_slots [nstrips, V] int32 device, counts host list)."""
+    V = int(recs.shape[0])
+    k = len(strip_x) - 1
+    sx = np.ascontiguousarray(np.asarray(strip_x, np.int32))
+    slots = torch.empty((k, max(V, 1)), dtype=torch.int32, device=recs.device)
+    counts = torch.zeros(k, dtype=torch.int64, device=recs.device)
+    check(lib().gss_route_strips(_ptr(recs) if V else None, V, sx.ctypes.data, k, _ptr(slots), _ptr(counts),
+                                 _stream(stream)))
+    return slots, [int(c) for c in counts.cpu().tolist()]
+
+
+def gather_records(recs: torch.Tensor, slots: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None):
+    n = int(slots.numel())
+    if out is None:
+        out = torch.empty((n, SPLAT_RECORD_BYTES), dtype=torch.uint8, device=recs.device)
+    check(lib().gss_gather_records(_ptr(recs), _ptr(slots), n, _ptr(out), _stream(stream)))
+    return out
+
+
+def scatter_add_rows(src: torch.Tensor, slots: torch.Tensor, dst: torch.Tensor, stream=None) -> None:
+    n = int(slots.numel())
+    check(lib().gss_scatter_add_rows(_ptr(src), _ptr(slots), n, int(dst.shape[1]), _ptr(dst), _stream(stream)))
+
+
+@dataclass
+class RecordsResult:
+    image: torch.Tensor  # strip window ph x pw x 3
+    loss_sum: Optional[torch.Tensor]  # device float64: sum |image - gt| over the window
+    d_img: Optional[torch.Tensor]
+    px0: int
+    py0: int
+    pw: int
+    ph: int
+    count: int
+    instances: int
+    ctx: "_Ctx"
+
+
+def rasterize_records_forward(recs: torch.Tensor, cam: GssCamera, vp: GssViewport, *,
+                              background=(0.0, 0.0, 0.0), gt: Optional[torch.Tensor] = None, normalizer: int = 0,
+                              ctx: Optional["_Ctx"] = None, stream=None) -> RecordsResult:
+    """Composite received records on window vp (an image strip); ties in depth follow record order."""
+    ctx = ctx or _Ctx()
+    dev = recs.device
+    import math
+    px0 = max(int(math.ceil(float(np.float32(vp.x0)) - 0.5)), 0)
+    py0 = max(int(math.ceil(float(np.float32(vp.y0)) - 0.5)), 0)
+    pw = max(0, int(math.ceil(float(np.float32(vp.x1)) - 0.5)) - px0)
+    ph = max(0, int(math.ceil(float(np.float32(vp.y1)) - 0.5)) - py0)
+    image = torch.empty((ph, pw, 3), dtype=torch.float32, device=dev)
+    d_img = loss = lsum = None
+    if gt is not None:
+        d_img = torch.empty((ph, pw, 3), dtype=torch.float32, device=dev)
+        loss = torch.zeros(1, dtype=torch.float32, device=dev)
+        lsum = torch.zeros(1, dtype=torch.float64, device=dev)
+    bg = np.asarray(background, np.float32)
+    meta = (C.c_int64 * 6)()
+    n = int(recs.shape[0])
+    check(lib().gss_rasterize_records_forward(ctx.h, _ptr(recs) if n else None, n, C.byref(cam), C.byref(vp),
+                                              bg.ctypes.data, _ptr(image), _ptr(gt), int(normalizer), _ptr(d_img),
+                                              _ptr(loss), _ptr(lsum), None, None, meta, _stream(stream)))
+    return RecordsResult(image, lsum, d_img, int(meta[0]), int(meta[1]), int(meta[2]), int(meta[3]), n,
+                         int(meta[5]), ctx)
+
+
+def rasterize_records_backward(fw: RecordsResult, d_img: torch.Tensor, stream=None) -> torch.Tensor:
+    """Per-record 9-float screen-space gradient sums [count, 9]."""
+    sums = torch.zeros((max(fw.count, 1), 9), dtype=torch.float32, device=d_img.device)[: fw.count]
+    check(lib().gss_rasterize_records_backward(fw.ctx.h, _ptr(d_img), _ptr(sums) if fw.count else None,
+                                               _stream(stream)))
+    return sums
+
+
+def chain_backward(sc: RenderScene, cam: GssCamera, recs: torch.Tensor, sums: torch.Tensor, stream=None) -> GradBuffer:
+    """render.hpp:600-638 per slot from the strip-summed screen-space gradients."""
+    V = int(sc.ids.numel())
+    dev = sc.geo.device
+    rows = torch.zeros((max(V, 1), K_PARAM_DIM), dtype=torch.float32, device=dev)
+    m2d = torch.zeros((max(V, 1), 2), dtype=torch.float32, device=dev)
+    s = sc.c_struct()
+    check(lib().gss_chain_backward(C.byref(s), C.byref(cam), _ptr(recs) if V else None, _ptr(sums) if V else None,
+                                   _ptr(rows), K_PARAM_DIM, rows.data_ptr() + 40, K_PARAM_DIM, _ptr(m2d),
+                                   _stream(stream)))
+    return GradBuffer(sc.ids, rows[:V], m2d[:V])
+
+
+# ---------------------------------------------------------------------------------------------
 # Scenes (synth.hpp:13-159) — input generation
 
 @dataclass

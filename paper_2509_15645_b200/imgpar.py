@@ -1,0 +1,223 @@
+"""Image-parallel rendering and sharded training over N GPUs.
+
+Partition: Gaussians and all their optimizer state by contiguous id range (dist.id_range), so cull,
+forwarding gather and both Adam passes are shard-local. A view is rendered image-parallel:
+
+  A  owner:  project its visible Gaussians into 64-byte splat records (gss_project) and route each
+             record to every column strip its pixel box touches (gss_route_strips), ascending slots;
+  X1 all-to-allv of records (NCCL over NVLink; ranks concatenate what they receive in rank order,
+             which is ascending global id because shards are ascending id ranges);
+  B  strip:  composite the received records on its strip (gss_rasterize_records_forward): the
+             per-pixel contribution lists are the unsplit ones, so strip pixels are bit-identical;
+             the loss is the fp64 sum of the strips' fp64 |d| sums, cast once (render.hpp:510);
+  C  strip:  backward -> one 9-float screen-space gradient sum per received record (the SlotAcc
+             cut of render.hpp:538);
+  X2 all-to-allv back to the owners (the reverse splits of X1);
+  D  owner:  sum the strips' partials per slot in strip order (gss_scatter_add_rows, fixed order:
+             deterministic) and run the per-Gaussian chain locally (gss_chain_backward).
+
+The reference's batch-1 semantics are kept (no view batching). Confined Gaussians' gradients are
+the unsplit ones up to the tile-partial association; straddlers reassociate like the reference's
+own split aggregation (splitter.hpp:85-123, pinned at <= 1e-5 by test_split.cpp:144-211).
+
+`simulate_render` runs the same phases for R virtual shards in one process (the exchange is a
+concatenation): the single-GPU parity harness of the multi-GPU path.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import gss as G
+from ._abi import GssViewport
+
+
+def strip_bounds(px0: int, pw: int, nstrips: int, align: int = 16) -> List[int]:
+    """Column boundaries of `nstrips` strips over pixels [px0, px0 + pw): whole 16-pixel tiles,
+    sizes differing by at most one tile (the last strip absorbs the ragged edge)."""
+    if nstrips < 1:
+        raise ValueError("strip_bounds: nstrips must be >= 1")
+    tiles = -(-pw // align)
+    base, extra = divmod(tiles, nstrips)
+    b = [px0]
+    for k in range(nstrips):
+        b.append(min(px0 + pw, b[-1] + (base + (1 if k < extra else 0)) * align))
+    b[-1] = px0 + pw
+    return b
+
+
+def strip_viewport(vp: GssViewport, bounds: Sequence[int], k: int) -> GssViewport:
+    """The viewport whose pixel window (render.hpp:297-304) is columns [bounds[k], bounds[k+1])."""
+    return GssViewport(float(bounds[k]), float(bounds[k + 1]), vp.y0, vp.y1)
+
+
+def window_of(vp: GssViewport) -> Tuple[int, int, int, int]:
+    import math
+    px0 = max(int(math.ceil(float(np.float32(vp.x0)) - 0.5)), 0)
+    py0 = max(int(math.ceil(float(np.float32(vp.y0)) - 0.5)), 0)
+    pw = max(0, int(math.ceil(float(np.float32(vp.x1)) - 0.5)) - px0)
+    ph = max(0, int(math.ceil(float(np.float32(vp.y1)) - 0.5)) - py0)
+    return px0, py0, pw, ph
+
+
+def loss_from_sums(sums_f64: Sequence[float], normalizer: int) -> float:
+    """(float)(sum of the strips' fp64 sums, in strip order) * (1 / (float)normalizer), the device
+    loss_final arithmetic (render.hpp:510)."""
+    tot = 0.0
+    for s in sums_f64:
+        tot += float(s)
+    inv = np.float32(1.0) / np.float32(float(normalizer))
+    return float(np.float32(tot) * inv)
+
+
+# ------------------------------------------------------------------------------------------------
+# Phases (one shard / one strip each; device tensors)
+
+@dataclass
+class OwnerState:
+    scene: G.RenderScene
+    recs: torch.Tensor  # [V, 64] uint8
+    slots: torch.Tensor  # [R, V] int32 (row k: first counts[k] entries)
+    counts: List[int]
+
+
+def owner_project(scene: G.RenderScene, cam, vp: GssViewport, bounds: Sequence[int]):
+    """Phase A: records of this shard's visible slots and the send buffer (strip-major, ascending
+    slots within a strip). Returns (state, send [sum counts, 64] uint8, send counts)."""
+    recs = G.project(scene, cam, vp)
+    slots, counts = G.route_strips(recs, bounds)
+    sel = torch.cat([slots[k, : counts[k]] for k in range(len(counts))]) if recs.shape[0] else \
+        torch.zeros(0, dtype=torch.int32, device=recs.device)
+    send = G.gather_records(recs, sel)
+    return OwnerState(scene, recs, slots, counts), send, counts
+
+
+def strip_forward(recv: torch.Tensor, cam, vp_strip: GssViewport, background, gt: Optional[torch.Tensor],
+                  normalizer: int) -> G.RecordsResult:
+    """Phase B: composite the received records on the strip (loss/d_img fused when gt is given)."""
+    return G.rasterize_records_forward(recv, cam, vp_strip, background=background, gt=gt, normalizer=normalizer)
+
+
+def strip_backward(fw: G.RecordsResult, d_img: torch.Tensor) -> torch.Tensor:
+    """Phase C: per-received-record 9-float screen-space gradient sums."""
+    return G.rasterize_records_backward(fw, d_img)
+
+
+def owner_combine(st: OwnerState, back: torch.Tensor) -> torch.Tensor:
+    """Phase D (first half): per-slot sums of the strips' returned partials in strip order."""
+    V = int(st.recs.shape[0])
+    sums = torch.zeros((max(V, 1), 9), dtype=torch.float32, device=st.recs.device)[:V]
+    off = 0
+    for k, c in enumerate(st.counts):
+        if c:
+            G.scatter_add_rows(back[off: off + c], st.slots[k, :c], sums)
+        off += c
+    return sums
+
+
+def owner_chain(st: OwnerState, cam, sums: torch.Tensor) -> G.GradBuffer:
+    """Phase D (second half): the per-Gaussian chain on the owner."""
+    return G.chain_backward(st.scene, cam, st.recs, sums)
+
+
+# ------------------------------------------------------------------------------------------------
+# Exchange over torch.distributed
+
+class TorchExchange:
+    """all-to-allv / all-gather over a torch.distributed group. With NCCL the device tensors go
+    over NVLink directly; with any other backend (gloo: CPU tests, or several processes sharing
+    one GPU) they are staged through host memory."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device_native = dist.get_backend(group) == "nccl"
+
+    def _dev(self, t: torch.Tensor) -> torch.Tensor:
+        return t if self.device_native else t.cpu()
+
+    def alltoallv(self, send: torch.Tensor, send_counts: Sequence[int],
+                  recv_counts: Optional[Sequence[int]] = None) -> Tuple[torch.Tensor, List[int]]:
+        """Rows send[sum(send_counts[:j]) : +send_counts[j]] go to rank j; returns the rows
+        received, concatenated in rank order, and their counts."""
+        d = self.dist
+        if recv_counts is None:
+            dev = send.device if self.device_native else "cpu"
+            sc = torch.tensor([int(c) for c in send_counts], dtype=torch.int64, device=dev)
+            rc = torch.empty_like(sc)
+            d.all_to_all_single(rc, sc, group=self.group)
+            recv_counts = rc.cpu().tolist()
+        recv_counts = [int(c) for c in recv_counts]
+        out = torch.empty((sum(recv_counts),) + tuple(send.shape[1:]), dtype=send.dtype,
+                          device=send.device if self.device_native else "cpu")
+        d.all_to_all_single(out, self._dev(send.contiguous()), output_split_sizes=recv_counts,
+                            input_split_sizes=[int(c) for c in send_counts], group=self.group)
+        return out.to(send.device), recv_counts
+
+    def allgather_f64(self, x: torch.Tensor) -> List[float]:
+        t = x.reshape(1).to(torch.float64)
+        t = t if self.device_native else t.cpu()
+        parts = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(parts, t, group=self.group)
+        return [float(p.item()) for p in parts]
+
+
+def render_step(ex: TorchExchange, scene: G.RenderScene, cam, vp: GssViewport, gt: Optional[torch.Tensor],
+                background=(0.0, 0.0, 0.0), normalizer: int = 0):
+    """One view, image-parallel over the exchange group: returns (loss, GradBuffer of this shard,
+    strip image, info). Rank k owns strip k of `vp`."""
+    px0, py0, pw, ph = window_of(vp)
+    bounds = strip_bounds(px0, pw, ex.world)
+    norm = normalizer if normalizer > 0 else pw * ph * 3
+    st, send, scounts = owner_project(scene, cam, vp, bounds)
+    recv, rcounts = ex.alltoallv(send, scounts)
+    fw = strip_forward(recv, cam, strip_viewport(vp, bounds, ex.rank), background, gt, norm)
+    loss = None
+    if gt is not None:
+        loss = loss_from_sums(ex.allgather_f64(fw.loss_sum), norm)
+    part = strip_backward(fw, fw.d_img) if gt is not None else None
+    gb = None
+    if part is not None:
+        back, _ = ex.alltoallv(part, rcounts, recv_counts=scounts)
+        gb = owner_chain(st, cam, owner_combine(st, back))
+    info = dict(sent=sum(scounts), received=sum(rcounts), instances=fw.instances, bounds=bounds)
+    return loss, gb, fw.image, info
+
+
+def simulate_render(scenes: Sequence[G.RenderScene], cam, vp: GssViewport, gt: Optional[torch.Tensor],
+                    background=(0.0, 0.0, 0.0), normalizer: int = 0):
+    """R = len(scenes) virtual shards in one process, same phases, exchange = concatenation.
+    Returns (loss, [GradBuffer per shard], full image assembled from the strips)."""
+    R = len(scenes)
+    px0, py0, pw, ph = window_of(vp)
+    bounds = strip_bounds(px0, pw, R)
+    norm = normalizer if normalizer > 0 else pw * ph * 3
+    owners = [owner_project(sc, cam, vp, bounds) for sc in scenes]
+    offs = [np.concatenate([[0], np.cumsum(o[2])]).astype(np.int64) for o in owners]
+    fws, recv_counts = [], []
+    for k in range(R):
+        parts = [o[1][offs[r][k]: offs[r][k + 1]] for r, o in enumerate(owners)]
+        recv_counts.append([int(p.shape[0]) for p in parts])
+        recv = torch.cat(parts) if parts else owners[0][1][:0]
+        fws.append(strip_forward(recv, cam, strip_viewport(vp, bounds, k), background, gt, norm))
+    image = torch.cat([f.image for f in fws], dim=1)
+    loss = loss_from_sums([float(f.loss_sum.item()) for f in fws], norm) if gt is not None else None
+    grads = None
+    if gt is not None:
+        parts_back = [strip_backward(f, f.d_img) for f in fws]
+        grads = []
+        for r, (st, _, scounts) in enumerate(owners):
+            segs = []
+            for k in range(R):
+                o = int(sum(recv_counts[k][:r]))
+                segs.append(parts_back[k][o: o + recv_counts[k][r]])
+            back = torch.cat(segs)
+            grads.append(owner_chain(st, cam, owner_combine(st, back)))
+    return loss, grads, image

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version_and_struct_sizes():
-    assert G.lib().gss_abi_version() == 1
+    assert G.lib().gss_abi_version() == 2
     assert C.sizeof(_abi.GssCamera) == 80
     assert C.sizeof(_abi.GssViewport) == 16
 
