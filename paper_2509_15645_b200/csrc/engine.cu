@@ -162,15 +162,21 @@ void ensure_rows(gss_engine* e, int64_t V) {
   if (V <= e->cap_rows) return;
   GSS_CUDA(cudaDeviceSynchronize());
   const int64_t cap = std::min<int64_t>(e->n, std::max<int64_t>(V + V / 4, 1024));
+  // The stage buffers hold live data across iterations (the pending gradients of g-1 feed
+  // forward_params(g) and lazy(g-1)): grow them preserving their contents.
+  auto grow = [&](float*& buf, int width) {
+    float* nb = dmalloc<float>((size_t)cap * width);
+    if (buf) {
+      GSS_CUDA(cudaMemcpy(nb, buf, (size_t)e->cap_rows * width * sizeof(float), cudaMemcpyDeviceToDevice));
+      cudaFree(buf);
+    }
+    buf = nb;
+  };
   for (int b = 0; b < 2; ++b) {
-    cudaFree(e->fwd[b]);
-    cudaFree(e->g_geo[b]);
-    cudaFree(e->g_ng[b]);
-    cudaFree(e->g_m2d[b]);
-    e->fwd[b] = dmalloc<float>((size_t)cap * kNgDim);
-    e->g_geo[b] = dmalloc<float>((size_t)cap * kGeoDim);
-    e->g_ng[b] = dmalloc<float>((size_t)cap * kNgDim);
-    e->g_m2d[b] = dmalloc<float>((size_t)cap * 2);
+    grow(e->fwd[b], kNgDim);
+    grow(e->g_geo[b], kGeoDim);
+    grow(e->g_ng[b], kNgDim);
+    grow(e->g_m2d[b], 2);
   }
   e->cap_rows = cap;
 }

@@ -221,3 +221,75 @@ def simulate_render(scenes: Sequence[G.RenderScene], cam, vp: GssViewport, gt: O
             back = torch.cat(segs)
             grads.append(owner_chain(st, cam, owner_combine(st, back)))
     return loss, grads, image
+
+
+class SelfExchange:
+    """The exchange of a single rank (world 1): every send segment comes straight back."""
+
+    rank, world = 0, 1
+
+    def alltoallv(self, send, send_counts, recv_counts=None):
+        return send, [int(c) for c in send_counts]
+
+    def allgather_f64(self, x):
+        return [float(x.reshape(-1)[0].item())]
+
+
+class ShardTrainer:
+    """One rank of sharded training: this rank's contiguous id shard of the scene
+    with its geometric (dense, geo_defer_max 0) and non-geometric (deferred, defer_max) Adam arenas
+    in HBM, and the reference engine's per-iteration DAG in run_serial order (engine.hpp:434-445):
+
+        cull(g) -> forward_params(g) [restore_view with pending grads(g-1)] -> lazy(g-1)
+        -> render(g) [image-parallel over the exchange group] -> geo_update(g)
+
+    Every stage is shard-local except the render's two all-to-allv exchanges. With one rank and
+    SelfExchange the trajectory equals OffloadEngine(pipelined=False) on the same shard."""
+
+    def __init__(self, init_rows: np.ndarray, cams, gts, ex=None, optim: Optional[G.OptimConfig] = None, *,
+                 sh_degree: int = 3, sh_warmup_step: int = 0, background=(0.0, 0.0, 0.0), device=None):
+        self.ex = ex or SelfExchange()
+        self.opt = optim or G.OptimConfig()
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        rows = torch.from_numpy(np.ascontiguousarray(init_rows, np.float32)).to(dev)
+        self.n = int(rows.shape[0])
+        self.geo = G.Arena(self.n, G.K_GEO_DIM, self.opt.geo_groups(), self.opt.geo_defer_max, device=dev)
+        self.ng = G.Arena(self.n, G.K_NONGEO_DIM, self.opt.nongeo_groups(), self.opt.defer_max, device=dev)
+        self.geo.w.copy_(rows[:, : G.K_GEO_DIM])
+        self.ng.w.copy_(rows[:, G.K_GEO_DIM:])
+        del rows
+        self.cams = list(cams)
+        self.gts = gts  # per camera: device tensor (H x W x 3; only this rank's strip is read) or None
+        self.sh_degree, self.sh_warmup_step = int(sh_degree), int(sh_warmup_step)
+        self.background = tuple(float(b) for b in background)
+        self.g = 0
+        self.pending: Optional[G.SparseGrads] = None
+        self.last_info = {}
+
+    def step(self, cam=None, gt: Optional[torch.Tensor] = None) -> float:
+        g = self.g
+        cam = cam if cam is not None else self.cams[g % len(self.cams)]
+        gt = gt if gt is not None else self.gts[g % len(self.cams)]
+        vp = G.viewport_full(cam.width, cam.height)
+        ids = G.frustum_cull(self.geo.w, self.n, cam, vp)                      # cull(g)
+        fwd = G.restore_view(self.ng, ids, self.pending)                       # forward_params(g)
+        if self.pending is not None:                                           # lazy(g-1)
+            G.deferred_update(self.ng, self.pending, want_touched=False, check_invariants=False)
+        deg = min(self.sh_degree, g // self.sh_warmup_step) if self.sh_warmup_step > 0 else self.sh_degree
+        sc = G.RenderScene(ids=ids, geo=self.geo.w, nongeo=fwd, nongeo_compact=True, sh_degree=deg,
+                           background=self.background)
+        loss, gb, _, info = render_step(self.ex, sc, cam, vp, gt, self.background)  # render(g)
+        G.deferred_update(self.geo, G.SparseGrads(ids, gb.rows, G.K_PARAM_DIM, 0), want_touched=False,
+                          check_invariants=False)                              # geo_update(g)
+        self.pending = G.SparseGrads(ids, gb.rows, G.K_PARAM_DIM, G.K_GEO_DIM)  # handoff(g)
+        self.last_info = dict(info, visible=int(ids.numel()))
+        self.g += 1
+        return loss
+
+    def drain(self) -> None:
+        if self.pending is not None:
+            G.deferred_update(self.ng, self.pending, want_touched=False, check_invariants=False)
+            self.pending = None
+
+    def state(self):
+        return dict(geo_w=self.geo.w, ng_w=self.ng.w, ng_m=self.ng.m, ng_v=self.ng.v, ng_counter=self.ng.counter)
