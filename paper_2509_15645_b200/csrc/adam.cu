@@ -361,57 +361,217 @@ __global__ void __launch_bounds__(kUpdThreads) update_kernel(ArenaDev a, GradsDe
   }
 }
 
-// Streams a touch list: warp per row, lanes on consecutive columns (lane-fixed column groups);
-// each warp takes kRB rows at a time and issues all their loads before any math.
+// Dense immediate update of an arena with defer_max 0 (the geometric tier, store.hpp:121-124;
+// engine.hpp:380-386): every row is touched at delay 0 (w_scale = 0, so the restoration term is
+// w - (+-0), kept exactly) and counters stay 0. A block owns 1024 contiguous rows = one contiguous
+// span of dim * 1024 floats per array, streamed as float4 (16-byte loads/stores, kU in flight per
+// thread); per element the row is a magic-number division, its gradient slot comes from the
+// block's SMEM row->slot map and its column constants from SMEM. Bit-identical to
+// deferred_scalar at delay 0.
+template <int K>
+__global__ void __launch_bounds__(kUpdThreads) dense_update_kernel(ArenaDev a, GradsDev gr, const int32_t* bstart,
+                                                                   const __grid_constant__ LutArgs<K> L,
+                                                                   int64_t* touched_count, uint32_t* touched_mask) {
+  __shared__ float4 cA[kMaxDim];  // ms, vs, one_minus_b1, one_minus_b2 per column
+  __shared__ float4 cB[kMaxDim];  // bias_correction, step_size, eps, -
+  __shared__ int32_t slot_of[kRowsPerBlock];
+  const int tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
+  const int nrows = (int)((a.n - r0) < kRowsPerBlock ? (a.n - r0) : kRowsPerBlock);
+  const int dim = a.dim;
+  for (int c = tid; c < dim; c += kUpdThreads) {
+    const int g = L.col_group[c];
+    cA[c] = make_float4(L.a1[g][0], L.a2[g][0], L.sc[g][0], L.sc[g][1]);
+    cB[c] = make_float4(L.sc[g][2], L.sc[g][3], L.sc[g][4], 0.0f);
+  }
+  for (int i = tid; i < kRowsPerBlock; i += kUpdThreads) slot_of[i] = -1;
+  __syncthreads();
+  if (gr.ids) {
+    const int64_t gcount = grads_count(gr);
+    const int lo = max(0, bstart[blockIdx.x]), hi = (int)min((int64_t)bstart[blockIdx.x + 1], gcount);
+    for (int k = lo + tid; k < hi; k += kUpdThreads) {
+      const int64_t local = (int64_t)gr.ids[k] - r0;
+      if (local >= 0 && local < kRowsPerBlock) slot_of[local] = k;
+    }
+  }
+  __syncthreads();
+  const int64_t e0 = r0 * dim;
+  const int ne = nrows * dim;
+  float4* W = reinterpret_cast<float4*>(a.w + e0);
+  float4* M = reinterpret_cast<float4*>(a.m + e0);
+  float4* V = reinterpret_cast<float4*>(a.v + e0);
+  const int nq = ne >> 2;
+  constexpr int kU = 2;
+  auto elem = [&](float& w, float& m, float& v, float gv, int col) {
+    const float4 A = cA[col], B = cB[col];
+    const float m_new = A.x * m + A.z * gv;
+    const float v_new = A.y * v + A.w * gv * gv;
+    const float num = 0.0f * m;  // w_scale(0) * m
+    w = (num == 0.0f && v >= 0.0f) ? w - num : w - div_rn(num, sqrtf(v) + B.z);
+    const float denom = div_rn(sqrtf(v_new), B.x) + B.z;
+    w = w - div_rn(B.y * m_new, denom);
+    m = m_new;
+    v = v_new;
+  };
+  for (int q0 = tid; q0 < nq; q0 += kUpdThreads * kU) {
+    float4 w[kU], m[kU], v[kU];
+    float gv[kU][4];
+    int col[kU][4];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int q = q0 + u * kUpdThreads;
+      const bool ok = q < nq;
+      w[u] = ok ? W[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      m[u] = ok ? M[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[u] = ok ? V[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t f = (uint32_t)(4 * q + i);
+        const int row = (int)__umulhi(f, a.div_magic);
+        col[u][i] = (int)f - row * dim;
+        const int sl = ok ? slot_of[row] : -1;
+        gv[u][i] = sl >= 0 ? gr.rows[(size_t)sl * gr.stride + gr.col0 + col[u][i]] : 0.0f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int q = q0 + u * kUpdThreads;
+      if (q >= nq) continue;
+      elem(w[u].x, m[u].x, v[u].x, gv[u][0], col[u][0]);
+      elem(w[u].y, m[u].y, v[u].y, gv[u][1], col[u][1]);
+      elem(w[u].z, m[u].z, v[u].z, gv[u][2], col[u][2]);
+      elem(w[u].w, m[u].w, v[u].w, gv[u][3], col[u][3]);
+      W[q] = w[u];
+      M[q] = m[u];
+      V[q] = v[u];
+    }
+  }
+  for (int f = 4 * nq + tid; f < ne; f += kUpdThreads) {  // ragged tail of the last block
+    const int row = (int)__umulhi((uint32_t)f, a.div_magic);
+    const int c = f - row * dim;
+    const int sl = slot_of[row];
+    float w = a.w[e0 + f], m = a.m[e0 + f], v = a.v[e0 + f];
+    elem(w, m, v, sl >= 0 ? gr.rows[(size_t)sl * gr.stride + gr.col0 + c] : 0.0f, c);
+    a.w[e0 + f] = w;
+    a.m[e0 + f] = m;
+    a.v[e0 + f] = v;
+  }
+  if (touched_count && tid == 0 && nrows > 0)
+    atomicAdd((unsigned long long*)touched_count, (unsigned long long)nrows);
+  if (touched_mask) {
+    for (int wi = tid; wi * 32 < nrows; wi += kUpdThreads) {
+      const int rem = nrows - wi * 32;
+      touched_mask[(r0 >> 5) + wi] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+    }
+  }
+}
+
+// Per-(group, delay) and per-group constants of a pass, packed for 16-byte SMEM loads.
+template <int K> struct PackedLuts {
+  float4 gd[kMaxGroups][K];  // param (w_scale), a1, a2, -
+  float4 sc[kMaxGroups];     // one_minus_b1, one_minus_b2, bias_correction, step_size
+  float eps[kMaxGroups];
+  uint8_t col_group[kMaxDim];
+};
+
+template <int K> __device__ void load_packed_luts(PackedLuts<K>& s, const LutArgs<K>& L, int dim) {
+  for (int i = threadIdx.x; i < L.ngroups * K; i += blockDim.x) {
+    const int g = i / K, e = i - g * K;
+    s.gd[g][e] = make_float4(L.param[g][e], L.a1[g][e], L.a2[g][e], 0.0f);
+  }
+  for (int g = threadIdx.x; g < L.ngroups; g += blockDim.x) {
+    s.sc[g] = make_float4(L.sc[g][0], L.sc[g][1], L.sc[g][2], L.sc[g][3]);
+    s.eps[g] = L.sc[g][4];
+  }
+  for (int i = threadIdx.x; i < dim; i += blockDim.x) s.col_group[i] = L.col_group[i];
+}
+
+// deferred_scalar (adam.hpp:102-110) with the exact zero-numerator shortcut of the restoration
+// term: (w_scale * m) / (sqrt(v) + eps) is the signed zero w_scale * m itself whenever it is zero
+// and v >= 0 (the denominator is then >= eps > 0) — every delay-0 row, i.e. every row touched
+// with a gradient the previous pass. Bit-identical to deferred_scalar.
+__device__ __forceinline__ void deferred_scalar_fast(float& w, float& m, float& v, float g, float4 gd, float4 sc,
+                                                     float eps) {
+  const float m_new = gd.y * m + sc.x * g;
+  const float v_new = gd.z * v + sc.y * g * g;
+  const float num = gd.x * m;
+  w = (num == 0.0f && v >= 0.0f) ? w - num : w - div_rn(num, sqrtf(v) + eps);
+  const float denom = div_rn(sqrtf(v_new), sc.z) + eps;
+  w = w - div_rn(sc.w * m_new, denom);
+  m = m_new;
+  v = v_new;
+}
+
+// Streams a touch list: a warp owns 32 list entries (rows) at a time and walks their flattened
+// (row, column) space, 32 x dim elements = dim iterations with every lane busy (lane l takes
+// elements l, l + 32, ...; consecutive lanes read consecutive columns, so each warp access is one
+// or two contiguous row spans). The 32 rows' (id, delay, gradient slot) sit in the lanes'
+// registers and are fetched with shuffles; kU elements per lane have all their loads in flight
+// before any math.
+#ifndef GSS_WALK_KU
+#define GSS_WALK_KU 4
+#endif
+#ifndef GSS_WALK_MINB
+#define GSS_WALK_MINB 4
+#endif
 template <int K, int MODE>
-__global__ void __launch_bounds__(kUpdThreads, 4) walk_kernel(ArenaDev a, GradsDev gr, const __grid_constant__ LutArgs<K> L,
-                                                           TouchList tl) {
-  __shared__ SmemLuts<K> lut;
-  load_luts<K>(lut, L, a.dim);
+__global__ void __launch_bounds__(kUpdThreads, GSS_WALK_MINB) walk_kernel(ArenaDev a, GradsDev gr, const __grid_constant__ LutArgs<K> L,
+                                                        TouchList tl) {
+  __shared__ PackedLuts<K> lut;
+  load_packed_luts<K>(lut, L, a.dim);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t T = (int64_t)*tl.count;
   const int dim = a.dim;
-  constexpr int kRB = 4;
-  const int npass = (dim + 31) >> 5;
-  const int64_t wstride = (int64_t)gridDim.x * (kUpdThreads / 32) * kRB;
-  for (int64_t t0 = ((int64_t)blockIdx.x * (kUpdThreads / 32) + (threadIdx.x >> 5)) * kRB; t0 < T; t0 += wstride) {
-    int64_t rbase[kRB];
-    int d[kRB], sl[kRB];
+  const int dq = 32 / dim, dr = 32 - dq * dim;  // per-iteration advance of (row, col)
+  constexpr int kU = GSS_WALK_KU;
+  const int64_t wstride = (int64_t)gridDim.x * (kUpdThreads / 32) * 32;
+  for (int64_t t0 = ((int64_t)blockIdx.x * (kUpdThreads / 32) + (threadIdx.x >> 5)) * 32; t0 < T; t0 += wstride) {
+    // this lane's list entry (row t0 + lane)
+    const bool mine = t0 + lane < T;
+    const int32_t my_row = mine ? tl.row[t0 + lane] : -1;
+    const int32_t my_del = mine ? tl.del[t0 + lane] : 0;
+    const int32_t my_slot = (mine && MODE == kDeferred) ? tl.slot[t0 + lane] : -1;
+    int r = lane / dim, c = lane - (lane / dim) * dim;
+    for (int i0 = 0; i0 < dim; i0 += kU) {
+      float w[kU], m[kU], v[kU], gv[kU];
+      size_t off[kU];
+      int dd[kU], cc[kU];
+      bool ok[kU];
 #pragma unroll
-    for (int u = 0; u < kRB; ++u) {
-      const bool ok = t0 + u < T;
-      rbase[u] = ok ? (int64_t)tl.row[t0 + u] * dim : -1;
-      d[u] = ok ? tl.del[t0 + u] : 0;
-      sl[u] = (ok && MODE == kDeferred) ? tl.slot[t0 + u] : -1;
-    }
-    for (int p = 0; p < npass; ++p) {
-      const int c = p * 32 + lane;
-      const bool cok = c < dim;
-      const int g = cok ? lut.col_group[c] : 0;
-      float w[kRB], m[kRB], v[kRB], gv[kRB];
-#pragma unroll
-      for (int u = 0; u < kRB; ++u) {
-        const bool ok = cok && rbase[u] >= 0;
-        const size_t off = ok ? (size_t)(rbase[u] + c) : 0;
-        w[u] = ok ? a.w[off] : 0.0f;
-        m[u] = ok ? a.m[off] : 0.0f;
-        v[u] = ok ? a.v[off] : 0.0f;
-        gv[u] = (cok && sl[u] >= 0) ? gr.rows[(size_t)sl[u] * gr.stride + gr.col0 + c] : 0.0f;
+      for (int u = 0; u < kU; ++u) {
+        const int rr = r < 32 ? r : 31;
+        const int32_t row = __shfl_sync(0xffffffffu, my_row, rr);
+        const int32_t sl = __shfl_sync(0xffffffffu, my_slot, rr);
+        dd[u] = __shfl_sync(0xffffffffu, my_del, rr);
+        cc[u] = c;
+        ok[u] = i0 + u < dim && row >= 0;
+        off[u] = ok[u] ? (size_t)row * dim + c : 0;
+        w[u] = ok[u] ? a.w[off[u]] : 0.0f;
+        m[u] = ok[u] ? a.m[off[u]] : 0.0f;
+        v[u] = ok[u] ? a.v[off[u]] : 0.0f;
+        gv[u] = (ok[u] && sl >= 0) ? gr.rows[(size_t)sl * gr.stride + gr.col0 + c] : 0.0f;
+        r += dq;
+        c += dr;
+        if (c >= dim) {
+          c -= dim;
+          ++r;
+        }
       }
 #pragma unroll
-      for (int u = 0; u < kRB; ++u) {
-        if (!(cok && rbase[u] >= 0)) continue;
-        const size_t off = (size_t)(rbase[u] + c);
+      for (int u = 0; u < kU; ++u) {
+        if (!ok[u]) continue;
+        const int g = lut.col_group[cc[u]];
+        const float4 gd = lut.gd[g][dd[u]];
         if (MODE == kDeferred) {
-          deferred_scalar(w[u], m[u], v[u], gv[u], lut.param[g][d[u]], lut.a1[g][d[u]], lut.a2[g][d[u]], lut.sc[g]);
-          a.w[off] = w[u];
-          a.m[off] = m[u];
-          a.v[off] = v[u];
+          deferred_scalar_fast(w[u], m[u], v[u], gv[u], gd, lut.sc[g], lut.eps[g]);
+          a.w[off[u]] = w[u];
+          a.m[off[u]] = m[u];
+          a.v[off[u]] = v[u];
         } else {
-          a.w[off] = w[u] - div_rn(lut.param[g][d[u]] * m[u], sqrtf(v[u]) + lut.sc[g][4]);  // adam.hpp:112-114
-          a.m[off] = m[u] * lut.a1[g][d[u]];
-          a.v[off] = v[u] * lut.a2[g][d[u]];
+          a.w[off[u]] = w[u] - div_rn(gd.x * m[u], sqrtf(v[u]) + lut.eps[g]);  // adam.hpp:112-114
+          a.m[off[u]] = m[u] * gd.y;
+          a.v[off[u]] = v[u] * gd.z;
         }
       }
     }
@@ -426,17 +586,17 @@ __global__ void __launch_bounds__(kUpdThreads, 4) walk_kernel(ArenaDev a, GradsD
 constexpr int kRestoreChunk = kUpdThreads;
 constexpr int kSeg = 2048;
 template <int K>
-__global__ void __launch_bounds__(kUpdThreads, 4) restore_kernel(ArenaDev a, const int32_t* ids, int64_t count,
+__global__ void __launch_bounds__(kUpdThreads, GSS_WALK_MINB) restore_kernel(ArenaDev a, const int32_t* ids, int64_t count,
                                                               const int64_t* count_dev, GradsDev pend,
                                                               const int32_t* pbstart, int has_pending,
                                                               const __grid_constant__ LutArgs<K> L, float* out) {
-  __shared__ SmemLuts<K> lut;
+  __shared__ PackedLuts<K> lut;
   __shared__ int32_t cid[kRestoreChunk];
   __shared__ uint8_t cdel[kRestoreChunk];
   __shared__ int32_t cslot[kRestoreChunk];
   __shared__ int32_t seg[kSeg];
   __shared__ int seg_lo, seg_n;
-  load_luts<K>(lut, L, a.dim);
+  load_packed_luts<K>(lut, L, a.dim);
   const int64_t cnt = count_dev ? *count_dev : count;
   const int64_t pcnt = has_pending ? grads_count(pend) : 0;
   const int nblk = (int)((a.n + kRowsPerBlock - 1) / kRowsPerBlock);
@@ -486,40 +646,57 @@ __global__ void __launch_bounds__(kUpdThreads, 4) restore_kernel(ArenaDev a, con
       }
     }
     __syncthreads();
-    // Warp per id, lanes on consecutive columns; kRB ids per warp with all loads issued first.
-    constexpr int kRB = 4;
-    const int npass = (dim + 31) >> 5;
+    // Flattened walk: warp w owns ids [32w, 32w + 32) of the chunk and streams their 32 x dim
+    // (id, column) elements with every lane busy (see walk_kernel); all kU loads in flight first.
     const int lane = tid & 31, warp = tid >> 5;
-    for (int t0 = warp * kRB; t0 < nk; t0 += (kUpdThreads / 32) * kRB) {
-      for (int p = 0; p < npass; ++p) {
-        const int c = p * 32 + lane;
-        const bool cok = c < dim;
-        const int g = cok ? lut.col_group[c] : 0;
-        float w[kRB], m[kRB], v[kRB], gv[kRB];
+    const int j = warp * 32 + lane;
+    const int32_t my_id = j < nk ? cid[j] : -1;
+    const int32_t my_del = j < nk ? cdel[j] : 0;
+    const int32_t my_slot = (j < nk && has_pending) ? cslot[j] : -1;
+    const int dq = 32 / dim, dr = 32 - dq * dim;
+    int r = lane / dim, c = lane - (lane / dim) * dim;
+    constexpr int kU = GSS_WALK_KU;
+    if (warp * 32 < nk) {
+      for (int i0 = 0; i0 < dim; i0 += kU) {
+        float w[kU], m[kU], v[kU], gv[kU];
+        size_t oo[kU];
+        int dd[kU], cc[kU];
+        bool ok[kU];
 #pragma unroll
-        for (int u = 0; u < kRB; ++u) {
-          const int t = t0 + u;
-          const bool ok = cok && t < nk;
-          const size_t off = ok ? (size_t)cid[t] * dim + c : 0;
-          const int sl = (ok && has_pending) ? cslot[t] : -1;
-          w[u] = ok ? a.w[off] : 0.0f;
-          m[u] = ok ? a.m[off] : 0.0f;
-          v[u] = ok ? a.v[off] : 0.0f;
-          gv[u] = sl >= 0 ? pend.rows[(size_t)sl * pend.stride + pend.col0 + c] : 0.0f;
+        for (int u = 0; u < kU; ++u) {
+          const int rr = r < 32 ? r : 31;
+          const int32_t id2 = __shfl_sync(0xffffffffu, my_id, rr);
+          const int32_t sl = __shfl_sync(0xffffffffu, my_slot, rr);
+          dd[u] = __shfl_sync(0xffffffffu, my_del, rr);
+          cc[u] = c;
+          ok[u] = i0 + u < dim && id2 >= 0;
+          const size_t off = ok[u] ? (size_t)id2 * dim + c : 0;
+          oo[u] = (size_t)(k0 + warp * 32 + rr) * dim + c;
+          w[u] = ok[u] ? a.w[off] : 0.0f;
+          m[u] = ok[u] ? a.m[off] : 0.0f;
+          v[u] = ok[u] ? a.v[off] : 0.0f;
+          gv[u] = (ok[u] && sl >= 0) ? pend.rows[(size_t)sl * pend.stride + pend.col0 + c] : 0.0f;
+          r += dq;
+          c += dr;
+          if (c >= dim) {
+            c -= dim;
+            ++r;
+          }
         }
 #pragma unroll
-        for (int u = 0; u < kRB; ++u) {
-          const int t = t0 + u;
-          if (!(cok && t < nk)) continue;
-          const int d = cdel[t];
+        for (int u = 0; u < kU; ++u) {
+          if (!ok[u]) continue;
+          const int g = lut.col_group[cc[u]];
+          const float4 gd = lut.gd[g][dd[u]];
           float ww = w[u];
           if (has_pending) {
             float mm = m[u], vv = v[u];
-            deferred_scalar(ww, mm, vv, gv[u], lut.param[g][d], lut.a1[g][d], lut.a2[g][d], lut.sc[g]);
-          } else {
-            ww = ww - div_rn(lut.param[g][d] * m[u], sqrtf(v[u]) + lut.sc[g][4]);
+            deferred_scalar_fast(ww, mm, vv, gv[u], gd, lut.sc[g], lut.eps[g]);
+          } else {  // restore_scalar (adam.hpp:112-114), zero-numerator shortcut as deferred_scalar_fast
+            const float num = gd.x * m[u];
+            ww = (num == 0.0f && v[u] >= 0.0f) ? ww - num : ww - div_rn(num, sqrtf(v[u]) + lut.eps[g]);
           }
-          out[(size_t)(k0 + t) * dim + c] = ww;
+          out[oo[u]] = ww;
         }
       }
     }
@@ -597,9 +774,8 @@ void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* 
   int32_t* bstart = nullptr;
   if (MODE == kDeferred && gd.ids) bstart = build_index(a, gd, err, st);
   const int blocks = (int)ceil_div(a.n, kRowsPerBlock);
-  if (MODE == kDeferred && a.defer_max == 0 && a.dim <= 32) {
-    update_kernel<K, MODE, true><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, bstart, *L, tmask, tcount, err,
-                                                                  TouchList{});
+  if (MODE == kDeferred && a.defer_max == 0) {
+    dense_update_kernel<K><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, bstart, *L, tcount, tmask);
     GSS_LAUNCHED();
   } else {
     // Pass 1: counters + touch list; pass 2: stream the list.
@@ -615,8 +791,8 @@ void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* 
     update_kernel<K, MODE, false><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, bstart, *L, tmask, tcount, err,
                                                                    tl);
     GSS_LAUNCHED();
-    const int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, (kUpdThreads / 32) * 4),
-                                                                    (int64_t)sm_count() * 4));
+    const int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, kUpdThreads),
+                                                                    (int64_t)sm_count() * 8));
     walk_kernel<K, MODE><<<wblocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, *L, tl);
     GSS_LAUNCHED();
     GSS_CUDA(cudaFreeAsync(buf, st));
