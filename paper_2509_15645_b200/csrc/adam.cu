@@ -124,13 +124,20 @@ __device__ __forceinline__ float div_rn(float n, float d) {
   return __fdiv_rn(n, d);
 }
 
+// IEEE sqrtf with +-0 answered without CUDA's out-of-range slow path (sqrt(+-0) = +-0): rows never
+// touched have v = 0 exactly, and one such lane would send its whole warp through the subroutine.
+__device__ __forceinline__ float sqrt_rn(float x) {
+  const float s = sqrtf(x == 0.0f ? 1.0f : x);
+  return x == 0.0f ? x : s;
+}
+
 // deferred_scalar (adam.hpp:102-110)
 __device__ __forceinline__ void deferred_scalar(float& w, float& m, float& v, float g, float ws, float ms, float vs,
                                                 const float* sc) {
   const float m_new = ms * m + sc[0] * g;
   const float v_new = vs * v + sc[1] * g * g;
-  w -= div_rn(ws * m, sqrtf(v) + sc[4]);
-  const float denom = div_rn(sqrtf(v_new), sc[2]) + sc[4];
+  w -= div_rn(ws * m, sqrt_rn(v) + sc[4]);
+  const float denom = div_rn(sqrt_rn(v_new), sc[2]) + sc[4];
   w = w - div_rn(sc[3] * m_new, denom);
   m = m_new;
   v = v_new;
@@ -181,10 +188,9 @@ __global__ void index_kernel(const int32_t* ids, int64_t count, const int64_t* c
   }
 }
 
-// One pass of deferred_update (adam.hpp:211-238) or flush_deferred (adam.hpp:293-313) over
-// rows [blockIdx*1024, +1024). DENSE: an arena with defer_max 0 (the geometric tier,
-// store.hpp:121-124) — every row is touched at delay 0 and counters stay 0, so the pass is a
-// contiguous vectorised stream over the block's rows (float4 loads/stores of w, m, v).
+// Pass 1 of deferred_update (adam.hpp:211-238) or flush_deferred (adam.hpp:293-313) over rows
+// [blockIdx*1024, +1024): counters and the touch list that walk_kernel (pass 2) streams.
+// (Arenas with defer_max 0 take dense_update_kernel instead.)
 struct TouchList {  // rows a deferred pass touches (unordered; each row at most once)
   int32_t* row;
   int32_t* slot;
@@ -192,7 +198,7 @@ struct TouchList {  // rows a deferred pass touches (unordered; each row at most
   unsigned long long* count;
 };
 
-template <int K, int MODE, bool DENSE>
+template <int K, int MODE>
 __global__ void __launch_bounds__(kUpdThreads) update_kernel(ArenaDev a, GradsDev gr, const int32_t* bstart,
                                                              const __grid_constant__ LutArgs<K> L,
                                                              uint32_t* touched_mask, int64_t* touched_count,
@@ -219,60 +225,6 @@ __global__ void __launch_bounds__(kUpdThreads) update_kernel(ArenaDev a, GradsDe
   }
   __syncthreads();
   const int dim = a.dim;
-  if (DENSE) {
-    // Every row at delay 0 (w_scale = 0: the restoration term is w - (+-0), kept exactly);
-    // counters untouched (they stay 0 under defer_max 0). Lane-fixed columns: lanes 0..rpp*dim-1
-    // of a warp cover rpp consecutive rows, so each lane's column group and constants live in
-    // registers and every warp access is one contiguous span.
-    const int rpp = 32 / dim;  // rows per warp pass
-    const int rr = lane / dim, c = lane - rr * dim;
-    const bool act = rr < rpp;
-    const int g = act ? lut.col_group[c] : 0;
-    const float ms = lut.a1[g][0], vs = lut.a2[g][0];
-    const float s0 = lut.sc[g][0], s1 = lut.sc[g][1], s2 = lut.sc[g][2], s3 = lut.sc[g][3], s4 = lut.sc[g][4];
-    const int npass = (nrows + rpp - 1) / rpp;
-    constexpr int kU = 4;  // passes per warp in flight: all loads issued before any math
-    constexpr int kW = kUpdThreads / 32;
-    for (int p0 = warp; p0 < npass; p0 += kW * kU) {
-      float w[kU], m[kU], v[kU], gv[kU];
-      size_t off[kU];
-      bool ok[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int lr = (p0 + u * kW) * rpp + rr;
-        ok[u] = act && p0 + u * kW < npass && lr < nrows;
-        off[u] = ok[u] ? (size_t)(r0 + lr) * dim + c : 0;
-        const int sl = ok[u] ? slot_of[lr] : -1;
-        w[u] = ok[u] ? a.w[off[u]] : 0.0f;
-        m[u] = ok[u] ? a.m[off[u]] : 0.0f;
-        v[u] = ok[u] ? a.v[off[u]] : 0.0f;
-        gv[u] = sl >= 0 ? gr.rows[(size_t)sl * gr.stride + gr.col0 + c] : 0.0f;
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        if (!ok[u]) continue;
-        const float m_new = ms * m[u] + s0 * gv[u];
-        const float v_new = vs * v[u] + s1 * gv[u] * gv[u];
-        // (0 * m) / (sqrt(v) + eps) is (0 * m) itself whenever v >= 0 (denominator >= eps > 0).
-        const float num = 0.0f * m[u];
-        float ww = v[u] >= 0.0f ? w[u] - num : w[u] - div_rn(num, sqrtf(v[u]) + s4);
-        const float denom = div_rn(sqrtf(v_new), s2) + s4;
-        ww = ww - div_rn(s3 * m_new, denom);
-        a.w[off[u]] = ww;
-        a.m[off[u]] = m_new;
-        a.v[off[u]] = v_new;
-      }
-    }
-    if (touched_count && tid == 0 && nrows > 0)
-      atomicAdd((unsigned long long*)touched_count, (unsigned long long)nrows);
-    if (touched_mask) {
-      for (int wi = tid; wi * 32 < nrows; wi += kUpdThreads) {
-        const int rem = nrows - wi * 32;
-        touched_mask[(r0 >> 5) + wi] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
-      }
-    }
-    return;
-  }
   // Counter pass: 4 consecutive rows per thread (one 32-bit load/store of counters).
   int my_cnt = 0;
   uint8_t del[4];
@@ -407,8 +359,8 @@ __global__ void __launch_bounds__(kUpdThreads) dense_update_kernel(ArenaDev a, G
     const float m_new = A.x * m + A.z * gv;
     const float v_new = A.y * v + A.w * gv * gv;
     const float num = 0.0f * m;  // w_scale(0) * m
-    w = (num == 0.0f && v >= 0.0f) ? w - num : w - div_rn(num, sqrtf(v) + B.z);
-    const float denom = div_rn(sqrtf(v_new), B.x) + B.z;
+    w = (num == 0.0f && v >= 0.0f) ? w - num : w - div_rn(num, sqrt_rn(v) + B.z);
+    const float denom = div_rn(sqrt_rn(v_new), B.x) + B.z;
     w = w - div_rn(B.y * m_new, denom);
     m = m_new;
     v = v_new;
@@ -495,8 +447,8 @@ __device__ __forceinline__ void deferred_scalar_fast(float& w, float& m, float& 
   const float m_new = gd.y * m + sc.x * g;
   const float v_new = gd.z * v + sc.y * g * g;
   const float num = gd.x * m;
-  w = (num == 0.0f && v >= 0.0f) ? w - num : w - div_rn(num, sqrtf(v) + eps);
-  const float denom = div_rn(sqrtf(v_new), sc.z) + eps;
+  w = (num == 0.0f && v >= 0.0f) ? w - num : w - div_rn(num, sqrt_rn(v) + eps);
+  const float denom = div_rn(sqrt_rn(v_new), sc.z) + eps;
   w = w - div_rn(sc.w * m_new, denom);
   m = m_new;
   v = v_new;
@@ -569,7 +521,7 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_WALK_MINB) walk_kernel(ArenaD
           a.m[off[u]] = m[u];
           a.v[off[u]] = v[u];
         } else {
-          a.w[off[u]] = w[u] - div_rn(gd.x * m[u], sqrtf(v[u]) + lut.eps[g]);  // adam.hpp:112-114
+          a.w[off[u]] = w[u] - div_rn(gd.x * m[u], sqrt_rn(v[u]) + lut.eps[g]);  // adam.hpp:112-114
           a.m[off[u]] = m[u] * gd.y;
           a.v[off[u]] = v[u] * gd.z;
         }
@@ -694,7 +646,7 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_WALK_MINB) restore_kernel(Are
             deferred_scalar_fast(ww, mm, vv, gv[u], gd, lut.sc[g], lut.eps[g]);
           } else {  // restore_scalar (adam.hpp:112-114), zero-numerator shortcut as deferred_scalar_fast
             const float num = gd.x * m[u];
-            ww = (num == 0.0f && v[u] >= 0.0f) ? ww - num : ww - div_rn(num, sqrtf(v[u]) + lut.eps[g]);
+            ww = (num == 0.0f && v[u] >= 0.0f) ? ww - num : ww - div_rn(num, sqrt_rn(v[u]) + lut.eps[g]);
           }
           out[oo[u]] = ww;
         }
@@ -788,7 +740,7 @@ void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* 
     tl.slot = tl.row + n;
     tl.del = reinterpret_cast<uint8_t*>(tl.slot + n);
     GSS_CUDA(cudaMemsetAsync(tl.count, 0, 8, st));
-    update_kernel<K, MODE, false><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, bstart, *L, tmask, tcount, err,
+    update_kernel<K, MODE><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, bstart, *L, tmask, tcount, err,
                                                                    tl);
     GSS_LAUNCHED();
     const int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, kUpdThreads),
