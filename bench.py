@@ -383,7 +383,7 @@ def kernel_probe(G, truth, cams, dev, a):
     # deferred Adam, 49-wide non-geo tier (adam.hpp:211-238):
     # B = sum_touched 4*49*(6 + has_grad) + 2 N
     opt = G.OptimConfig()
-    arena = G.Arena(n, 49, opt.nongeo_groups(), 15, device=dev)
+    arena = G.Arena(n, 49, opt.nongeo_groups(), 15, device=dev, interleaved=True)  # the engine's layout
     arena.w.uniform_(-1, 1)
     dens = 0.0828
     gen = torch.Generator(device=dev)

@@ -49,7 +49,10 @@ typedef struct {
 
 /* Arena<float> (adam.hpp:119-159): row-major w/m/v [n][dim] + uint8 counter[n], all device
  * pointers (or pinned host pointers where documented). `step` = applied update passes; the
- * update entry points advance it on the host at enqueue time. */
+ * update entry points advance it on the host at enqueue time. row_stride (floats between
+ * consecutive rows of w, m and v; 0 = dim) lets w/m/v share one row-interleaved buffer
+ * (w = base, m = base + dim, v = base + 2*dim, row_stride >= 3*dim): a touched row is then one
+ * contiguous span instead of three scattered ones (the reference layout is row_stride = dim). */
 typedef struct {
   float* w;
   float* m;
@@ -61,6 +64,7 @@ typedef struct {
   int64_t step;
   int32_t ngroups;
   gss_group groups[8];
+  int64_t row_stride;
 } gss_arena;
 
 /* SparseGrads<float> (adam.hpp:163-169): sorted ids; row(k) = rows + k*stride + col0.

@@ -59,6 +59,7 @@ class GssArena(C.Structure):
         ("step", C.c_int64),
         ("ngroups", C.c_int32),
         ("groups", GssGroup * 8),
+        ("row_stride", C.c_int64),
     ]
 
 

@@ -94,6 +94,7 @@ struct ArenaDev {
   int dim;
   int defer_max;
   uint32_t div_magic;  // ceil(2^32 / dim)
+  int64_t stride;      // floats between rows of w, m, v (>= dim)
 };
 
 struct GradsDev {
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_WALK_MINB) walk_kernel(ArenaD
         dd[u] = __shfl_sync(0xffffffffu, my_del, rr);
         cc[u] = c;
         ok[u] = i0 + u < dim && row >= 0;
-        off[u] = ok[u] ? (size_t)row * dim + c : 0;
+        off[u] = ok[u] ? (size_t)row * a.stride + c : 0;
         w[u] = ok[u] ? a.w[off[u]] : 0.0f;
         m[u] = ok[u] ? a.m[off[u]] : 0.0f;
         v[u] = ok[u] ? a.v[off[u]] : 0.0f;
@@ -528,6 +529,115 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_WALK_MINB) walk_kernel(ArenaD
       }
     }
   }
+}
+
+// Vector walk for arenas whose w/m/v rows are 16-byte aligned with whole float4 row segments
+// (row_stride % 4 == 0: the engine's row-interleaved non-geometric tier, w @ 0, m @ 52, v @ 104 of a
+// 160-float row). A unit = 4 consecutive columns of one row: one 16-byte load/store each of w, m,
+// v; a warp walks the flattened (row, unit) space of 32 list rows, so the per-element address
+// arithmetic and shuffles of the scalar walk are amortised over 4 columns. Columns dim..4*nq-1 of
+// the last unit are row padding (never read back as data).
+#ifndef GSS_WALK4_KU
+#define GSS_WALK4_KU 2
+#endif
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float& at(float4& v, int i) {
+  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(kUpdThreads, 3) walk4_kernel(ArenaDev a, GradsDev gr,
+                                                                         const __grid_constant__ LutArgs<K> L,
+                                                                         TouchList tl) {
+  __shared__ PackedLuts<K> lut;
+  load_packed_luts<K>(lut, L, a.dim);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t T = (int64_t)*tl.count;
+  const int dim = a.dim;
+  const int nq = (dim + 3) >> 2;  // float4 units per row
+  const int dq = 32 / nq, dr = 32 - dq * nq;
+  constexpr int kU = GSS_WALK4_KU;
+  const int64_t wstride = (int64_t)gridDim.x * (kUpdThreads / 32) * 32;
+  for (int64_t t0 = ((int64_t)blockIdx.x * (kUpdThreads / 32) + (threadIdx.x >> 5)) * 32; t0 < T; t0 += wstride) {
+    const bool mine = t0 + lane < T;
+    const int64_t my_base = mine ? (int64_t)tl.row[t0 + lane] * a.stride : -1;
+    const int32_t my_del = mine ? tl.del[t0 + lane] : 0;
+    const int32_t my_slot = (mine && MODE == kDeferred) ? tl.slot[t0 + lane] : -1;
+    int r = lane / nq, q = lane - (lane / nq) * nq;
+    for (int i0 = 0; i0 < nq; i0 += kU) {
+      float4 w[kU], m[kU], v[kU];
+      float gv[kU][4];
+      int64_t base[kU];
+      int dd[kU], c0[kU];
+      bool ok[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int rr = r < 32 ? r : 31;
+        base[u] = __shfl_sync(0xffffffffu, my_base, rr);
+        const int32_t sl = __shfl_sync(0xffffffffu, my_slot, rr);
+        dd[u] = __shfl_sync(0xffffffffu, my_del, rr);
+        c0[u] = 4 * q;
+        ok[u] = i0 + u < nq && base[u] >= 0;
+        const int64_t o = ok[u] ? base[u] + c0[u] : 0;
+        w[u] = ok[u] ? ld4(a.w + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+        m[u] = ok[u] ? ld4(a.m + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[u] = ok[u] ? ld4(a.v + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float* grow = gr.rows + (int64_t)sl * gr.stride + gr.col0 + c0[u];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          gv[u][i] = (ok[u] && sl >= 0 && c0[u] + i < dim) ? grow[i] : 0.0f;
+        r += dq;
+        q += dr;
+        if (q >= nq) {
+          q -= nq;
+          ++r;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (!ok[u]) continue;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int c = c0[u] + i < dim ? c0[u] + i : dim - 1;  // padding columns reuse a valid group
+          const int g = lut.col_group[c];
+          const float4 gd = lut.gd[g][dd[u]];
+          if (MODE == kDeferred) {
+            deferred_scalar_fast(at(w[u], i), at(m[u], i), at(v[u], i), gv[u][i], gd, lut.sc[g], lut.eps[g]);
+          } else {
+            at(w[u], i) = at(w[u], i) - div_rn(gd.x * at(m[u], i), sqrt_rn(at(v[u], i)) + lut.eps[g]);
+            at(m[u], i) = at(m[u], i) * gd.y;
+            at(v[u], i) = at(v[u], i) * gd.z;
+          }
+        }
+        const int64_t o = base[u] + c0[u];
+        st4(a.w + o, w[u]);
+        st4(a.m + o, m[u]);
+        st4(a.v + o, v[u]);
+      }
+    }
+  }
+}
+
+// Can w/m/v be walked with 16-byte accesses? Row segments 16-byte aligned and non-overlapping
+// when rounded up to whole float4 units.
+bool vector_rows(const gss_arena& a) {
+  const int64_t stride = a.row_stride > 0 ? a.row_stride : a.dim;
+  if (stride % 4 != 0) return false;
+  for (const float* p : {a.w, a.m, a.v})
+    if (reinterpret_cast<uintptr_t>(p) % 16 != 0) return false;
+  const int64_t seg = ((a.dim + 3) / 4) * 4;
+  if (seg > stride) return false;
+  const float* ps[3] = {a.w, a.m, a.v};
+  for (int i = 0; i < 3; ++i)
+    for (int j = i + 1; j < 3; ++j) {
+      const int64_t d = ps[i] - ps[j];
+      const int64_t ad = d < 0 ? -d : d;
+      if (ad < seg && ad != 0) return false;  // same row: the padded segments must not overlap
+      if (ad == 0) return false;
+    }
+  return true;
 }
 
 // restore_view (adam.hpp:252-289): out[k] = restored row ids[k] (+ pending pass). Grid-stride
@@ -622,7 +732,7 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_WALK_MINB) restore_kernel(Are
           dd[u] = __shfl_sync(0xffffffffu, my_del, rr);
           cc[u] = c;
           ok[u] = i0 + u < dim && id2 >= 0;
-          const size_t off = ok[u] ? (size_t)id2 * dim + c : 0;
+          const size_t off = ok[u] ? (size_t)id2 * a.stride + c : 0;
           oo[u] = (size_t)(k0 + warp * 32 + rr) * dim + c;
           w[u] = ok[u] ? a.w[off] : 0.0f;
           m[u] = ok[u] ? a.m[off] : 0.0f;
@@ -660,6 +770,7 @@ ArenaDev arena_dev(const gss_arena& a) {
   d.w = a.w; d.m = a.m; d.v = a.v; d.counter = a.counter;
   d.n = a.n; d.dim = a.dim; d.defer_max = a.defer_max;
   d.div_magic = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)a.dim - 1) / (uint64_t)a.dim);
+  d.stride = a.row_stride > 0 ? a.row_stride : a.dim;
   return d;
 }
 
@@ -679,6 +790,7 @@ void validate_arena(const gss_arena& a) {
     covered += G.dim;
   }
   require(covered == a.dim, "arena: group dims must cover the row");
+  require(a.row_stride == 0 || a.row_stride >= a.dim, "arena: row_stride must be 0 or >= dim");
   require(a.n == 0 || (a.w && a.m && a.v && a.counter), "arena: null buffer");
 }
 
@@ -726,7 +838,7 @@ void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* 
   int32_t* bstart = nullptr;
   if (MODE == kDeferred && gd.ids) bstart = build_index(a, gd, err, st);
   const int blocks = (int)ceil_div(a.n, kRowsPerBlock);
-  if (MODE == kDeferred && a.defer_max == 0) {
+  if (MODE == kDeferred && a.defer_max == 0 && (a.row_stride == 0 || a.row_stride == a.dim)) {
     dense_update_kernel<K><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, bstart, *L, tcount, tmask);
     GSS_LAUNCHED();
   } else {
@@ -745,7 +857,10 @@ void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* 
     GSS_LAUNCHED();
     const int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, kUpdThreads),
                                                                     (int64_t)sm_count() * 8));
-    walk_kernel<K, MODE><<<wblocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, *L, tl);
+    if (vector_rows(a))
+      walk4_kernel<K, MODE><<<wblocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, *L, tl);
+    else
+      walk_kernel<K, MODE><<<wblocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, *L, tl);
     GSS_LAUNCHED();
     GSS_CUDA(cudaFreeAsync(buf, st));
   }
@@ -833,11 +948,12 @@ __global__ void __launch_bounds__(kUpdThreads) dense_kernel(ArenaDev a, const fl
     const int64_t row = f / a.dim;
     const int c = (int)(f - row * a.dim);
     const int g = lut.col_group[c];
-    float w = a.w[f], m = a.m[f], v = a.v[f];
+    const int64_t o = row * a.stride + c;
+    float w = a.w[o], m = a.m[o], v = a.v[o];
     deferred_scalar(w, m, v, grads ? grads[f] : 0.0f, lut.param[g][0], lut.a1[g][0], lut.a2[g][0], lut.sc[g]);
-    a.w[f] = w;
-    a.m[f] = m;
-    a.v[f] = v;
+    a.w[o] = w;
+    a.m[o] = m;
+    a.v[o] = v;
   }
 }
 }  // namespace

@@ -46,6 +46,11 @@ namespace gssd {
 namespace {
 
 constexpr int kGeoDim = 10, kNgDim = 49, kRowDim = 59;
+// Non-geometric tier layout: w, m, v of a row interleaved in one 640-byte span (5 x 128-byte
+// lines: w at 0, m at 52, v at 104, each segment 16-byte aligned and padded to 13 float4), so a
+// touched row of the deferred update / forwarding gather is five whole cache lines walked with
+// 16-byte accesses instead of three scattered 196-byte rows.
+constexpr int kNgStride = 160, kNgSeg = 52;
 
 __global__ void handoff_stats_kernel(const int32_t* ids, const int64_t* count, const float* mean2d, double* norm,
                                      int32_t* cnt) {
@@ -63,7 +68,7 @@ __global__ void split_rows_kernel(const float* rows, int64_t n, float* geo, floa
   if (i >= n * kRowDim) return;
   const int64_t r = i / kRowDim;
   const int c = (int)(i - r * kRowDim);
-  if (c < kGeoDim) geo[r * kGeoDim + c] = rows[i]; else ng[r * kNgDim + (c - kGeoDim)] = rows[i];
+  if (c < kGeoDim) geo[r * kGeoDim + c] = rows[i]; else ng[r * kNgStride + (c - kGeoDim)] = rows[i];
 }
 
 __global__ void join_rows_kernel(const float* geo, const float* ng, int64_t n, float* rows) {
@@ -442,21 +447,18 @@ gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss
   e->gv = dmalloc<float>(nn * kGeoDim);
   e->gcnt = dmalloc<uint8_t>(nn);
   if (e->ng_host) {
-    GSS_CUDA(cudaHostAlloc((void**)&e->nw, nn * kNgDim * 4, cudaHostAllocMapped));
-    GSS_CUDA(cudaHostAlloc((void**)&e->nm, nn * kNgDim * 4, cudaHostAllocMapped));
-    GSS_CUDA(cudaHostAlloc((void**)&e->nv, nn * kNgDim * 4, cudaHostAllocMapped));
+    GSS_CUDA(cudaHostAlloc((void**)&e->nw, nn * kNgStride * 4, cudaHostAllocMapped));
     GSS_CUDA(cudaHostAlloc((void**)&e->ncnt, nn, cudaHostAllocMapped));
   } else {
-    e->nw = dmalloc<float>(nn * kNgDim);
-    e->nm = dmalloc<float>(nn * kNgDim);
-    e->nv = dmalloc<float>(nn * kNgDim);
+    e->nw = dmalloc<float>(nn * kNgStride);
     e->ncnt = dmalloc<uint8_t>(nn);
   }
+  e->nm = e->nw + kNgSeg;
+  e->nv = e->nw + 2 * kNgSeg;
   GSS_CUDA(cudaMemsetAsync(e->gm, 0, nn * kGeoDim * 4, e->sD));
   GSS_CUDA(cudaMemsetAsync(e->gv, 0, nn * kGeoDim * 4, e->sD));
   GSS_CUDA(cudaMemsetAsync(e->gcnt, 0, nn, e->sD));
-  GSS_CUDA(cudaMemsetAsync(e->nm, 0, nn * kNgDim * 4, e->sD));
-  GSS_CUDA(cudaMemsetAsync(e->nv, 0, nn * kNgDim * 4, e->sD));
+  GSS_CUDA(cudaMemsetAsync(e->nw, 0, nn * kNgStride * 4, e->sD));
   GSS_CUDA(cudaMemsetAsync(e->ncnt, 0, nn, e->sD));
   if (n > 0) {
     float* rows_dev = dmalloc<float>((size_t)n * kRowDim);
@@ -468,6 +470,7 @@ gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss
   }
   setup_arena(e->geo, e->gw, e->gm, e->gv, e->gcnt, n, kGeoDim, cfg->geo_defer_max, true, *cfg);
   setup_arena(e->ng, e->nw, e->nm, e->nv, e->ncnt, n, kNgDim, cfg->defer_max, false, *cfg);
+  e->ng.row_stride = kNgStride;
   for (int p = 0; p < 3; ++p) {
     e->ids[p] = dmalloc<int32_t>(nn);
     e->count[p] = dmalloc<int64_t>(1);
@@ -511,9 +514,9 @@ void engine_destroy(gss_engine* e) {
   auto f = [](void* p) { if (p) cudaFree(p); };
   f(e->gts_dev); f(e->gw); f(e->gm); f(e->gv); f(e->gcnt);
   if (e->ng_host) {
-    cudaFreeHost(e->nw); cudaFreeHost(e->nm); cudaFreeHost(e->nv); cudaFreeHost(e->ncnt);
+    cudaFreeHost(e->nw); cudaFreeHost(e->ncnt);
   } else {
-    f(e->nw); f(e->nm); f(e->nv); f(e->ncnt);
+    f(e->nw); f(e->ncnt);
   }
   for (int p = 0; p < 3; ++p) { f(e->ids[p]); f(e->count[p]); }
   if (e->count_host) cudaFreeHost(e->count_host);
@@ -616,9 +619,12 @@ void engine_state(gss_engine* e, float* geo_w, float* ng_w, float* ng_m, float* 
   GSS_CUDA(cudaDeviceSynchronize());
   const size_t n = (size_t)e->n;
   if (geo_w) GSS_CUDA(cudaMemcpy(geo_w, e->gw, n * kGeoDim * 4, cudaMemcpyDefault));
-  if (ng_w) GSS_CUDA(cudaMemcpy(ng_w, e->nw, n * kNgDim * 4, cudaMemcpyDefault));
-  if (ng_m) GSS_CUDA(cudaMemcpy(ng_m, e->nm, n * kNgDim * 4, cudaMemcpyDefault));
-  if (ng_v) GSS_CUDA(cudaMemcpy(ng_v, e->nv, n * kNgDim * 4, cudaMemcpyDefault));
+  auto rows2d = [&](float* dst, const float* src) {  // strided tier rows -> packed n x 49
+    if (dst && n) GSS_CUDA(cudaMemcpy2D(dst, kNgDim * 4, src, kNgStride * 4, kNgDim * 4, n, cudaMemcpyDefault));
+  };
+  rows2d(ng_w, e->nw);
+  rows2d(ng_m, e->nm);
+  rows2d(ng_v, e->nv);
   if (ng_counter) GSS_CUDA(cudaMemcpy(ng_counter, e->ncnt, n, cudaMemcpyDefault));
   if (steps2) {
     steps2[0] = e->geo.step;

@@ -160,7 +160,8 @@ def build_group_luts(hp: Hyperparams, t: int, max_delay: int) -> GroupLuts:
 class Arena:
     """Arena<float> (adam.hpp:119-159) resident in device memory: w, m, v [n, dim] + uint8 counter."""
 
-    def __init__(self, n: int, dim: int, groups: Sequence[GroupSpec], defer_max: int, device=None):
+    def __init__(self, n: int, dim: int, groups: Sequence[GroupSpec], defer_max: int, device=None, *,
+                 interleaved: bool = False):
         if defer_max < 0 or defer_max > 254:
             raise ConfigError(2, "arena: defer max must be in [0, 254]")
         covered = 0
@@ -171,9 +172,18 @@ class Arena:
             raise ConfigError(2, "arena: group dims must cover the row")
         dev = _dev(device)
         self.count, self.dim, self.groups, self.defer_max = int(n), int(dim), list(groups), int(defer_max)
-        self.w = torch.zeros((n, dim), dtype=torch.float32, device=dev)
-        self.m = torch.zeros((n, dim), dtype=torch.float32, device=dev)
-        self.v = torch.zeros((n, dim), dtype=torch.float32, device=dev)
+        if interleaved:
+            # one row-interleaved buffer: [w | m | v | pad] per row, each segment padded to whole
+            # float4s (16-byte aligned), the row to whole 128-byte lines (the engine's layout)
+            seg = -(-dim // 4) * 4
+            self.row_stride = -(-3 * seg // 32) * 32
+            self._buf = torch.zeros((n, self.row_stride), dtype=torch.float32, device=dev)
+            self.w, self.m, self.v = (self._buf[:, i * seg:i * seg + dim] for i in range(3))
+        else:
+            self.row_stride = dim
+            self.w = torch.zeros((n, dim), dtype=torch.float32, device=dev)
+            self.m = torch.zeros((n, dim), dtype=torch.float32, device=dev)
+            self.v = torch.zeros((n, dim), dtype=torch.float32, device=dev)
         self.counter = torch.zeros(max(n, 1), dtype=torch.uint8, device=dev)[:n]
         self.step = 0
 
@@ -181,6 +191,7 @@ class Arena:
         a = GssArena()
         a.w, a.m, a.v, a.counter = _ptr(self.w), _ptr(self.m), _ptr(self.v), _ptr(self.counter)
         a.n, a.dim, a.defer_max, a.step = self.count, self.dim, self.defer_max, self.step
+        a.row_stride = self.row_stride
         a.ngroups = len(self.groups)
         for i, g in enumerate(self.groups):
             a.groups[i] = GssGroup(g.col0, g.dim, g.hp.lr, g.hp.beta1, g.hp.beta2, g.hp.eps)

@@ -254,7 +254,8 @@ class ShardTrainer:
         rows = torch.from_numpy(np.ascontiguousarray(init_rows, np.float32)).to(dev)
         self.n = int(rows.shape[0])
         self.geo = G.Arena(self.n, G.K_GEO_DIM, self.opt.geo_groups(), self.opt.geo_defer_max, device=dev)
-        self.ng = G.Arena(self.n, G.K_NONGEO_DIM, self.opt.nongeo_groups(), self.opt.defer_max, device=dev)
+        self.ng = G.Arena(self.n, G.K_NONGEO_DIM, self.opt.nongeo_groups(), self.opt.defer_max, device=dev,
+                          interleaved=True)
         self.geo.w.copy_(rows[:, : G.K_GEO_DIM])
         self.ng.w.copy_(rows[:, G.K_GEO_DIM:])
         del rows

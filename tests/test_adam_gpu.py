@@ -1,5 +1,6 @@
 """GPU parity of the optimizer kernels (adam.hpp:67-313) through the C ABI: given identical
-gradients, arena state after every pass is bit-identical to the reference."""
+gradients, arena state after every pass is bit-identical to the reference — for the reference's
+separate w/m/v arrays and for the row-interleaved layout (gss_arena.row_stride) the engine uses."""
 import numpy as np
 import pytest
 import torch
@@ -17,10 +18,10 @@ def bits(a):
     return np.ascontiguousarray(a, np.float32).view(np.uint32)
 
 
-def make_pair(n, dim, groups, defer_max, rng):
+def make_pair(n, dim, groups, defer_max, rng, interleaved=False):
     ra = O.RefArena(n, dim, groups, defer_max)
     ga = G.Arena(n, dim, [G.GroupSpec(f"g{i}", c0, d, G.Hyperparams(lr)) for i, (c0, d, lr) in enumerate(groups)],
-                 defer_max)
+                 defer_max, interleaved=interleaved)
     w0 = rng.uniform(-1, 1, (n, dim)).astype(np.float32)
     ra.w[:] = w0
     ga.w.copy_(torch.from_numpy(w0))
@@ -35,13 +36,14 @@ def assert_same(ra, ga):
     assert ra.step == ga.step
 
 
+@pytest.mark.parametrize("interleaved", [False, True])
 @pytest.mark.parametrize("defer_max", [0, 1, 7, 15, 40])
 @pytest.mark.parametrize("n,dim,groups", [(3000, 49, GROUPS49), (2100, 10, GROUPS10), (777, 59, None)])
-def test_deferred_schedule_bitwise(ref, defer_max, n, dim, groups):
+def test_deferred_schedule_bitwise(ref, defer_max, n, dim, groups, interleaved):
     rng = np.random.default_rng(defer_max * 1000 + n)
     if groups is None:
         groups = GROUPS10 + [(10 + c0, d, lr) for c0, d, lr in GROUPS49]
-    ra, ga = make_pair(n, dim, groups, defer_max, rng)
+    ra, ga = make_pair(n, dim, groups, defer_max, rng, interleaved)
     for step in range(30):
         dens = 0.0 if step % 11 == 5 else rng.uniform(0.02, 0.3)
         ids = np.nonzero(rng.uniform(size=n) < dens)[0].astype(np.int32)
@@ -65,11 +67,12 @@ def test_strided_grads_with_col0_bitwise(ref):
         assert_same(ra, ga)
 
 
-def test_dense_step_bitwise_and_fixed_point(ref):
+@pytest.mark.parametrize("interleaved", [False, True])
+def test_dense_step_bitwise_and_fixed_point(ref, interleaved):
     rng = np.random.default_rng(2)
     n, dim = 999, 59
     groups = GROUPS10 + [(10 + c0, d, lr) for c0, d, lr in GROUPS49]
-    ra, ga = make_pair(n, dim, groups, 0, rng)
+    ra, ga = make_pair(n, dim, groups, 0, rng, interleaved)
     for s in range(5):
         g = rng.normal(size=(n, dim)).astype(np.float32)
         ra.dense(g)
@@ -104,10 +107,11 @@ def test_max0_deferred_equals_dense_bitwise():
         assert torch.equal(dense.w, defer.w) and torch.equal(dense.m, defer.m) and torch.equal(dense.v, defer.v)
 
 
-def test_restore_view_with_and_without_pending_bitwise(ref):
+@pytest.mark.parametrize("interleaved", [False, True])
+def test_restore_view_with_and_without_pending_bitwise(ref, interleaved):
     rng = np.random.default_rng(29)
     n, dim = 2000, 49
-    ra, ga = make_pair(n, dim, GROUPS49, 6, rng)
+    ra, ga = make_pair(n, dim, GROUPS49, 6, rng, interleaved)
     for _ in range(9):
         ids = np.nonzero(rng.uniform(size=n) < 0.3)[0].astype(np.int32)
         rows = rng.normal(size=(ids.size, dim)).astype(np.float32)
@@ -130,10 +134,11 @@ def test_restore_view_with_and_without_pending_bitwise(ref):
     assert np.array_equal(bits(w[touched]), bits(fwd[touched]))
 
 
-def test_flush_equals_restore_and_reference(ref):
+@pytest.mark.parametrize("interleaved", [False, True])
+def test_flush_equals_restore_and_reference(ref, interleaved):
     rng = np.random.default_rng(41)
     n, dim = 500, 49
-    ra, ga = make_pair(n, dim, GROUPS49, 15, rng)
+    ra, ga = make_pair(n, dim, GROUPS49, 15, rng, interleaved)
     for _ in range(12):
         ids = np.nonzero(rng.uniform(size=n) < 0.3)[0].astype(np.int32)
         rows = rng.normal(size=(ids.size, dim)).astype(np.float32)
