@@ -648,10 +648,11 @@ bool vector_rows(const gss_arena& a) {
 constexpr int kRestoreChunk = kUpdThreads;
 constexpr int kSeg = 2048;
 template <int K>
-__global__ void __launch_bounds__(kUpdThreads, GSS_WALK_MINB) restore_kernel(ArenaDev a, const int32_t* ids, int64_t count,
+__global__ void __launch_bounds__(kUpdThreads, 3) restore_kernel(ArenaDev a, const int32_t* ids, int64_t count,
                                                               const int64_t* count_dev, GradsDev pend,
                                                               const int32_t* pbstart, int has_pending,
-                                                              const __grid_constant__ LutArgs<K> L, float* out) {
+                                                              const __grid_constant__ LutArgs<K> L, float* out,
+                                                              int vec) {
   __shared__ PackedLuts<K> lut;
   __shared__ int32_t cid[kRestoreChunk];
   __shared__ uint8_t cdel[kRestoreChunk];
@@ -715,6 +716,65 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_WALK_MINB) restore_kernel(Are
     const int32_t my_id = j < nk ? cid[j] : -1;
     const int32_t my_del = j < nk ? cdel[j] : 0;
     const int32_t my_slot = (j < nk && has_pending) ? cslot[j] : -1;
+    if (vec && warp * 32 < nk) {
+      // 16-byte units of 4 columns (see walk4_kernel): row-interleaved arenas
+      const int nq = (dim + 3) >> 2;
+      const int dq = 32 / nq, dr = 32 - dq * nq;
+      const int64_t my_base = j < nk ? (int64_t)my_id * a.stride : -1;
+      int r = lane / nq, q = lane - (lane / nq) * nq;
+      constexpr int kV = 2;
+      for (int i0 = 0; i0 < nq; i0 += kV) {
+        float4 w[kV], m[kV], v[kV];
+        float gv[kV][4];
+        int dd[kV], c0[kV], rr4[kV];
+        bool ok[kV];
+#pragma unroll
+        for (int u = 0; u < kV; ++u) {
+          const int rr = r < 32 ? r : 31;
+          const int64_t base = __shfl_sync(0xffffffffu, my_base, rr);
+          const int32_t sl = __shfl_sync(0xffffffffu, my_slot, rr);
+          dd[u] = __shfl_sync(0xffffffffu, my_del, rr);
+          c0[u] = 4 * q;
+          rr4[u] = rr;
+          ok[u] = i0 + u < nq && base >= 0;
+          const int64_t o = ok[u] ? base + c0[u] : 0;
+          w[u] = ok[u] ? ld4(a.w + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+          m[u] = ok[u] ? ld4(a.m + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[u] = ok[u] ? ld4(a.v + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float* prow = pend.rows + (int64_t)sl * pend.stride + pend.col0 + c0[u];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) gv[u][i] = (ok[u] && sl >= 0 && c0[u] + i < dim) ? prow[i] : 0.0f;
+          r += dq;
+          q += dr;
+          if (q >= nq) {
+            q -= nq;
+            ++r;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kV; ++u) {
+          if (!ok[u]) continue;
+          float* orow = out + (size_t)(k0 + warp * 32 + rr4[u]) * dim + c0[u];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (c0[u] + i >= dim) break;
+            const int g = lut.col_group[c0[u] + i];
+            const float4 gd = lut.gd[g][dd[u]];
+            float ww = at(w[u], i);
+            if (has_pending) {
+              float mm = at(m[u], i), vv = at(v[u], i);
+              deferred_scalar_fast(ww, mm, vv, gv[u][i], gd, lut.sc[g], lut.eps[g]);
+            } else {
+              const float num = gd.x * at(m[u], i);
+              ww = (num == 0.0f && at(v[u], i) >= 0.0f) ? ww - num
+                                                        : ww - div_rn(num, sqrt_rn(at(v[u], i)) + lut.eps[g]);
+            }
+            orow[i] = ww;
+          }
+        }
+      }
+      continue;
+    }
     const int dq = 32 / dim, dr = 32 - dq * dim;
     int r = lane / dim, c = lane - (lane / dim) * dim;
     constexpr int kU = GSS_WALK_KU;
@@ -1012,13 +1072,13 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
     std::memset(L.get(), 0, sizeof(LutArgs<16>));
     fill_luts<16>(a, t, false, *L);
     restore_kernel<16><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), ids, count, count_dev, pd, pbstart,
-                                                       pending ? 1 : 0, *L, out);
+                                                       pending ? 1 : 0, *L, out, vector_rows(a) ? 1 : 0);
   } else {
     auto L = std::make_unique<LutArgs<256>>();
     std::memset(L.get(), 0, sizeof(LutArgs<256>));
     fill_luts<256>(a, t, false, *L);
     restore_kernel<256><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), ids, count, count_dev, pd, pbstart,
-                                                        pending ? 1 : 0, *L, out);
+                                                        pending ? 1 : 0, *L, out, vector_rows(a) ? 1 : 0);
   }
   GSS_LAUNCHED();
   if (pbstart) GSS_CUDA(cudaFreeAsync(pbstart, st));
