@@ -461,7 +461,7 @@ def load_traffic():
     committed ncu --set full capture of this workload (profiles/); {} when absent."""
     f = ROOT / "profiles" / "ncu_traffic.json"
     try:
-        return {k: v["dram_bytes"] for k, v in json.loads(f.read_text()).items()}
+        return {k: v["dram_bytes"] for k, v in json.loads(f.read_text()).items() if not k.startswith("_")}
     except Exception:
         return {}
 
