@@ -204,7 +204,6 @@ __global__ void __launch_bounds__(kUpdThreads) update_kernel(ArenaDev a, GradsDe
                                                              const __grid_constant__ LutArgs<K> L,
                                                              uint32_t* touched_mask, int64_t* touched_count,
                                                              int* err_flag, TouchList tl) {
-  __shared__ SmemLuts<K> lut;
   __shared__ int32_t slot_of[kRowsPerBlock];
   __shared__ int warp_tot[kUpdThreads / 32];
   __shared__ int ntouched;
@@ -212,7 +211,6 @@ __global__ void __launch_bounds__(kUpdThreads) update_kernel(ArenaDev a, GradsDe
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
   const int nrows = (int)((a.n - r0) < kRowsPerBlock ? (a.n - r0) : kRowsPerBlock);
-  load_luts<K>(lut, L, a.dim);
   for (int i = tid; i < kRowsPerBlock; i += kUpdThreads) slot_of[i] = -1;
   __syncthreads();
   if (MODE == kDeferred && gr.ids) {
@@ -225,7 +223,6 @@ __global__ void __launch_bounds__(kUpdThreads) update_kernel(ArenaDev a, GradsDe
     }
   }
   __syncthreads();
-  const int dim = a.dim;
   // Counter pass: 4 consecutive rows per thread (one 32-bit load/store of counters).
   int my_cnt = 0;
   uint8_t del[4];
@@ -876,11 +873,26 @@ int sm_count() {
   return sms;
 }
 
-// Stream-ordered scratch for the block index of a sorted id list (nblocks + 1 entries).
-int32_t* build_index(const gss_arena& a, const GradsDev& g, int* err, cudaStream_t st) {
+// Per-arena scratch (keyed by the counter buffer, like the error flag), grown on demand from the
+// stream-ordered pool and kept: a pass allocates and frees nothing. Slot 0 serves the update passes
+// (block index + touch list), slot 1 the forwarding gather (pending block index); one writer per
+// arena at a time (the reference engine's DAG) keeps each slot single-stream.
+std::mutex g_scr_mu;
+std::unordered_map<const void*, std::pair<void*, size_t>> g_scr[2];
+char* arena_scratch(const gss_arena& a, int slot, size_t bytes, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_scr_mu);
+  auto& e = g_scr[slot][a.counter];
+  if (e.second < bytes) {
+    if (e.first) GSS_CUDA(cudaFreeAsync(e.first, st));
+    GSS_CUDA(cudaMallocAsync(&e.first, bytes, st));
+    e.second = bytes;
+  }
+  return static_cast<char*>(e.first);
+}
+
+// Block index of a sorted id list (nblocks + 1 entries) into `bstart`.
+int32_t* build_index(const gss_arena& a, const GradsDev& g, int* err, int32_t* bstart, cudaStream_t st) {
   const int nblk = (int)ceil_div(a.n, kRowsPerBlock);
-  int32_t* bstart = nullptr;
-  GSS_CUDA(cudaMallocAsync((void**)&bstart, (size_t)(nblk + 1) * 4, st));
   const int64_t cap = g.count_dev ? std::max<int64_t>(g.count, a.n) : g.count;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap + 1, 256), 148 * 16));
   index_kernel<<<blocks, 256, 0, st>>>(g.ids, g.count, g.count_dev, a.n, nblk, bstart, err);
@@ -895,18 +907,19 @@ void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* 
   std::memset(L.get(), 0, sizeof(LutArgs<K>));
   fill_luts<K>(a, t, MODE == kFlush, *L);
   int* err = err_flag_for(a);
-  int32_t* bstart = nullptr;
-  if (MODE == kDeferred && gd.ids) bstart = build_index(a, gd, err, st);
   const int blocks = (int)ceil_div(a.n, kRowsPerBlock);
+  const size_t n = (size_t)a.n;
+  const size_t idx_bytes = ((size_t)(blocks + 1) * 4 + 255) / 256 * 256;
+  char* scr = arena_scratch(a, 0, idx_bytes + 16 + n * 9, st);
+  int32_t* bstart = nullptr;
+  if (MODE == kDeferred && gd.ids) bstart = build_index(a, gd, err, reinterpret_cast<int32_t*>(scr), st);
   if (MODE == kDeferred && a.defer_max == 0 && (a.row_stride == 0 || a.row_stride == a.dim)) {
     dense_update_kernel<K><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, bstart, *L, tcount, tmask);
     GSS_LAUNCHED();
   } else {
     // Pass 1: counters + touch list; pass 2: stream the list.
     TouchList tl;
-    const size_t n = (size_t)a.n;
-    char* buf = nullptr;
-    GSS_CUDA(cudaMallocAsync((void**)&buf, 16 + n * 9, st));
+    char* buf = scr + idx_bytes;
     tl.count = reinterpret_cast<unsigned long long*>(buf);
     tl.row = reinterpret_cast<int32_t*>(buf + 16);
     tl.slot = tl.row + n;
@@ -922,9 +935,7 @@ void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* 
     else
       walk_kernel<K, MODE><<<wblocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, *L, tl);
     GSS_LAUNCHED();
-    GSS_CUDA(cudaFreeAsync(buf, st));
   }
-  if (bstart) GSS_CUDA(cudaFreeAsync(bstart, st));
 }
 
 struct IsSet {
@@ -1066,7 +1077,10 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
   const int64_t cap = count_dev ? std::max<int64_t>(count, a.n) : count;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kRestoreChunk), (int64_t)sms * 4));
   int32_t* pbstart = nullptr;
-  if (pending && pd.ids) pbstart = build_index(a, pd, err_flag_for(a), st);
+  if (pending && pd.ids)
+    pbstart = build_index(a, pd, err_flag_for(a),
+                          reinterpret_cast<int32_t*>(arena_scratch(a, 1, (size_t)(ceil_div(a.n, kRowsPerBlock) + 1) * 4, st)),
+                          st);
   if (a.defer_max < 16) {
     auto L = std::make_unique<LutArgs<16>>();
     std::memset(L.get(), 0, sizeof(LutArgs<16>));
@@ -1081,7 +1095,6 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
                                                         pending ? 1 : 0, *L, out, vector_rows(a) ? 1 : 0);
   }
   GSS_LAUNCHED();
-  if (pbstart) GSS_CUDA(cudaFreeAsync(pbstart, st));
 }
 
 int arena_check(const gss_arena* ap, cudaStream_t st) {

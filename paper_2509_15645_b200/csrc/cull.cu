@@ -33,7 +33,10 @@ namespace gssd {
 namespace {
 
 constexpr int kTile = 512;
-constexpr int kThreads = 256;
+#ifndef CULL_THREADS
+#define CULL_THREADS 256
+#endif
+constexpr int kThreads = CULL_THREADS;
 #ifndef CULL_STAGES
 #define CULL_STAGES 3
 #endif
