@@ -890,6 +890,19 @@ char* arena_scratch(const gss_arena& a, int slot, size_t bytes, cudaStream_t st)
   return static_cast<char*>(e.first);
 }
 
+// Is the arena's w in host memory (the pinned host tier of selective offloading)? Kernels that
+// walk such an arena are bound by the host link, not by SM count: they get a small grid (enough
+// requests in flight to fill the link) so the render on the other stream keeps the SMs.
+bool host_resident(const gss_arena& a) {
+  cudaPointerAttributes at{};
+  if (!a.w || cudaPointerGetAttributes(&at, a.w) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+constexpr int kHostTierBlocks = 64;
+
 // Block index of a sorted id list (nblocks + 1 entries) into `bstart`.
 int32_t* build_index(const gss_arena& a, const GradsDev& g, int* err, int32_t* bstart, cudaStream_t st) {
   const int nblk = (int)ceil_div(a.n, kRowsPerBlock);
@@ -928,8 +941,8 @@ void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* 
     update_kernel<K, MODE><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, bstart, *L, tmask, tcount, err,
                                                                    tl);
     GSS_LAUNCHED();
-    const int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, kUpdThreads),
-                                                                    (int64_t)sm_count() * 8));
+    int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, kUpdThreads), (int64_t)sm_count() * 8));
+    if (host_resident(a)) wblocks = std::min(wblocks, 4 * kHostTierBlocks);  // reads + writes in flight
     if (vector_rows(a))
       walk4_kernel<K, MODE><<<wblocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, *L, tl);
     else
@@ -1075,7 +1088,8 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
   GSS_CUDA(cudaGetDevice(&dev));
   GSS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int64_t cap = count_dev ? std::max<int64_t>(count, a.n) : count;
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kRestoreChunk), (int64_t)sms * 4));
+  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kRestoreChunk), (int64_t)sms * 4));
+  if (host_resident(a)) blocks = std::min(blocks, kHostTierBlocks);
   int32_t* pbstart = nullptr;
   if (pending && pd.ids)
     pbstart = build_index(a, pd, err_flag_for(a),

@@ -34,6 +34,10 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
 void rasterize_forward(gss_render_ctx* ctx, const gss_render_scene* scene, const gss_camera* cam,
                        const gss_viewport* vp, float* image, const float* gt, int64_t normalizer, float* d_img,
                        float* loss_dev, float* final_T_opt, int32_t* ncontrib_opt, int64_t* meta, cudaStream_t st);
+void rasterize_forward_geometry(gss_render_ctx* ctx, const gss_render_scene* scene, const gss_camera* cam,
+                                const gss_viewport* vp, cudaStream_t st);
+void rasterize_forward_finish(gss_render_ctx* ctx, float* image, const float* gt, int64_t normalizer, float* d_img,
+                              float* loss_dev, cudaStream_t st);
 void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int64_t gstride, float* gn,
                         int64_t nstride, float* mean2d, cudaStream_t st);
 void render_ctx_destroy(gss_render_ctx* ctx);
@@ -270,11 +274,6 @@ void stage_forward_params(gss_engine* e, int g) {
 void stage_render(gss_engine* e, int g, const gss_camera& cam, const float* gt_dev, float* loss_out) {
   const int p = g % 3, b = g % 2;
   cudaStream_t s = e->sD;
-  if (e->cfg.pipelined) {
-    GSS_CUDA(cudaStreamWaitEvent(s, e->ev_fp[b].e, 0));
-    // grads[b] is free once lazy(g-2) consumed it
-    GSS_CUDA(cudaStreamWaitEvent(s, e->ev_lazy[b].e, 0));
-  }
   require(e->fwd_iter[b] == g, "render: forwarded buffer is not for this iteration", GSS_ERR_INVARIANT);
   stage_begin(e, kRender, s, b);
   const int64_t V = e->count_host[p];
@@ -293,8 +292,15 @@ void stage_render(gss_engine* e, int g, const gss_camera& cam, const float* gt_d
   sc.low_pass = e->cfg.low_pass;
   const gss_viewport vp{0.0f, (float)cam.width, 0.0f, (float)cam.height};
   const int64_t full = (int64_t)cam.width * cam.height * 3;
-  rasterize_forward(e->rctx, &sc, &cam, &vp, e->image, gt_dev, full, e->d_img, loss_out,
-                    nullptr, nullptr, nullptr, s);
+  // Geometry half first: it reads only the geometric tier, so in pipelined mode it overlaps the
+  // forwarding gather of this iteration on stream H; colour + composite wait for fp(g).
+  rasterize_forward_geometry(e->rctx, &sc, &cam, &vp, s);
+  if (e->cfg.pipelined) {
+    GSS_CUDA(cudaStreamWaitEvent(s, e->ev_fp[b].e, 0));
+    // grads[b] is free once lazy(g-2) consumed it
+    GSS_CUDA(cudaStreamWaitEvent(s, e->ev_lazy[b].e, 0));
+  }
+  rasterize_forward_finish(e->rctx, e->image, gt_dev, full, e->d_img, loss_out, s);
   rasterize_backward(e->rctx, e->d_img, e->g_geo[b], kGeoDim, e->g_ng[b], kNgDim, e->g_m2d[b], s);
   e->g_plan[b] = p;
   stage_end(e, kRender, s, b);

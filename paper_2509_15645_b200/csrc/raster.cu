@@ -104,6 +104,38 @@ __device__ __forceinline__ const float* ng_row(const SceneDev& s, int k, int id)
 }
 
 // project_all (render.hpp:361-380) + CSR box (render.hpp:297-314, 418-419) + tile count.
+// Opacity and view-dependent colour of slot k (render.hpp:372-378, sh.hpp:77-86).
+__device__ __forceinline__ void splat_colour(const SceneDev& s, const Cam& cam, int k, int id, const float* g,
+                                             SplatRec& r) {
+  const float* ng = ng_row(s, k, id);
+  r.ab = 1.0f / (1.0f + gss_expf(-ng[0]));
+  const f3 cp = cam_position(cam);
+  f3 dir{g[0] - cp.x, g[1] - cp.y, g[2] - cp.z};
+  const float dn = sqrtf(dir.x * dir.x + dir.y * dir.y + dir.z * dir.z);
+  if (dn > 1e-12f) {
+    const float inv = 1.0f / dn;
+    dir = f3{dir.x * inv, dir.y * inv, dir.z * inv};
+  } else {
+    dir = f3{0.0f, 0.0f, 1.0f};
+  }
+  float basis[16];
+  sh_basis(dir.x, dir.y, dir.z, s.sh_degree, basis);
+  const int nb = (s.sh_degree + 1) * (s.sh_degree + 1);
+  float rgb0 = 0.5f, rgb1 = 0.5f, rgb2 = 0.5f;
+  for (int b = 0; b < nb; ++b) {
+    rgb0 += basis[b] * ng[1 + 3 * b];
+    rgb1 += basis[b] * ng[2 + 3 * b];
+    rgb2 += basis[b] * ng[3 + 3 * b];
+  }
+  r.r = clamp01(rgb0);
+  r.g = clamp01(rgb1);
+  r.bl = clamp01(rgb2);
+}
+
+// project_all (render.hpp:361-380) + CSR box (render.hpp:297-314, 418-419) + tile count. With
+// COLOUR = false only the geometry is produced (opacity/colour zero) — colour_kernel fills it in
+// once the non-geometric rows are available, so binning can run while they are gathered.
+template <bool COLOUR>
 __global__ void preprocess_kernel(SceneDev s, Cam cam, Win w, int64_t V, SplatRec* recs, int32_t* ntiles,
                                   uint32_t* dkey, int32_t* dslot) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -116,28 +148,8 @@ __global__ void preprocess_kernel(SceneDev s, Cam cam, Win w, int64_t V, SplatRe
   memset(&r, 0, sizeof(r));
   int nt = 0;
   if (project_geo(cam, g, s.lp, p, t)) {
-    const float* ng = ng_row(s, (int)k, id);
-    const float ab = 1.0f / (1.0f + gss_expf(-ng[0]));
-    const f3 cp = cam_position(cam);
-    f3 dir{g[0] - cp.x, g[1] - cp.y, g[2] - cp.z};
-    const float dn = sqrtf(dir.x * dir.x + dir.y * dir.y + dir.z * dir.z);
-    if (dn > 1e-12f) {
-      const float inv = 1.0f / dn;
-      dir = f3{dir.x * inv, dir.y * inv, dir.z * inv};
-    } else {
-      dir = f3{0.0f, 0.0f, 1.0f};
-    }
-    float basis[16];
-    sh_basis(dir.x, dir.y, dir.z, s.sh_degree, basis);
-    const int nb = (s.sh_degree + 1) * (s.sh_degree + 1);
-    float rgb0 = 0.5f, rgb1 = 0.5f, rgb2 = 0.5f;
-    for (int b = 0; b < nb; ++b) {
-      rgb0 += basis[b] * ng[1 + 3 * b];
-      rgb1 += basis[b] * ng[2 + 3 * b];
-      rgb2 += basis[b] * ng[3 + 3 * b];
-    }
-    r.mx = p.mx; r.my = p.my; r.a = p.a; r.b = p.b; r.c = p.c; r.ab = ab;
-    r.r = clamp01(rgb0); r.g = clamp01(rgb1); r.bl = clamp01(rgb2);
+    if (COLOUR) splat_colour(s, cam, (int)k, id, g, r);
+    r.mx = p.mx; r.my = p.my; r.a = p.a; r.b = p.b; r.c = p.c;
     r.depth = t.z;
     r.det = p.a * p.c - p.b * p.b;
     if (r.det > 0.0f) {
@@ -163,6 +175,20 @@ __global__ void preprocess_kernel(SceneDev s, Cam cam, Win w, int64_t V, SplatRe
   // Depth sort key: binned splats have depth >= near > 0, whose IEEE bits order like the values.
   dkey[k] = nt > 0 ? __float_as_uint(r.depth) : 0xffffffffu;
   dslot[k] = (int32_t)k;
+}
+
+// The colour half of preprocess for the binned splats (ntiles > 0: the only records compositing
+// and the sweep read; a valid unbinned slot's opacity only meets zero gradient sums in the chain).
+__global__ void colour_kernel(SceneDev s, Cam cam, int64_t V, const int32_t* ntiles, SplatRec* recs) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= V || ntiles[k] == 0) return;
+  const int id = s.ids[k];
+  SplatRec r;
+  splat_colour(s, cam, (int)k, id, s.geo + (int64_t)id * s.geo_stride, r);
+  recs[k].ab = r.ab;
+  recs[k].r = r.r;
+  recs[k].g = r.g;
+  recs[k].bl = r.bl;
 }
 
 // Records projected against a larger window (another GPU's projection of the whole view),
@@ -966,22 +992,12 @@ struct FwdOut {
 // Everything after the records exist: common to rasterize_forward (records from preprocess) and
 // the image-parallel strip forward (records received from other GPUs, re-clipped). Expects
 // ctx->recs / ntiles / dkeys_a / order_a filled for V records, boxes clipped to w.
-void bin_and_composite(gss_render_ctx* ctx, const Win& w, int64_t V, const FwdOut& o, cudaStream_t st) {
-  const SceneDev& s = ctx->sc;
+// bin_phase: depth sort, instance offsets, tile keys, tile sort, tile ranges (ctx->I set; the
+// sorted instance values end in ctx->vals_a, the ranges in ctx->ranges).
+void bin_phase(gss_render_ctx* ctx, const Win& w, int64_t V, cudaStream_t st) {
   const int64_t npix = (int64_t)w.pw * w.ph;
-  float* fT = static_cast<float*>(ctx->fT.get((size_t)std::max<int64_t>(npix, 1) * 4, st));
-  int32_t* last = static_cast<int32_t*>(ctx->last.get((size_t)std::max<int64_t>(npix, 1) * 4, st));
-  auto write_meta = [&](int64_t I) {
-    if (o.meta) {
-      o.meta[0] = w.px0; o.meta[1] = w.py0; o.meta[2] = w.pw; o.meta[3] = w.ph; o.meta[4] = V; o.meta[5] = I;
-    }
-  };
-  if (npix == 0) {
-    if (o.gt) GSS_CUDA(cudaMemsetAsync(o.loss_dev, 0, sizeof(float), st));
-    if (o.gt && o.loss_sum) GSS_CUDA(cudaMemsetAsync(o.loss_sum, 0, sizeof(double), st));
-    write_meta(0);
-    return;
-  }
+  ctx->I = 0;
+  if (npix == 0) return;
   SplatRec* recs = static_cast<SplatRec*>(ctx->recs.p);
   int32_t* nt = static_cast<int32_t*>(ctx->ntiles.p);
   int32_t* offs = static_cast<int32_t*>(ctx->offsets.get((size_t)(V + 1) * 4, st));
@@ -990,7 +1006,7 @@ void bin_and_composite(gss_render_ctx* ctx, const Win& w, int64_t V, const FwdOu
   const int ntile = w.tw * w.th;
   int2* ranges = static_cast<int2*>(ctx->ranges.get((size_t)ntile * sizeof(int2), st));
   GSS_CUDA(cudaMemsetAsync(ranges, 0, (size_t)ntile * sizeof(int2), st));
-  int32_t* vals_sorted = static_cast<int32_t*>(ctx->vals_a.get(16, st));
+  ctx->vals_a.get(16, st);
   if (V > 0) {
     auto* dka = static_cast<uint32_t*>(ctx->dkeys_a.p);
     auto* dkb = static_cast<uint32_t*>(ctx->dkeys_b.get((size_t)V * 4, st));
@@ -1025,7 +1041,6 @@ void bin_and_composite(gss_render_ctx* ctx, const Win& w, int64_t V, const FwdOu
     auto* vb = static_cast<int32_t*>(ctx->vals_b.get((size_t)std::max<int64_t>(I, 1) * 4, st));
     duplicate_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(recs, order, nt, offs, w, V, ka, va, recs, soff);
     GSS_LAUNCHED();
-    vals_sorted = va;
     if (I > 0) {
       // 3. stable sort of the instances by tile (only the tile bits).
       int tile_bits = 1;
@@ -1037,25 +1052,48 @@ void bin_and_composite(gss_render_ctx* ctx, const Win& w, int64_t V, const FwdOu
       void* stmp = ctx->cub_tmp.get(std::max(sb, std::max(db, tb)), st);
       GSS_CUDA(cub::DeviceRadixSort::SortPairs(stmp, sb, dk, dv, (int)I, 0, tile_bits, st));
       count_launch();
-      vals_sorted = dv.Current();
-      // keep the sorted arrays addressable for backward
+      // keep the sorted arrays addressable (vals_a) for composite and backward
       if (dk.Current() != ka) std::swap(ctx->keys_a, ctx->keys_b);
       if (dv.Current() != va) std::swap(ctx->vals_a, ctx->vals_b);
-      ranges_kernel<<<(unsigned)ceil_div(I, 256), 256, 0, st>>>(dk.Current(), I, ranges);
+      ranges_kernel<<<(unsigned)ceil_div(I, 256), 256, 0, st>>>(static_cast<const uint32_t*>(ctx->keys_a.p), I,
+                                                                ranges);
       GSS_LAUNCHED();
     }
   }
   ctx->I = I;
+}
+
+// composite_phase: per-pixel compositing fused with the L1 loss (forward_kernel).
+void composite_phase(gss_render_ctx* ctx, const Win& w, int64_t V, const FwdOut& o, cudaStream_t st) {
+  const SceneDev& s = ctx->sc;
+  const int64_t npix = (int64_t)w.pw * w.ph;
+  float* fT = static_cast<float*>(ctx->fT.get((size_t)std::max<int64_t>(npix, 1) * 4, st));
+  int32_t* last = static_cast<int32_t*>(ctx->last.get((size_t)std::max<int64_t>(npix, 1) * 4, st));
+  if (o.meta) {
+    o.meta[0] = w.px0; o.meta[1] = w.py0; o.meta[2] = w.pw; o.meta[3] = w.ph; o.meta[4] = V; o.meta[5] = ctx->I;
+  }
+  if (npix == 0) {
+    if (o.gt) GSS_CUDA(cudaMemsetAsync(o.loss_dev, 0, sizeof(float), st));
+    if (o.gt && o.loss_sum) GSS_CUDA(cudaMemsetAsync(o.loss_sum, 0, sizeof(double), st));
+    return;
+  }
+  const int ntile = w.tw * w.th;
   double* lp = o.gt ? static_cast<double*>(ctx->lossp.get((size_t)ntile * 8, st)) : nullptr;
-  forward_kernel<<<ntile, kTilePix, 0, st>>>(recs, vals_sorted, ranges, w, s.bg[0], s.bg[1], s.bg[2], o.image, fT,
-                                             last, o.ncontrib, o.gt, o.gt_width, o.inv, o.d_img, lp);
+  forward_kernel<<<ntile, kTilePix, 0, st>>>(static_cast<const SplatRec*>(ctx->recs.p),
+                                             static_cast<const int32_t*>(ctx->vals_a.p),
+                                             static_cast<const int2*>(ctx->ranges.p), w, s.bg[0], s.bg[1], s.bg[2],
+                                             o.image, fT, last, o.ncontrib, o.gt, o.gt_width, o.inv, o.d_img, lp);
   GSS_LAUNCHED();
   if (o.gt) {
     loss_final_kernel<<<1, 1024, 0, st>>>(lp, ntile, o.inv, o.loss_dev, o.loss_sum);
     GSS_LAUNCHED();
   }
   if (o.final_T) GSS_CUDA(cudaMemcpyAsync(o.final_T, fT, npix * 4, cudaMemcpyDeviceToDevice, st));
-  write_meta(I);
+}
+
+void bin_and_composite(gss_render_ctx* ctx, const Win& w, int64_t V, const FwdOut& o, cudaStream_t st) {
+  bin_phase(ctx, w, V, st);
+  composite_phase(ctx, w, V, o, st);
 }
 
 void begin_forward(gss_render_ctx* ctx, const gss_camera* cam, const Win& w, int64_t V, cudaStream_t st) {
@@ -1131,7 +1169,7 @@ void rasterize_forward(gss_render_ctx* ctx, const gss_render_scene* scene, const
   const float inv = gt ? 1.0f / (float)(double)(normalizer > 0 ? normalizer : npix * 3) : 0.0f;
   alloc_records(ctx, V, st);
   if (V > 0 && npix > 0) {
-    preprocess_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(
+    preprocess_kernel<true><<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(
         ctx->sc, ctx->cam, w, V, static_cast<SplatRec*>(ctx->recs.p), static_cast<int32_t*>(ctx->ntiles.p),
         static_cast<uint32_t*>(ctx->dkeys_a.p), static_cast<int32_t*>(ctx->order_a.p));
     GSS_LAUNCHED();
@@ -1172,6 +1210,47 @@ void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int6
                nstride, mean2d, st);
 }
 
+// Two-phase forward for the engine: the geometry half (projection, depth/tile sort, tile ranges)
+// needs only the geometric tier, so it runs while the forwarding gather of the non-geometric rows
+// is still in flight on the other stream; finish() adds opacity/colour and composites.
+void rasterize_forward_geometry(gss_render_ctx* ctx, const gss_render_scene* scene, const gss_camera* cam,
+                                const gss_viewport* vp, cudaStream_t st) {
+  require(ctx && scene && cam && vp, "rasterize_forward: null argument");
+  set_scene(ctx, scene);
+  if (!ctx->pinned) GSS_CUDA(cudaMallocHost(&ctx->pinned, 4 * sizeof(int64_t)));
+  const Win w = make_window(*vp);
+  const int64_t V = scene_count(ctx, scene, st);
+  begin_forward(ctx, cam, w, V, st);
+  alloc_records(ctx, V, st);
+  if (V > 0 && (int64_t)w.pw * w.ph > 0) {
+    preprocess_kernel<false><<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(
+        ctx->sc, ctx->cam, w, V, static_cast<SplatRec*>(ctx->recs.p), static_cast<int32_t*>(ctx->ntiles.p),
+        static_cast<uint32_t*>(ctx->dkeys_a.p), static_cast<int32_t*>(ctx->order_a.p));
+    GSS_LAUNCHED();
+  }
+  bin_phase(ctx, w, V, st);
+}
+
+void rasterize_forward_finish(gss_render_ctx* ctx, float* image, const float* gt, int64_t normalizer, float* d_img,
+                              float* loss_dev, cudaStream_t st) {
+  require(ctx && ctx->have_forward && image, "rasterize_forward: no geometry phase / null image");
+  require(!gt || (d_img && loss_dev), "rasterize_forward: gt needs d_img and loss_dev");
+  const Win& w = ctx->win;
+  const int64_t V = ctx->V;
+  const int64_t npix = (int64_t)w.pw * w.ph;
+  require(!gt || (w.px0 + w.pw <= ctx->cam.width && w.py0 + w.ph <= ctx->cam.height),
+          "compute_loss_l1: image and ground-truth shapes differ");
+  const float inv = gt ? 1.0f / (float)(double)(normalizer > 0 ? normalizer : npix * 3) : 0.0f;
+  if (V > 0 && npix > 0) {
+    colour_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(ctx->sc, ctx->cam, V,
+                                                              static_cast<const int32_t*>(ctx->ntiles.p),
+                                                              static_cast<SplatRec*>(ctx->recs.p));
+    GSS_LAUNCHED();
+  }
+  composite_phase(ctx, w, V, FwdOut{image, gt, ctx->cam.width, inv, d_img, loss_dev, nullptr, nullptr, nullptr,
+                                    nullptr}, st);
+}
+
 // ---- split-phase rasterizer for image-parallel rendering ----------------------
 
 void project(const gss_render_scene* scene, const gss_camera* cam, const gss_viewport* vp, void* records,
@@ -1185,7 +1264,7 @@ void project(const gss_render_scene* scene, const gss_camera* cam, const gss_vie
   if (V == 0) return;
   Cam c;
   std::memcpy(&c, cam, sizeof(Cam));
-  preprocess_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(tmp.sc, c, make_window(*vp), V,
+  preprocess_kernel<true><<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(tmp.sc, c, make_window(*vp), V,
                                                                 static_cast<SplatRec*>(records), nullptr, nullptr,
                                                                 nullptr);
   GSS_LAUNCHED();
