@@ -141,6 +141,18 @@ __device__ __forceinline__ int classify(const CullArgs& a, const float* g) {
   return (dok && a.all_exact) ? 2 : code;
 }
 
+#ifdef CULL_TRACE
+__device__ unsigned long long g_cull_trace[4096][6];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(i) do { if (threadIdx.x == 0 && blockIdx.x < 4096) g_cull_trace[blockIdx.x][i] = gtime(); } while (0)
+#else
+#define TRACE(i) do {} while (0)
+#endif
+
 __device__ __forceinline__ unsigned long long pack_state(unsigned long long flag, unsigned epoch,
                                                          unsigned long long v) {
   return (flag << 62) | ((unsigned long long)(epoch & 0x3fffffffu) << 32) | (v & 0xffffffffull);
@@ -162,6 +174,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) cull_kernel(const __grid
   __shared__ long long base_s;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  TRACE(0);
   if (tid == 0) {
     qn = 0;
     for (int i = 0; i < kStages; ++i) consumed[i] = 0;
@@ -257,11 +270,16 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) cull_kernel(const __grid
     }
   }
   __syncthreads();
+  TRACE(1);
   // Resolve the deferred rows with the exact reference predicate, all threads in parallel.
   const int nq = min(qn, kDefer);
   for (int q = tid; q < nq; q += kThreads)
     if (keep_exact(a, qrow[q])) atomicOr(&words[qidx[q] >> 5], 1u << (qidx[q] & 31));
   __syncthreads();
+  TRACE(2);
+#ifdef CULL_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 4096) g_cull_trace[blockIdx.x][5] = (unsigned long long)qn;
+#endif
   // Exclusive prefix of kept counts over this CTA's tiles (ascending row order).
   int tc = 0;
   if (tid < ntl) {
@@ -309,6 +327,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) cull_kernel(const __grid
   }
   __syncthreads();
   const long long base = base_s;
+  TRACE(3);
   // Scatter ascending ids (+ optional mask words): warp per tile, lane l < 16 owns word l.
   for (int jt = warp; jt < ntl; jt += kThreads / 32) {
     const uint32_t wv = lane < kWordsPerTile ? words[jt * kWordsPerTile + lane] : 0u;
@@ -332,6 +351,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) cull_kernel(const __grid
       }
     }
   }
+  TRACE(4);
 }
 
 __global__ void expf_kernel(const float* x, float* y, int64_t n) {

@@ -7,6 +7,7 @@ void set_error(const std::string&) {}
 void count_launch() {}
 int64_t launches() { return 0; }
 }
+#include <algorithm>
 #include <cstdio>
 #include <vector>
 int main(int argc, char** argv) {
@@ -29,5 +30,20 @@ int main(int argc, char** argv) {
   float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= reps;
   int64_t v; cudaMemcpy(&v, cnt, 8, cudaMemcpyDeviceToHost);
   printf("%s: %.2f us  visible %lld  %.0f GB/s\n", argv[2], ms * 1e3, (long long)v, (40.0 * n + 4.0 * v) / ms / 1e6);
+#ifdef CULL_TRACE
+  static unsigned long long tr[4096][6];
+  cudaMemcpyFromSymbol(tr, gssd::g_cull_trace, sizeof(tr));
+  int ctas = 0;
+  while (ctas < 4096 && tr[ctas][0] != 0) ++ctas;
+  unsigned long long t0 = ~0ull, qmax = 0, qsum = 0;
+  for (int c = 0; c < ctas; ++c) { t0 = std::min(t0, tr[c][0]); qmax = std::max(qmax, tr[c][5]); qsum += tr[c][5]; }
+  printf("ctas %d  queued rows: total %llu max per CTA %llu\n", ctas, qsum, qmax);
+  for (int ph = 0; ph < 5; ++ph) {
+    unsigned long long mn = ~0ull, mx = 0;
+    double avg = 0;
+    for (int c = 0; c < ctas; ++c) { mn = std::min(mn, tr[c][ph] - t0); mx = std::max(mx, tr[c][ph] - t0); avg += tr[c][ph] - t0; }
+    printf("phase %d: min %.2f us  avg %.2f us  max %.2f us\n", ph, mn / 1e3, avg / ctas / 1e3, mx / 1e3);
+  }
+#endif
   return 0;
 }
