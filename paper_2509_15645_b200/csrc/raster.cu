@@ -739,6 +739,7 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(SceneDev s, Cam ca
                                                               float* gg, int64_t gstride,
                                                               float* gn, int64_t nstride, float* mean2d) {
   __shared__ float row_s[kChainThreads / 32][32][kChainRow];
+  __shared__ float geo_s[kChainThreads / 32][32][11];  // the 10 geometric gradients, odd pitch
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t k0 = (int64_t)blockIdx.x * kChainThreads + warp * 32;
   if (k0 >= V) return;
@@ -756,9 +757,13 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(SceneDev s, Cam ca
   }
   __syncwarp();
   const int64_t k = k0 + lane;
-  float out[59];
+  // Geometric gradients (row columns 0..9) live in registers; the 49 non-geometric ones overwrite
+  // this lane's staged non-geometric row in place (column 10 + i -> slot i, each slot read before
+  // it is written), which keeps the kernel's register footprint small enough for occupancy.
+  float out[10];
 #pragma unroll
-  for (int i = 0; i < 59; ++i) out[i] = 0.0f;
+  for (int i = 0; i < 10; ++i) out[i] = 0.0f;
+  float* orow = rows[lane];
   float sa[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) sa[i] = lane < nk ? sums[(k0 + lane) * 9 + i] : 0.0f;
@@ -771,7 +776,7 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(SceneDev s, Cam ca
     const SplatRec r = recs[k];
     const float* ng = rows[lane];
     const float ab = r.ab;
-    out[10] += sa[8] * ab * (1.0f - ab);
+    const float d_opacity = 0.0f + sa[8] * ab * (1.0f - ab);
     const f3 cp = cam_position(cam);
     const f3 dir{g[0] - cp.x, g[1] - cp.y, g[2] - cp.z};
     const float dn = sqrtf(dir.x * dir.x + dir.y * dir.y + dir.z * dir.z);
@@ -798,8 +803,8 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(SceneDev s, Cam ca
         float coef_dot = 0.0f;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          out[11 + 3 * b + c] += basis[b] * gc[c];
           coef_dot += ng[1 + 3 * b + c] * gc[c];
+          orow[1 + 3 * b + c] = 0.0f + basis[b] * gc[c];
         }
         ddir.x += bgr[b].x * coef_dot;
         ddir.y += bgr[b].y * coef_dot;
@@ -808,7 +813,13 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(SceneDev s, Cam ca
       const float dotp = u.x * ddir.x + u.y * ddir.y + u.z * ddir.z;
       const float inv2 = 1.0f / dn;
       dmd = f3{(ddir.x - u.x * dotp) * inv2, (ddir.y - u.y * dotp) * inv2, (ddir.z - u.z * dotp) * inv2};
+#pragma unroll
+      for (int i = 1 + 3 * nb; i < 49; ++i) orow[i] = 0.0f;  // bands above DEG
+    } else {
+#pragma unroll
+      for (int i = 1; i < 49; ++i) orow[i] = 0.0f;
     }
+    orow[0] = d_opacity;
     out[0] += dmd.x;
     out[1] += dmd.y;
     out[2] += dmd.z;
@@ -911,10 +922,14 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(SceneDev s, Cam ca
     out[1] += W[1] * dt.x + W[4] * dt.y + W[7] * dt.z;
     out[2] += W[2] * dt.x + W[5] * dt.y + W[8] * dt.z;
   }
+  if (lane < nk && !valid) {
+#pragma unroll
+    for (int i = 0; i < 49; ++i) orow[i] = 0.0f;
+  }
   __syncwarp();
   if (lane < nk) {
 #pragma unroll
-    for (int i = 0; i < 59; ++i) rows[lane][i] = out[i];
+    for (int i = 0; i < 10; ++i) geo_s[warp][lane][i] = out[i];
     if (mean2d) {
       mean2d[k * 2] = sa[3];
       mean2d[k * 2 + 1] = sa[4];
@@ -923,11 +938,11 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(SceneDev s, Cam ca
   __syncwarp();
   for (int e = lane; e < nk * 10; e += 32) {
     const int kk = e / 10, c = e - kk * 10;
-    gg[(k0 + kk) * gstride + c] = rows[kk][c];
+    gg[(k0 + kk) * gstride + c] = geo_s[warp][kk][c];
   }
   for (int e = lane; e < nk * 49; e += 32) {
     const int kk = e / 49, c = e - kk * 49;
-    gn[(k0 + kk) * nstride + c] = rows[kk][10 + c];
+    gn[(k0 + kk) * nstride + c] = rows[kk][c];
   }
 }
 
