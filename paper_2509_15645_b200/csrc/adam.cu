@@ -537,6 +537,9 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_WALK_MINB) walk_kernel(ArenaD
 #ifndef GSS_WALK4_KU
 #define GSS_WALK4_KU 2
 #endif
+#ifndef GSS_WALK4_MINB
+#define GSS_WALK4_MINB 3
+#endif
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
 __device__ __forceinline__ float& at(float4& v, int i) {
@@ -544,7 +547,7 @@ __device__ __forceinline__ float& at(float4& v, int i) {
 }
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(kUpdThreads, 3) walk4_kernel(ArenaDev a, GradsDev gr,
+__global__ void __launch_bounds__(kUpdThreads, GSS_WALK4_MINB) walk4_kernel(ArenaDev a, GradsDev gr,
                                                                          const __grid_constant__ LutArgs<K> L,
                                                                          TouchList tl) {
   __shared__ PackedLuts<K> lut;
