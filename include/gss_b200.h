@@ -263,6 +263,28 @@ int gss_engine_stage_ms(gss_engine* e, double* out6);
 /* Kernel launches issued by the last run/step (for bench accounting). */
 int64_t gss_engine_launches(gss_engine* e);
 
+/* ---- densification (trainer.hpp:166-213, engine.hpp:116-163) ------------- */
+/* DensifyConfig (trainer.hpp:32-47): the thresholds of plan_densify. */
+typedef struct {
+  double grad_threshold;      /* densify when mean |d L / d mean2d| > this */
+  double percent_dense;       /* clone below percent_dense * extent, split above */
+  double opacity_prune;       /* prune sigmoid(opacity) < this */
+  double split_scale_divisor; /* split children's scale shrinks by this */
+} gss_densify_config;
+/* plan_densify on a restored snapshot in device memory (rows n x 59) with device statistics
+ * accum_norm (double[n]) / accum_cnt (int32[n]): survivors (device int32, capacity n) receive the
+ * ascending kept ids, children (device, capacity 2n x 59) the appended rows in the reference's order;
+ * counts_host[0..4] = survivors, children, clones, splits, pruned. Decisions and child rows are
+ * bit-identical to the reference (the split children's Rng / libm part runs on the host). */
+int gss_plan_densify(const float* rows, int64_t n, const double* accum_norm, const int32_t* accum_cnt,
+                     const gss_densify_config* cfg, double extent, uint64_t seed, int32_t* survivors,
+                     float* children, int64_t* counts_host, gss_stream_t stream);
+/* A densification event of the engine (drains first): snapshot, plan, apply — survivors keep
+ * their stored parameters, optimizer state and counters, children get zero state; statistics reset.
+ * counts_host[0..5] = survivors, children, clones, splits, pruned, new Gaussian count. */
+int gss_engine_densify(gss_engine* e, const gss_densify_config* cfg, double extent, uint64_t seed,
+                       int64_t* counts_host);
+
 /* ---- scene inputs (not on the hot path) ---------------------------------------------------- */
 /* synth_scene parameter + camera generation (synth.hpp:100-154), bit-identical to the reference
  * generator; cfg[14] = box, radius_min, radius_max, fov_deg, fov_ramp, target_jitter, near, far,

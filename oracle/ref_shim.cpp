@@ -389,3 +389,47 @@ REF_API void ref_engine_stage_ns(void* h, int64_t* out6) {
     for (int k = 0; k < 6; ++k)
       if (std::strcmp(r.stage, names[k]) == 0) out6[k] += r.t1_ns - r.t0_ns;
 }
+
+// Densification (trainer.hpp:166-213; engine.hpp:116-163). dcfg = grad_threshold, percent_dense,
+// opacity_prune, split_scale_divisor. counts5 = survivors, children, clones, splits, pruned.
+namespace {
+DensifyConfig densify_cfg(const double* d) {
+  DensifyConfig dc;
+  dc.grad_threshold = d[0];
+  dc.percent_dense = d[1];
+  dc.opacity_prune = d[2];
+  dc.split_scale_divisor = d[3];
+  return dc;
+}
+}  // namespace
+REF_API void ref_plan_densify(int n, const float* rows, const double* norm, const int* cnt, const double* dcfg,
+                              double extent, uint64_t seed, int* survivors, float* children, int64_t* counts5) {
+  const GaussianSet<F> gs = set_from_rows(n, rows);
+  const std::vector<double> nv(norm, norm + n);
+  const std::vector<int> cv(cnt, cnt + n);
+  const DensifyPlan<F> plan = plan_densify<F>(gs, nv, cv, densify_cfg(dcfg), extent, seed);
+  std::memcpy(survivors, plan.survivors.data(), plan.survivors.size() * sizeof(int));
+  std::memcpy(children, plan.child_rows.data(), plan.child_rows.size() * sizeof(F));
+  counts5[0] = (int64_t)plan.survivors.size();
+  counts5[1] = (int64_t)(plan.child_rows.size() / kParamDim);
+  counts5[2] = plan.clones;
+  counts5[3] = plan.splits;
+  counts5[4] = plan.pruned;
+}
+REF_API int ref_engine_densify(void* h, const double* dcfg, double extent, uint64_t seed, int64_t* counts5) {
+  try {
+    auto* e = static_cast<RefEngine*>(h);
+    const GaussianSet<F> snap = e->eng->snapshot();
+    const DensifyPlan<F> plan =
+        plan_densify<F>(snap, e->eng->accum_grad_norm(), e->eng->accum_grad_count(), densify_cfg(dcfg), extent, seed);
+    e->eng->apply_densify(plan.survivors, plan.child_rows);
+    counts5[0] = (int64_t)plan.survivors.size();
+    counts5[1] = (int64_t)(plan.child_rows.size() / kParamDim);
+    counts5[2] = plan.clones;
+    counts5[3] = plan.splits;
+    counts5[4] = plan.pruned;
+    return 0;
+  } catch (...) {
+    return status_of_current();
+  }
+}

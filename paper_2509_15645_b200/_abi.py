@@ -115,6 +115,11 @@ class GssEngineConfig(C.Structure):
     ]
 
 
+class GssDensifyConfig(C.Structure):
+    _fields_ = [("grad_threshold", C.c_double), ("percent_dense", C.c_double), ("opacity_prune", C.c_double),
+                ("split_scale_divisor", C.c_double)]
+
+
 P, I64, I32, F32, F64, SZ = C.c_void_p, C.c_int64, C.c_int32, C.c_float, C.c_double, C.c_size_t
 
 # name -> (restype, argtypes); the exported symbol set of include/gss_b200.h.
@@ -147,6 +152,8 @@ SIGNATURES = {
     "gss_rasterize_records_backward": (C.c_int, [P, P, P, P]),
     "gss_chain_backward": (C.c_int, [C.POINTER(GssRenderScene), C.POINTER(GssCamera), P, P, P, I64, P, I64, P, P]),
     "gss_engine_config_default": (None, [C.POINTER(GssEngineConfig)]),
+    "gss_plan_densify": (C.c_int, [P, I64, P, P, C.POINTER(GssDensifyConfig), F64, C.c_uint64, P, P, P, P]),
+    "gss_engine_densify": (C.c_int, [P, C.POINTER(GssDensifyConfig), F64, C.c_uint64, P]),
     "gss_engine_create": (P, [I64, P, I32, P, P, C.POINTER(GssEngineConfig)]),
     "gss_engine_destroy": (None, [P]),
     "gss_engine_run": (C.c_int, [P, I32, P, P]),

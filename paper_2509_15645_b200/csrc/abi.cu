@@ -48,6 +48,10 @@ void chain_backward(const gss_render_scene* scene, const gss_camera* cam, const 
                     float* gg, int64_t gstride, float* gn, int64_t nstride, float* mean2d, cudaStream_t st);
 // engine.cu
 void engine_config_default(gss_engine_config* c);
+void engine_densify(gss_engine* e, const gss_densify_config* dc, double extent, uint64_t seed, int64_t* counts);
+void plan_densify(const float* rows, int64_t n, const double* norm, const int32_t* cnt,
+                  const gss_densify_config* dc, double extent, uint64_t seed, int32_t* survivors, float* children,
+                  int64_t* counts, cudaStream_t st);
 gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss_camera* cams, const float* gts,
                           const gss_engine_config* cfg);
 void engine_destroy(gss_engine* e);
@@ -270,6 +274,24 @@ GSS_API int gss_chain_backward(const gss_render_scene* scene, const gss_camera* 
     require_device();
     chain_backward(scene, cam, records, sums, grad_geo, geo_stride, grad_nongeo, ng_stride, mean2d_opt,
                    as_stream(stream));
+  });
+}
+
+GSS_API int gss_plan_densify(const float* rows, int64_t n, const double* accum_norm, const int32_t* accum_cnt,
+                             const gss_densify_config* cfg, double extent, uint64_t seed, int32_t* survivors,
+                             float* children, int64_t* counts_host, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    plan_densify(rows, n, accum_norm, accum_cnt, cfg, extent, seed, survivors, children, counts_host,
+                 as_stream(stream));
+  });
+}
+
+GSS_API int gss_engine_densify(gss_engine* e, const gss_densify_config* cfg, double extent, uint64_t seed,
+                               int64_t* counts_host) {
+  return guarded([&] {
+    require_device();
+    engine_densify(e, cfg, extent, seed, counts_host);
   });
 }
 

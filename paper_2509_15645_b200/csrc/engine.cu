@@ -34,6 +34,9 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
 void rasterize_forward(gss_render_ctx* ctx, const gss_render_scene* scene, const gss_camera* cam,
                        const gss_viewport* vp, float* image, const float* gt, int64_t normalizer, float* d_img,
                        float* loss_dev, float* final_T_opt, int32_t* ncontrib_opt, int64_t* meta, cudaStream_t st);
+void plan_densify(const float* rows, int64_t n, const double* norm, const int32_t* cnt,
+                  const gss_densify_config* dc, double extent, uint64_t seed, int32_t* survivors, float* children,
+                  int64_t* counts, cudaStream_t st);
 void rasterize_forward_geometry(gss_render_ctx* ctx, const gss_render_scene* scene, const gss_camera* cam,
                                 const gss_viewport* vp, cudaStream_t st);
 void rasterize_forward_finish(gss_render_ctx* ctx, float* image, const float* gt, int64_t normalizer, float* d_img,
@@ -596,13 +599,10 @@ void engine_drain(gss_engine* e) {
   drain(e);
 }
 
-// snapshot (engine.hpp:91-111): both tiers restored (no pending pass), joined to n x 59.
-void engine_snapshot(gss_engine* e, float* rows_out) {
-  require(e && rows_out, "snapshot: null argument");
-  if (e->open_pending >= 0) drain(e);
+namespace {
+// Restored parameters of both tiers joined to n x 59 rows in device memory (engine.hpp:91-111).
+float* snapshot_dev(gss_engine* e, cudaStream_t s) {
   const int64_t n = e->n;
-  if (n == 0) return;
-  cudaStream_t s = e->sD;
   int32_t* all = dmalloc<int32_t>((size_t)n);
   float* geo = dmalloc<float>((size_t)n * kGeoDim);
   float* ng = dmalloc<float>((size_t)n * kNgDim);
@@ -613,9 +613,127 @@ void engine_snapshot(gss_engine* e, float* rows_out) {
   adam_restore(&e->ng, all, n, nullptr, nullptr, ng, s);
   join_rows_kernel<<<(unsigned)ceil_div(n * kRowDim, 256), 256, 0, s>>>(geo, ng, n, rows);
   GSS_LAUNCHED();
-  GSS_CUDA(cudaMemcpyAsync(rows_out, rows, (size_t)n * kRowDim * 4, cudaMemcpyDeviceToHost, s));
   GSS_CUDA(cudaStreamSynchronize(s));
-  cudaFree(all); cudaFree(geo); cudaFree(ng); cudaFree(rows);
+  cudaFree(all); cudaFree(geo); cudaFree(ng);
+  return rows;
+}
+
+// apply_densify (engine.hpp:116-163): row j < nsurv of the new tiers = old row survivors[j] (stored
+// w/m/v and counter); row nsurv + k = child k (w from the child row, zero state).
+__global__ void densify_apply_kernel(int64_t nsurv, int64_t nchild, const int32_t* survivors, const float* children,
+                                     const float* gw, const float* gm, const float* gv, const uint8_t* gc,
+                                     const float* nwold, const uint8_t* nc, float* gw2, float* gm2, float* gv2,
+                                     uint8_t* gc2, float* nw2, uint8_t* nc2) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= nsurv + nchild) return;
+  if (j < nsurv) {
+    const int64_t o = survivors[j];
+    for (int c = 0; c < kGeoDim; ++c) {
+      gw2[j * kGeoDim + c] = gw[o * kGeoDim + c];
+      gm2[j * kGeoDim + c] = gm[o * kGeoDim + c];
+      gv2[j * kGeoDim + c] = gv[o * kGeoDim + c];
+    }
+    for (int c = 0; c < kNgStride; ++c) nw2[j * kNgStride + c] = nwold[o * kNgStride + c];  // w, m, v
+    gc2[j] = gc[o];
+    nc2[j] = nc[o];
+  } else {
+    const float* row = children + (j - nsurv) * kRowDim;
+    for (int c = 0; c < kGeoDim; ++c) {
+      gw2[j * kGeoDim + c] = row[c];
+      gm2[j * kGeoDim + c] = 0.0f;
+      gv2[j * kGeoDim + c] = 0.0f;
+    }
+    for (int c = 0; c < kNgStride; ++c) nw2[j * kNgStride + c] = 0.0f;
+    for (int c = 0; c < kNgDim; ++c) nw2[j * kNgStride + c] = row[kGeoDim + c];
+    gc2[j] = 0;
+    nc2[j] = 0;
+  }
+}
+}  // namespace
+
+// snapshot (engine.hpp:91-111): both tiers restored (no pending pass), joined to n x 59.
+void engine_snapshot(gss_engine* e, float* rows_out) {
+  require(e && rows_out, "snapshot: null argument");
+  if (e->open_pending >= 0) drain(e);
+  const int64_t n = e->n;
+  if (n == 0) return;
+  cudaStream_t s = e->sD;
+  float* rows = snapshot_dev(e, s);
+  GSS_CUDA(cudaMemcpy(rows_out, rows, (size_t)n * kRowDim * 4, cudaMemcpyDeviceToHost));
+  cudaFree(rows);
+}
+
+// Densification event (trainer.hpp:578-591 with engine.hpp:116-163): snapshot, plan_densify on the
+// device statistics, apply. counts[0..5] = survivors, children, clones, splits, pruned, new n.
+void engine_densify(gss_engine* e, const gss_densify_config* dc, double extent, uint64_t seed, int64_t* counts) {
+  require(e && dc && counts, "densify: null argument");
+  if (e->open_pending >= 0) drain(e);
+  GSS_CUDA(cudaDeviceSynchronize());
+  cudaStream_t s = e->sD;
+  const int64_t n = e->n;
+  float* rows = n > 0 ? snapshot_dev(e, s) : nullptr;
+  int32_t* surv = dmalloc<int32_t>((size_t)std::max<int64_t>(n, 1));
+  float* children = dmalloc<float>((size_t)std::max<int64_t>(2 * n, 1) * kRowDim);
+  plan_densify(rows, n, e->accum_norm, e->accum_cnt, dc, extent, seed, surv, children, counts, s);
+  const int64_t nsurv = counts[0], nchild = counts[1], n2 = nsurv + nchild;
+  require(n2 <= INT32_MAX, "densify: population overflow");
+  const size_t nn = (size_t)std::max<int64_t>(n2, 1);
+  float* gw2 = dmalloc<float>(nn * kGeoDim);
+  float* gm2 = dmalloc<float>(nn * kGeoDim);
+  float* gv2 = dmalloc<float>(nn * kGeoDim);
+  uint8_t* gc2 = dmalloc<uint8_t>(nn);
+  float* nw2 = nullptr;
+  uint8_t* nc2 = nullptr;
+  if (e->ng_host) {
+    GSS_CUDA(cudaHostAlloc((void**)&nw2, nn * kNgStride * 4, cudaHostAllocMapped));
+    GSS_CUDA(cudaHostAlloc((void**)&nc2, nn, cudaHostAllocMapped));
+  } else {
+    nw2 = dmalloc<float>(nn * kNgStride);
+    nc2 = dmalloc<uint8_t>(nn);
+  }
+  if (n2 > 0) {
+    densify_apply_kernel<<<(unsigned)ceil_div(n2, 256), 256, 0, s>>>(nsurv, nchild, surv, children, e->gw, e->gm,
+                                                                    e->gv, e->gcnt, e->nw, e->ncnt, gw2, gm2, gv2,
+                                                                    gc2, nw2, nc2);
+    GSS_LAUNCHED();
+  }
+  GSS_CUDA(cudaStreamSynchronize(s));
+  cudaFree(rows);
+  cudaFree(surv);
+  cudaFree(children);
+  cudaFree(e->gw); cudaFree(e->gm); cudaFree(e->gv); cudaFree(e->gcnt);
+  if (e->ng_host) {
+    cudaFreeHost(e->nw); cudaFreeHost(e->ncnt);
+  } else {
+    cudaFree(e->nw); cudaFree(e->ncnt);
+  }
+  e->gw = gw2; e->gm = gm2; e->gv = gv2; e->gcnt = gc2;
+  e->nw = nw2; e->nm = nw2 + kNgSeg; e->nv = nw2 + 2 * kNgSeg; e->ncnt = nc2;
+  e->n = n2;
+  e->geo.w = gw2; e->geo.m = gm2; e->geo.v = gv2; e->geo.counter = gc2; e->geo.n = n2;
+  e->ng.w = e->nw; e->ng.m = e->nm; e->ng.v = e->nv; e->ng.counter = nc2; e->ng.n = n2;
+  // n-sized per-iteration buffers and statistics
+  for (int p = 0; p < 3; ++p) {
+    cudaFree(e->ids[p]);
+    e->ids[p] = dmalloc<int32_t>(nn);
+  }
+  cudaFree(e->cull_ws);
+  e->cull_ws_bytes = cull_workspace_bytes(n2);
+  e->cull_ws = dmalloc<char>(e->cull_ws_bytes);
+  GSS_CUDA(cudaMemset(e->cull_ws, 0, e->cull_ws_bytes));
+  cudaFree(e->accum_norm);
+  cudaFree(e->accum_cnt);
+  e->accum_norm = dmalloc<double>(nn);
+  e->accum_cnt = dmalloc<int32_t>(nn);
+  GSS_CUDA(cudaMemset(e->accum_norm, 0, nn * 8));
+  GSS_CUDA(cudaMemset(e->accum_cnt, 0, nn * 4));
+  // stage buffers hold rows of the old population: invalidate (engine.hpp:154-162)
+  for (int b = 0; b < 2; ++b) {
+    e->fwd_iter[b] = -1;
+    e->g_iter[b] = -1;
+    e->g_plan[b] = -1;
+  }
+  counts[5] = n2;
 }
 
 void engine_state(gss_engine* e, float* geo_w, float* ng_w, float* ng_m, float* ng_v, uint8_t* ng_counter,

@@ -23,7 +23,7 @@ from typing import Optional, Sequence
 import numpy as np
 import torch
 
-from ._abi import (GssArena, GssCamera, GssEngineConfig, GssGroup, GssRenderScene, GssSparseGrads, GssViewport,
+from ._abi import (GssArena, GssCamera, GssDensifyConfig, GssEngineConfig, GssGroup, GssRenderScene, GssSparseGrads, GssViewport,
                    ConfigError, InvariantViolation, check, lib)
 
 K_GEO_DIM, K_NONGEO_DIM, K_PARAM_DIM = 10, 49, 59
@@ -594,6 +594,37 @@ class OptimConfig:
                 GroupSpec("sh_rest", 14, 45, hp(self.lr_sh / self.sh_rest_divisor))]
 
 
+@dataclass
+class DensifyConfig:
+    """DensifyConfig (trainer.hpp:32-47) thresholds."""
+
+    grad_threshold: float = 2e-4
+    percent_dense: float = 0.01
+    opacity_prune: float = 0.005
+    split_scale_divisor: float = 1.6
+
+    def c_struct(self) -> GssDensifyConfig:
+        return GssDensifyConfig(self.grad_threshold, self.percent_dense, self.opacity_prune, self.split_scale_divisor)
+
+
+def plan_densify(rows: torch.Tensor, accum_norm: torch.Tensor, accum_cnt: torch.Tensor, cfg: DensifyConfig,
+                 extent: float, seed: int, stream=None):
+    """plan_densify (trainer.hpp:166-213) on a device snapshot (n x 59): (survivors ascending,
+    child rows k x 59, counts dict)."""
+    n = int(rows.shape[0])
+    dev = rows.device
+    surv = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    kids = torch.empty((max(2 * n, 1), K_PARAM_DIM), dtype=torch.float32, device=dev)
+    counts = np.zeros(5, np.int64)
+    c = cfg.c_struct()
+    check(lib().gss_plan_densify(_ptr(rows), n, _ptr(accum_norm), _ptr(accum_cnt), C.byref(c), float(extent),
+                                 int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(surv), _ptr(kids), counts.ctypes.data,
+                                 _stream(stream)))
+    torch.cuda.current_stream().synchronize()
+    k = dict(zip(("survivors", "children", "clones", "splits", "pruned"), counts.tolist()))
+    return surv[: k["survivors"]], kids[: k["children"]], k
+
+
 class OffloadEngine:
     """OffloadEngine (engine.hpp:55-192) on the B200: two CUDA streams replace the two workers."""
 
@@ -678,6 +709,15 @@ class OffloadEngine:
 
     def launches(self) -> int:
         return int(lib().gss_engine_launches(self.h))
+
+    def densify(self, cfg: DensifyConfig, extent: float, seed: int):
+        """A densification event (trainer.hpp:578-591): snapshot, plan_densify, apply_densify."""
+        counts = np.zeros(6, np.int64)
+        c = cfg.c_struct()
+        check(lib().gss_engine_densify(self.h, C.byref(c), float(extent), int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                       counts.ctypes.data))
+        self.n = int(counts[5])
+        return dict(zip(("survivors", "children", "clones", "splits", "pruned", "n"), counts.tolist()))
 
 
 def launch_count() -> int:

@@ -61,6 +61,8 @@ def ref():
             "ref_engine_state": (None, [P, P, P, P, P, P, P]),
             "ref_engine_accum": (None, [P, P, P]),
             "ref_engine_stage_ns": (None, [P, P]),
+            "ref_plan_densify": (None, [C.c_int, P, P, P, P, F64, C.c_uint64, P, P, P]),
+            "ref_engine_densify": (C.c_int, [P, P, F64, C.c_uint64, P]),
         }
         for k, (r, a) in sig.items():
             f = getattr(l, k)
@@ -334,6 +336,14 @@ class RefEngine:
         ref().ref_engine_accum(self.h, _p(norm), _p(cnt))
         return norm[: self.n], cnt[: self.n]
 
+    def densify(self, dcfg, extent, seed):
+        """plan_densify + apply_densify (trainer.hpp:578-591) on the reference engine."""
+        counts = np.zeros(5, np.int64)
+        st = ref().ref_engine_densify(self.h, _p(np.asarray(dcfg, np.float64)), float(extent), int(seed), _p(counts))
+        assert st == 0, st
+        self.n = int(counts[0] + counts[1])
+        return counts
+
     def stage_ns(self):
         out = np.zeros(6, np.int64)
         ref().ref_engine_stage_ns(self.h, _p(out))
@@ -434,3 +444,18 @@ def check_scene(seed, n, img, sh_degree):
     cam = look_at([0, 0, -2.2], [0, 0, 0], fx, fx, img, img, 0.1, 50.0)
     gt = np.array([rng.uniform(0.0, 1.0) for _ in range(img * img * 3)], np.float64).astype(np.float32)
     return rows, cam, gt.reshape(img, img, 3)
+
+
+def ref_plan_densify(rows, norm, cnt, dcfg, extent, seed):
+    """The reference plan_densify (trainer.hpp:166-213) on a host snapshot: (survivors, children, counts)."""
+    rows = np.ascontiguousarray(rows, np.float32)
+    n = rows.shape[0]
+    norm = np.ascontiguousarray(norm, np.float64)
+    cnt = np.ascontiguousarray(cnt, np.int32)
+    surv = np.zeros(max(n, 1), np.int32)
+    kids = np.zeros((max(2 * n, 1), 59), np.float32)
+    counts = np.zeros(5, np.int64)
+    d = np.asarray(dcfg, np.float64)
+    ref().ref_plan_densify(n, _p(rows), _p(norm), _p(cnt), _p(d), float(extent), int(seed), _p(surv), _p(kids),
+                           _p(counts))
+    return surv[: counts[0]], kids[: counts[1]], counts
