@@ -175,6 +175,10 @@ int gss_loss_l1(const float* image, const float* gt, int64_t elems, int64_t norm
 int gss_rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* grad_geo, int64_t geo_stride,
                            float* grad_nongeo, int64_t ng_stride, float* mean2d_opt, gss_stream_t stream);
 
+/* image_mse numerator (trainer.hpp:113-122) for psnr / psnr_over_views (trainer.hpp:124-145):
+ * sum_dev (device double) = sum over elems of (double(a) - double(b))^2, fixed-order reduction. */
+int gss_image_sq_err(const float* a, const float* b, int64_t elems, double* sum_dev, gss_stream_t stream);
+
 /* ---- split-phase rasterizer: image-parallel rendering over N GPUs --------- */
 /* The reference renders a view on one process (render.hpp:384-640) and splits it only into two
  * viewports (engine.hpp:266-273, splitter.hpp:31-123). Across GPUs the view is cut into column

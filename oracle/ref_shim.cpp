@@ -433,3 +433,38 @@ REF_API int ref_engine_densify(void* h, const double* dcfg, double extent, uint6
     return status_of_current();
   }
 }
+
+// compute_split_points (splitter.hpp:31-81) on n x 10 geo rows. out (per camera): split flag,
+// column, left count, right count, search evals; ratio: used ratio.
+REF_API void ref_compute_split_points(const float* geo, int n, int ncams, const void* cams, double mem_limit,
+                                      int* out5, double* ratio) {
+  std::vector<Camera<F>> cv(static_cast<const Camera<F>*>(cams), static_cast<const Camera<F>*>(cams) + ncams);
+  const SplitTable t = compute_split_points<F>(RowView<F>{geo, kGeoDim}, n, cv, mem_limit);
+  for (int i = 0; i < ncams; ++i) {
+    const SplitEntry& e = t.cameras[i];
+    out5[i * 5 + 0] = e.split ? 1 : 0;
+    out5[i * 5 + 1] = e.column;
+    out5[i * 5 + 2] = e.left_count;
+    out5[i * 5 + 3] = e.right_count;
+    out5[i * 5 + 4] = e.search_evals;
+    ratio[i] = e.used_ratio;
+  }
+}
+
+// psnr_over_views (trainer.hpp:131-145) of n x 59 rows over the given cameras / ground truths.
+REF_API double ref_psnr_over_views(int n, const float* rows, int ncams, const void* cams, const float* gts,
+                                   int sh_degree, int* exact) {
+  const GaussianSet<F> gs = set_from_rows(n, rows);
+  std::vector<Camera<F>> cv(static_cast<const Camera<F>*>(cams), static_cast<const Camera<F>*>(cams) + ncams);
+  std::vector<Image<F>> gv;
+  size_t off = 0;
+  for (int k = 0; k < ncams; ++k) {
+    Image<F> im(cv[k].width, cv[k].height);
+    std::memcpy(im.data.data(), gts + off, im.data.size() * sizeof(F));
+    off += im.data.size();
+    gv.push_back(std::move(im));
+  }
+  const PsnrResult r = psnr_over_views<F>(gs, cv, gv, sh_degree, Vec3<F>{0, 0, 0}, 1);
+  *exact = r.exact ? 1 : 0;
+  return r.db;
+}

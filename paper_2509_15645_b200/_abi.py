@@ -143,6 +143,7 @@ SIGNATURES = {
                                         C.POINTER(GssViewport), P, P, I64, P, P, P, P, P, P]),
     "gss_loss_l1": (C.c_int, [P, P, I64, I64, P, P, P]),
     "gss_rasterize_backward": (C.c_int, [P, P, P, I64, P, I64, P, P]),
+    "gss_image_sq_err": (C.c_int, [P, P, I64, P, P]),
     "gss_project": (C.c_int, [C.POINTER(GssRenderScene), C.POINTER(GssCamera), C.POINTER(GssViewport), P, P]),
     "gss_route_strips": (C.c_int, [P, I64, P, I32, P, P, P]),
     "gss_gather_records": (C.c_int, [P, P, I64, P, P]),

@@ -33,6 +33,7 @@ void loss_l1(const float* image, const float* gt, int64_t elems, int64_t normali
              cudaStream_t st);
 void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int64_t gstride, float* gn,
                         int64_t nstride, float* mean2d, cudaStream_t st);
+void image_sq_err(const float* a, const float* b, int64_t elems, double* sum_dev, cudaStream_t st);
 void project(const gss_render_scene* scene, const gss_camera* cam, const gss_viewport* vp, void* records,
              cudaStream_t st);
 void route_strips(const void* records, int64_t count, const int32_t* strip_x, int nstrips, int32_t* dest_slots,
@@ -213,6 +214,13 @@ GSS_API int gss_rasterize_backward(gss_render_ctx* ctx, const float* d_img, floa
   return guarded([&] {
     require_device();
     rasterize_backward(ctx, d_img, grad_geo, geo_stride, grad_nongeo, ng_stride, mean2d_opt, as_stream(stream));
+  });
+}
+
+GSS_API int gss_image_sq_err(const float* a, const float* b, int64_t elems, double* sum_dev, gss_stream_t stream) {
+  return guarded([&] {
+    require_device();
+    image_sq_err(a, b, elems, sum_dev, as_stream(stream));
   });
 }
 

@@ -426,6 +426,39 @@ __global__ void loss_partial_kernel(const float* img, const float* gt, int64_t n
   }
 }
 
+// image_mse numerator (trainer.hpp:113-122): sum of (double(a) - double(b))^2, per-block fp64 partials
+// in a fixed order (deterministic).
+__global__ void sq_err_partial_kernel(const float* a, const float* b, int64_t n, double* partials) {
+  __shared__ double red[8];
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = (double)a[i] - (double)b[i];
+    acc += d * d;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    partials[blockIdx.x] = s;
+  }
+}
+
+__global__ void sum_partials_kernel(const double* partials, int n, double* out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partials[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    *out = t;
+  }
+}
+
 // Fixed-order final reduction: loss = float(sum) * inv (render.hpp:510).
 __global__ void loss_final_kernel(const double* partials, int n, float inv, float* loss, double* sum_out) {
   __shared__ double red[32];
@@ -1208,6 +1241,22 @@ void loss_l1(const float* image, const float* gt, int64_t elems, int64_t normali
   loss_partial_kernel<<<blocks, 256, 0, st>>>(image, gt, elems, inv, d_img, lp);
   GSS_LAUNCHED();
   loss_final_kernel<<<1, 1024, 0, st>>>(lp, blocks, inv, loss_dev, nullptr);
+  GSS_LAUNCHED();
+  GSS_CUDA(cudaFreeAsync(lp, st));
+}
+
+void image_sq_err(const float* a, const float* b, int64_t elems, double* sum_dev, cudaStream_t st) {
+  require(elems >= 0 && sum_dev && (elems == 0 || (a && b)), "image_sq_err: null argument");
+  if (elems == 0) {
+    GSS_CUDA(cudaMemsetAsync(sum_dev, 0, sizeof(double), st));
+    return;
+  }
+  const int blocks = (int)std::min<int64_t>(ceil_div(elems, 256), 1024);
+  double* lp = nullptr;
+  GSS_CUDA(cudaMallocAsync((void**)&lp, (size_t)blocks * 8, st));
+  sq_err_partial_kernel<<<blocks, 256, 0, st>>>(a, b, elems, lp);
+  GSS_LAUNCHED();
+  sum_partials_kernel<<<1, 1024, 0, st>>>(lp, blocks, sum_dev);
   GSS_LAUNCHED();
   GSS_CUDA(cudaFreeAsync(lp, st));
 }

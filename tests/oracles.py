@@ -63,6 +63,8 @@ def ref():
             "ref_engine_stage_ns": (None, [P, P]),
             "ref_plan_densify": (None, [C.c_int, P, P, P, P, F64, C.c_uint64, P, P, P]),
             "ref_engine_densify": (C.c_int, [P, P, F64, C.c_uint64, P]),
+            "ref_compute_split_points": (None, [P, C.c_int, C.c_int, P, F64, P, P]),
+            "ref_psnr_over_views": (F64, [C.c_int, P, C.c_int, P, P, C.c_int, P]),
         }
         for k, (r, a) in sig.items():
             f = getattr(l, k)
@@ -459,3 +461,23 @@ def ref_plan_densify(rows, norm, cnt, dcfg, extent, seed):
     ref().ref_plan_densify(n, _p(rows), _p(norm), _p(cnt), _p(d), float(extent), int(seed), _p(surv), _p(kids),
                            _p(counts))
     return surv[: counts[0]], kids[: counts[1]], counts
+
+
+def ref_compute_split_points(geo, cams, mem_limit):
+    """compute_split_points (splitter.hpp:31-81): per camera (split, column, left, right, evals), used ratios."""
+    geo = np.ascontiguousarray(geo, np.float32)
+    cams = np.ascontiguousarray(cams, np.float32)
+    out = np.zeros((cams.shape[0], 5), np.int32)
+    ratio = np.zeros(cams.shape[0], np.float64)
+    ref().ref_compute_split_points(_p(geo), geo.shape[0], cams.shape[0], _p(cams), float(mem_limit), _p(out),
+                                   _p(ratio))
+    return out, ratio
+
+
+def ref_psnr_over_views(rows, cams, gts, sh_degree=3):
+    rows = np.ascontiguousarray(rows, np.float32)
+    cams = np.ascontiguousarray(cams, np.float32)
+    gts = np.ascontiguousarray(gts, np.float32)
+    exact = np.zeros(1, np.int32)
+    db = ref().ref_psnr_over_views(rows.shape[0], _p(rows), cams.shape[0], _p(cams), _p(gts), sh_degree, _p(exact))
+    return db, bool(exact[0])
