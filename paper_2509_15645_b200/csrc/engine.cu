@@ -148,8 +148,9 @@ struct gss_engine {
   double* accum_norm = nullptr;
   int32_t* accum_cnt = nullptr;
   // streams / events
-  cudaStream_t sD = nullptr, sH = nullptr;
-  gssd::Ev ev_cull[3], ev_fp[2], ev_handoff[2], ev_lazy[2], ev_render[2];
+  cudaStream_t sD = nullptr, sH = nullptr, sC = nullptr;  // sC: host->device ground-truth copies of step()
+  gssd::Ev ev_cull[3], ev_fp[2], ev_handoff[2], ev_lazy[2], ev_render[2], ev_gt;
+  bool gt_pending = false;  // render must wait for ev_gt (the step's ground truth in flight)
   struct TimeRec {
     int stage;
     cudaEvent_t a, b;
@@ -303,6 +304,10 @@ void stage_render(gss_engine* e, int g, const gss_camera& cam, const float* gt_d
     // grads[b] is free once lazy(g-2) consumed it
     GSS_CUDA(cudaStreamWaitEvent(s, e->ev_lazy[b].e, 0));
   }
+  if (e->gt_pending) {  // step(): the ground truth was copied in on sC, overlapping cull/geometry/gather
+    GSS_CUDA(cudaStreamWaitEvent(s, e->ev_gt.e, 0));
+    e->gt_pending = false;
+  }
   rasterize_forward_finish(e->rctx, e->image, gt_dev, full, e->d_img, loss_out, s);
   rasterize_backward(e->rctx, e->d_img, e->g_geo[b], kGeoDim, e->g_ng[b], kNgDim, e->g_m2d[b], s);
   e->g_plan[b] = p;
@@ -450,6 +455,7 @@ gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss
   e->ng_host = cfg->nongeo_on_host != 0;
   GSS_CUDA(cudaStreamCreateWithFlags(&e->sD, cudaStreamNonBlocking));
   GSS_CUDA(cudaStreamCreateWithFlags(&e->sH, cudaStreamNonBlocking));
+  GSS_CUDA(cudaStreamCreateWithFlags(&e->sC, cudaStreamNonBlocking));
   const size_t nn = (size_t)std::max<int64_t>(n, 1);
   e->gw = dmalloc<float>(nn * kGeoDim);
   e->gm = dmalloc<float>(nn * kGeoDim);
@@ -537,6 +543,7 @@ void engine_destroy(gss_engine* e) {
   for (auto ev : e->ev_free) cudaEventDestroy(ev);
   if (e->sD) cudaStreamDestroy(e->sD);
   if (e->sH) cudaStreamDestroy(e->sH);
+  if (e->sC) cudaStreamDestroy(e->sC);
   cudaGetLastError();
   delete e;
 }
@@ -583,7 +590,11 @@ void engine_step(gss_engine* e, const gss_camera* cam, const float* gt_host, flo
     e->valid_counts.clear();
   }
   const size_t bytes = (size_t)cam->width * cam->height * 3 * 4;
-  GSS_CUDA(cudaMemcpyAsync(e->gt_step, gt_host, bytes, cudaMemcpyHostToDevice, e->sD));
+  // The previous step's composite has finished (step() synchronises on its loss), so the single
+  // ground-truth buffer is free; the copy runs on its own stream and only the composite waits for it.
+  GSS_CUDA(cudaMemcpyAsync(e->gt_step, gt_host, bytes, cudaMemcpyHostToDevice, e->sC));
+  GSS_CUDA(cudaEventRecord(e->ev_gt.e, e->sC));
+  e->gt_pending = true;
   iteration(e, g, *cam, e->gt_step, e->loss_dev);
   e->next_iter = g + 1;
   float l = 0.0f;
