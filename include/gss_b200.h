@@ -296,6 +296,11 @@ int gss_engine_densify(gss_engine* e, const gss_densify_config* cfg, double exte
  * rows_out: host n x 59; cams_out: host cams. Ground truth is rendered with gss_rasterize_forward. */
 int gss_synth_scene(uint64_t seed, int64_t n, int32_t cams, int32_t width, int32_t height, int32_t sh_degree,
                     const double* cfg, float* rows_out, gss_camera* cams_out);
+/* init_gaussians (scene.hpp:146-195): one Gaussian per point (host positions m x 3, colors m x 3
+ * or NULL) with the exact O(M^2) kNN log-scale (fp64 on the device), identity rotation, opacity
+ * logit(init_opacity), DC colour; rows_out host m x 59, bit-identical to the reference. */
+int gss_init_gaussians(const float* positions, const float* colors, int32_t m, int32_t knn, double min_knn_dist,
+                       double init_opacity, float* rows_out);
 /* look_at_camera (scene.hpp:99-126). */
 int gss_look_at_camera(const float* eye, const float* target, float fx, float fy, int32_t w, int32_t h,
                        float near_p, float far_p, gss_camera* out);

@@ -468,3 +468,22 @@ REF_API double ref_psnr_over_views(int n, const float* rows, int ncams, const vo
   *exact = r.exact ? 1 : 0;
   return r.db;
 }
+
+// init_gaussians (scene.hpp:146-195) of a point cloud; rows_out m x 59.
+REF_API int ref_init_gaussians(const float* positions, const float* colors, int m, int knn, double min_knn_dist,
+                               double init_opacity, float* rows_out) {
+  try {
+    PointCloud pc;
+    pc.positions.assign(positions, positions + size_t(m) * 3);
+    if (colors) pc.colors.assign(colors, colors + size_t(m) * 3);
+    InitConfig ic;
+    ic.knn = knn;
+    ic.min_knn_dist = min_knn_dist;
+    ic.init_opacity = init_opacity;
+    const GaussianSet<F> gs = init_gaussians<F>(pc, ic);
+    for (int i = 0; i < m; ++i) gs.full_row(i, rows_out + size_t(i) * kParamDim);
+    return 0;
+  } catch (...) {
+    return status_of_current();
+  }
+}

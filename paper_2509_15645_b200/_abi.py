@@ -167,6 +167,7 @@ SIGNATURES = {
     "gss_engine_stage_ms": (C.c_int, [P, P]),
     "gss_engine_launches": (I64, [P]),
     "gss_synth_scene": (C.c_int, [C.c_uint64, I64, I32, I32, I32, I32, P, P, P]),
+    "gss_init_gaussians": (C.c_int, [P, P, I32, I32, F64, F64, P]),
     "gss_look_at_camera": (C.c_int, [P, P, F32, F32, I32, I32, F32, F32, C.POINTER(GssCamera)]),
 }
 

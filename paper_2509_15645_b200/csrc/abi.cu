@@ -49,6 +49,8 @@ void chain_backward(const gss_render_scene* scene, const gss_camera* cam, const 
                     float* gg, int64_t gstride, float* gn, int64_t nstride, float* mean2d, cudaStream_t st);
 // engine.cu
 void engine_config_default(gss_engine_config* c);
+void init_gaussians(const float* positions, const float* colors, int m, int knn, double min_knn_dist,
+                    double init_opacity, float* rows_out);
 void engine_densify(gss_engine* e, const gss_densify_config* dc, double extent, uint64_t seed, int64_t* counts);
 void plan_densify(const float* rows, int64_t n, const double* norm, const int32_t* cnt,
                   const gss_densify_config* dc, double extent, uint64_t seed, int32_t* survivors, float* children,
@@ -300,6 +302,14 @@ GSS_API int gss_engine_densify(gss_engine* e, const gss_densify_config* cfg, dou
   return guarded([&] {
     require_device();
     engine_densify(e, cfg, extent, seed, counts_host);
+  });
+}
+
+GSS_API int gss_init_gaussians(const float* positions, const float* colors, int32_t m, int32_t knn,
+                               double min_knn_dist, double init_opacity, float* rows_out) {
+  return guarded([&] {
+    require_device();
+    init_gaussians(positions, colors, m, knn, min_knn_dist, init_opacity, rows_out);
   });
 }
 

@@ -263,3 +263,104 @@ void plan_densify(const float* rows, int64_t n, const double* norm, const int32_
 }
 
 }  // namespace gssd
+
+// ---- init_gaussians (scene.hpp:146-195) ------------------------------------------
+// Exact O(M^2) kNN on the device: thread per point, candidate points streamed through SMEM tiles,
+// distances in fp64 exactly as the reference (double differences, IEEE sqrt, no contraction); the k
+// smallest are kept sorted (ties keep the earlier value, as the reference's insertion sort) and
+// summed ascending. mean_dist comes back to the host, whose libm takes the log (bit-identical rows).
+namespace gssd {
+namespace {
+constexpr int kKnnMax = 16;
+constexpr int kKnnTile = 256;
+
+__global__ void knn_mean_kernel(const float* pos, int m, int k, double min_dist, double* mean_out) {
+  __shared__ float tile[kKnnTile * 3];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double best[kKnnMax];
+  int filled = 0;
+  const double xi = i < m ? (double)pos[i * 3] : 0.0, yi = i < m ? (double)pos[i * 3 + 1] : 0.0,
+               zi = i < m ? (double)pos[i * 3 + 2] : 0.0;
+  for (int t0 = 0; t0 < m; t0 += kKnnTile) {
+    const int nt = min(kKnnTile, m - t0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nt * 3; e += blockDim.x) tile[e] = pos[t0 * 3 + e];
+    __syncthreads();
+    if (i >= m) continue;
+    for (int jj = 0; jj < nt; ++jj) {
+      const int j = t0 + jj;
+      if (j == i) continue;
+      const double dx = (double)tile[jj * 3] - xi;
+      const double dy = (double)tile[jj * 3 + 1] - yi;
+      const double dz = (double)tile[jj * 3 + 2] - zi;
+      const double d = sqrt(dx * dx + dy * dy + dz * dz);
+      if (filled < k) {
+        int b = filled++;
+        best[b] = d;
+        for (; b > 0 && best[b] < best[b - 1]; --b) {
+          const double tmp = best[b];
+          best[b] = best[b - 1];
+          best[b - 1] = tmp;
+        }
+      } else if (d < best[k - 1]) {
+        int b = k - 1;
+        best[b] = d;
+        for (; b > 0 && best[b] < best[b - 1]; --b) {
+          const double tmp = best[b];
+          best[b] = best[b - 1];
+          best[b - 1] = tmp;
+        }
+      }
+    }
+  }
+  if (i >= m) return;
+  double mean_dist = min_dist;
+  if (m > 1) {
+    double s = 0.0;
+    for (int b = 0; b < filled; ++b) s += best[b];
+    mean_dist = filled > 0 ? s / filled : min_dist;
+    if (mean_dist < min_dist) mean_dist = min_dist;
+  }
+  mean_out[i] = mean_dist;
+}
+}  // namespace
+
+// rows_out (host, m x 59): init_gaussians of the point cloud positions (host, m x 3) / colors
+// (host m x 3 or null).
+void init_gaussians(const float* positions, const float* colors, int m, int knn, double min_knn_dist,
+                    double init_opacity, float* rows_out) {
+  require(m >= 1, "init_gaussians: point cloud is empty");
+  require(positions && rows_out, "init_gaussians: null argument");
+  const int k = std::max(1, std::min(knn, m - 1));
+  require(k <= kKnnMax, "init_gaussians: knn must be <= 16");
+  float* pos_dev = nullptr;
+  double* mean_dev = nullptr;
+  GSS_CUDA(cudaMalloc(&pos_dev, (size_t)m * 12));
+  GSS_CUDA(cudaMalloc(&mean_dev, (size_t)m * 8));
+  GSS_CUDA(cudaMemcpy(pos_dev, positions, (size_t)m * 12, cudaMemcpyHostToDevice));
+  knn_mean_kernel<<<(unsigned)ceil_div(m, 128), 128>>>(pos_dev, m, k, min_knn_dist, mean_dev);
+  GSS_LAUNCHED();
+  std::vector<double> mean((size_t)m);
+  GSS_CUDA(cudaMemcpy(mean.data(), mean_dev, (size_t)m * 8, cudaMemcpyDeviceToHost));
+  cudaFree(pos_dev);
+  cudaFree(mean_dev);
+  const double kShC0 = 0.28209479177387814;
+  const float op = float(std::log(init_opacity) - std::log(1.0 - init_opacity));  // logit (scene.hpp:141)
+  for (int i = 0; i < m; ++i) {
+    float* r = rows_out + (size_t)i * kRow;
+    std::memset(r, 0, kRow * sizeof(float));
+    const float log_s = float(std::log(mean[i]));
+    for (int a = 0; a < 3; ++a) {
+      r[a] = positions[i * 3 + a];
+      r[3 + a] = log_s;
+    }
+    r[6] = 1.0f;
+    r[10] = op;
+    for (int c = 0; c < 3; ++c) {
+      const double col = colors ? double(colors[i * 3 + c]) : 0.5;
+      r[11 + c] = float((col - 0.5) / kShC0);
+    }
+  }
+}
+
+}  // namespace gssd

@@ -546,6 +546,18 @@ def synth_scene_params(cfg: SynthConfig):
     return rows[: cfg.n], [cams[i] for i in range(cfg.cams)]
 
 
+def init_gaussians(positions: np.ndarray, colors: Optional[np.ndarray] = None, knn: int = 3,
+                   min_knn_dist: float = 0.01, init_opacity: float = 0.1) -> np.ndarray:
+    """init_gaussians (scene.hpp:146-195) with the exact O(M^2) kNN on the device: rows m x 59."""
+    pos = np.ascontiguousarray(positions, np.float32).reshape(-1, 3)
+    m = pos.shape[0]
+    col = None if colors is None else np.ascontiguousarray(colors, np.float32).reshape(-1, 3)
+    rows = np.zeros((max(m, 1), K_PARAM_DIM), np.float32)
+    check(lib().gss_init_gaussians(pos.ctypes.data, None if col is None else col.ctypes.data, m, int(knn),
+                                   float(min_knn_dist), float(init_opacity), rows.ctypes.data))
+    return rows[:m]
+
+
 def render_view(rows: torch.Tensor, cam: GssCamera, sh_degree: int, background=(0.0, 0.0, 0.0)) -> torch.Tensor:
     """render_view (synth.hpp:81-94) on the device: cull + rasterize over a full viewport."""
     geo = rows[:, :K_GEO_DIM].contiguous()

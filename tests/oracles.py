@@ -65,6 +65,7 @@ def ref():
             "ref_engine_densify": (C.c_int, [P, P, F64, C.c_uint64, P]),
             "ref_compute_split_points": (None, [P, C.c_int, C.c_int, P, F64, P, P]),
             "ref_psnr_over_views": (F64, [C.c_int, P, C.c_int, P, P, C.c_int, P]),
+            "ref_init_gaussians": (C.c_int, [P, P, C.c_int, C.c_int, F64, F64, P]),
         }
         for k, (r, a) in sig.items():
             f = getattr(l, k)
@@ -481,3 +482,13 @@ def ref_psnr_over_views(rows, cams, gts, sh_degree=3):
     exact = np.zeros(1, np.int32)
     db = ref().ref_psnr_over_views(rows.shape[0], _p(rows), cams.shape[0], _p(cams), _p(gts), sh_degree, _p(exact))
     return db, bool(exact[0])
+
+
+def ref_init_gaussians(positions, colors=None, knn=3, min_knn_dist=0.01, init_opacity=0.1):
+    pos = np.ascontiguousarray(positions, np.float32)
+    col = None if colors is None else np.ascontiguousarray(colors, np.float32)
+    m = pos.shape[0]
+    rows = np.zeros((m, 59), np.float32)
+    st = ref().ref_init_gaussians(_p(pos), _p(col), m, knn, float(min_knn_dist), float(init_opacity), _p(rows))
+    assert st == 0, st
+    return rows

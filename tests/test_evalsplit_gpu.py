@@ -72,3 +72,17 @@ def test_balanced_strips_render_bit_exact():
         parts.append(IP.strip_forward(recv, cam, IP.strip_viewport(vp, b, k), (0.0, 0.0, 0.0), None, 0).image)
     img = torch.cat(parts, dim=1)
     assert torch.equal(img, fw.image)
+
+
+@pytest.mark.parametrize("m,knn,colors", [(1, 3, False), (2, 3, True), (5000, 3, True), (3001, 8, False)])
+def test_init_gaussians_equals_reference(ref, m, knn, colors):
+    """init_gaussians (scene.hpp:146-195): exact O(M^2) kNN on the device."""
+    rng = np.random.default_rng(m + knn)
+    pos = rng.uniform(-1, 1, (m, 3)).astype(np.float32)
+    if m > 10:
+        pos[5] = pos[3]  # duplicate points: zero distances and ties
+        pos[7] = pos[3]
+    col = rng.uniform(0, 1, (m, 3)).astype(np.float32) if colors else None
+    want = O.ref_init_gaussians(pos, col, knn)
+    got = G.init_gaussians(pos, col, knn)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
