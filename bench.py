@@ -399,15 +399,16 @@ def kernel_probe(G, truth, cams, dev, a):
     for k in range(nsched):
         m = torch.rand(n, device=dev, generator=gen) < dens
         gi = torch.nonzero(m).flatten().to(torch.int32)
-        sched.append((gi, torch.randn(gi.numel(), 49, device=dev, generator=gen)))
+        # gradient rows in the engine's stage layout: 49 values in 52-float (16-byte aligned) rows
+        sched.append((gi, torch.randn(gi.numel(), 52, device=dev, generator=gen)))
     # steady state: counters spread over [0, defer_max] (a long run's distribution; a fresh arena's
     # never-touched rows would all saturate in the same pass every 16th pass)
     arena.counter.copy_(torch.randint(0, 16, (n,), device=dev, generator=gen, dtype=torch.int32).to(torch.uint8))
     tcount = torch.zeros(reps + 8, dtype=torch.int64, device=dev)
     for k in range(20):
-        G.deferred_update(arena, G.SparseGrads(sched[k % nsched][0], sched[k % nsched][1], 49), want_touched=False)
+        G.deferred_update(arena, G.SparseGrads(sched[k % nsched][0], sched[k % nsched][1], 52), want_touched=False)
     st = arena.c_struct()
-    gs = [G.SparseGrads(gi, gr, 49).c_struct() for gi, gr in sched]
+    gs = [G.SparseGrads(gi, gr, 52).c_struct() for gi, gr in sched]
     tot = {"t": 0, "g": 0}
 
     def deferred(r):

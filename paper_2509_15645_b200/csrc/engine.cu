@@ -58,6 +58,9 @@ constexpr int kGeoDim = 10, kNgDim = 49, kRowDim = 59;
 // touched row of the deferred update / forwarding gather is five whole cache lines walked with
 // 16-byte accesses instead of three scattered 196-byte rows.
 constexpr int kNgStride = 160, kNgSeg = 52;
+// Gradient stage rows of the non-geometric tier: 52 floats (16-byte aligned, the deferred pass's TMA
+// gathers them whole).
+constexpr int kNgGradStride = 52;
 
 __global__ void handoff_stats_kernel(const int32_t* ids, const int64_t* count, const float* mean2d, double* norm,
                                      int32_t* cnt) {
@@ -188,7 +191,7 @@ void ensure_rows(gss_engine* e, int64_t V) {
   for (int b = 0; b < 2; ++b) {
     grow(e->fwd[b], kNgDim);
     grow(e->g_geo[b], kGeoDim);
-    grow(e->g_ng[b], kNgDim);
+    grow(e->g_ng[b], kNgGradStride);
     grow(e->g_m2d[b], 2);
   }
   e->cap_rows = cap;
@@ -265,7 +268,7 @@ void stage_forward_params(gss_engine* e, int g) {
     pg.count = e->count_host[pp];
     pg.count_dev = e->count[pp];
     pg.rows = e->g_ng[pb];
-    pg.stride = kNgDim;
+    pg.stride = kNgGradStride;
     pg.col0 = 0;
   }
   adam_restore(&e->ng, e->ids[p], V, e->count[p], pending ? &pg : nullptr, e->fwd[b], s);
@@ -309,7 +312,7 @@ void stage_render(gss_engine* e, int g, const gss_camera& cam, const float* gt_d
     e->gt_pending = false;
   }
   rasterize_forward_finish(e->rctx, e->image, gt_dev, full, e->d_img, loss_out, s);
-  rasterize_backward(e->rctx, e->d_img, e->g_geo[b], kGeoDim, e->g_ng[b], kNgDim, e->g_m2d[b], s);
+  rasterize_backward(e->rctx, e->d_img, e->g_geo[b], kGeoDim, e->g_ng[b], kNgGradStride, e->g_m2d[b], s);
   e->g_plan[b] = p;
   stage_end(e, kRender, s, b);
   GSS_CUDA(cudaEventRecord(e->ev_render[b].e, s));
@@ -361,7 +364,7 @@ void stage_lazy(gss_engine* e, int g) {
   gr.count = e->count_host[p];
   gr.count_dev = e->count[p];
   gr.rows = e->g_ng[b];
-  gr.stride = kNgDim;
+  gr.stride = kNgGradStride;
   gr.col0 = 0;
   adam_update(&e->ng, &gr, nullptr, nullptr, s);
   stage_end(e, kLazy, s, b);

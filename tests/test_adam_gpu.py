@@ -193,3 +193,24 @@ def test_optim_bench_equivalence_on_device(ref):
     G.flush_deferred(defer)
     dev = O.rel_err(dense.w.cpu().numpy(), defer.w.cpu().numpy()).max()
     assert dev <= 1e-4
+
+
+@pytest.mark.parametrize("defer_max", [1, 15])
+def test_engine_layout_interleaved_aligned_grads_bitwise(ref, defer_max):
+    """The engine's layout: row-interleaved arena + 16-byte-aligned gradient rows (stride 52, the
+    engine's gradient stage); padding columns of the gradient rows are never read as data."""
+    rng = np.random.default_rng(77 + defer_max)
+    n, dim = 5000, 49
+    ra, ga = make_pair(n, dim, GROUPS49, defer_max, rng, interleaved=True)
+    for step in range(40):
+        dens = 0.0 if step % 13 == 7 else rng.uniform(0.02, 0.3)
+        ids = np.nonzero(rng.uniform(size=n) < dens)[0].astype(np.int32)
+        rows = rng.normal(size=(ids.size, 52)).astype(np.float32)
+        rows[:, 49:] = np.nan  # padding: must never be read as data
+        t_ref = ra.deferred(ids, rows, 52)
+        t_gpu = G.deferred_update(ga, G.SparseGrads(torch.from_numpy(ids).cuda(), torch.from_numpy(rows).cuda(), 52))
+        assert np.array_equal(t_ref, t_gpu.cpu().numpy())
+        assert_same(ra, ga)
+    ra.flush()
+    G.flush_deferred(ga)
+    assert_same(ra, ga)
