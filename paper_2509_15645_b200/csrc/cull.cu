@@ -328,26 +328,31 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) cull_kernel(const __grid
   __syncthreads();
   const long long base = base_s;
   TRACE(3);
-  // Scatter ascending ids (+ optional mask words): warp per tile, lane l < 16 owns word l.
-  for (int jt = warp; jt < ntl; jt += kThreads / 32) {
-    const uint32_t wv = lane < kWordsPerTile ? words[jt * kWordsPerTile + lane] : 0u;
-    const long long wg = (rowc >> 5) + (long long)jt * kWordsPerTile + lane;
-    if (a.mask && lane < kWordsPerTile && wg < a.nwords) a.mask[wg] = wv;
+  // Scatter ascending ids (+ optional mask words): thread per mask word (16-lane segments = one tile),
+  // segmented scan of the words' popcounts for the in-tile offset, then each thread writes its word's
+  // set bits (few at the sparse keep rates of a view: no per-tile serial loop).
+  static_assert(kWordsPerTile == 16, "segmented scan assumes 16 words per tile");
+  for (int w0 = warp * 32; w0 < ntl * kWordsPerTile; w0 += kThreads) {
+    const int w = w0 + lane;
+    const int jt = w / kWordsPerTile;
+    const bool okw = w < ntl * kWordsPerTile;
+    uint32_t wv = okw ? words[w] : 0u;
+    const long long wg = (rowc >> 5) + w;
+    if (a.mask && okw && wg < a.nwords) a.mask[wg] = wv;
     const int pc = __popc(wv);
     int wi = pc;
 #pragma unroll
     for (int o = 1; o < 16; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += v;
+      const int v = __shfl_up_sync(0xffffffffu, wi, o, 16);
+      if ((lane & 15) >= o) wi += v;
     }
-    const long long tbase = base + tpre[jt];
-#pragma unroll 4
-    for (int i = 0; i < kWordsPerTile; ++i) {
-      const uint32_t wbits = __shfl_sync(0xffffffffu, wv, i);
-      const int wp = __shfl_sync(0xffffffffu, wi - pc, i);
-      if (wbits & (1u << lane)) {
-        const long long pos = tbase + wp + __popc(wbits & ((1u << lane) - 1u));
-        a.ids[pos] = (int32_t)(rowc + ((long long)jt * kWordsPerTile + i) * 32 + lane);
+    if (okw) {
+      long long pos = base + tpre[jt] + (wi - pc);
+      const long long id0 = rowc + (long long)w * 32;
+      while (wv) {
+        const int bit = __ffs(wv) - 1;
+        wv &= wv - 1;
+        a.ids[pos++] = (int32_t)(id0 + bit);
       }
     }
   }
