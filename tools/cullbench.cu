@@ -44,6 +44,18 @@ int main(int argc, char** argv) {
     for (int c = 0; c < ctas; ++c) { mn = std::min(mn, tr[c][ph] - t0); mx = std::max(mx, tr[c][ph] - t0); avg += tr[c][ph] - t0; }
     printf("phase %d: min %.2f us  avg %.2f us  max %.2f us\n", ph, mn / 1e3, avg / ctas / 1e3, mx / 1e3);
   }
+  // streaming-end time by CTA index (deciles) and the slowest CTAs with their queued-row counts
+  for (int d = 0; d < 10; ++d) {
+    double s1 = 0; int c0 = d * ctas / 10, c1 = (d + 1) * ctas / 10;
+    for (int c = c0; c < c1; ++c) s1 += tr[c][1] - t0;
+    printf("ctas %3d-%3d: stream end avg %.2f us\n", c0, c1 - 1, s1 / (c1 - c0) / 1e3);
+  }
+  for (int r = 0; r < 8; ++r) {
+    int worst = 0;
+    for (int c = 1; c < ctas; ++c) if (tr[c][1] > tr[worst][1]) worst = c;
+    printf("slow cta %d: stream end %.2f us queued %llu start %.2f\n", worst, (tr[worst][1] - t0) / 1e3, tr[worst][5], (tr[worst][0]-t0)/1e3);
+    tr[worst][1] = 0;
+  }
 #endif
   return 0;
 }
