@@ -1091,7 +1091,7 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
   GSS_CUDA(cudaGetDevice(&dev));
   GSS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int64_t cap = count_dev ? std::max<int64_t>(count, a.n) : count;
-  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kRestoreChunk), (int64_t)sms * 4));
+  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kRestoreChunk), (int64_t)sms * 64));
   if (host_resident(a)) blocks = std::min(blocks, kHostTierBlocks);
   int32_t* pbstart = nullptr;
   if (pending && pd.ids)
