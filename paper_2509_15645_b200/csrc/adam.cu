@@ -537,6 +537,9 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_WALK_MINB) walk_kernel(ArenaD
 #ifndef GSS_WALK4_KU
 #define GSS_WALK4_KU 2
 #endif
+#ifndef GSS_WALK_GRID
+#define GSS_WALK_GRID 8  // walk blocks per SM (grid-stride over the touch list)
+#endif
 #ifndef GSS_WALK4_MINB
 #define GSS_WALK4_MINB 3
 #endif
@@ -944,7 +947,7 @@ void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* 
     update_kernel<K, MODE><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, bstart, *L, tmask, tcount, err,
                                                                    tl);
     GSS_LAUNCHED();
-    int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, kUpdThreads), (int64_t)sm_count() * 8));
+    int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, kUpdThreads), (int64_t)sm_count() * GSS_WALK_GRID));
     if (host_resident(a)) wblocks = std::min(wblocks, 4 * kHostTierBlocks);  // reads + writes in flight
     if (vector_rows(a))
       walk4_kernel<K, MODE><<<wblocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, *L, tl);
