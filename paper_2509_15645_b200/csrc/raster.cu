@@ -761,13 +761,16 @@ __global__ void __launch_bounds__(kSumThreads) slot_sum_kernel(int64_t V, const 
 }
 
 constexpr int kChainThreads = 128;
+#ifndef GSS_CHAIN_MINB
+#define GSS_CHAIN_MINB 6  // 6 blocks of 128 threads per SM (80 registers): the chain is latency bound
+#endif
 constexpr int kChainRow = 61;     // odd row pitch: conflict-free per-lane row access
 // Warp-cooperative: a warp owns 32 consecutive slots. It sums each slot's instance partials with
 // all lanes, stages the slots' 49-float non-geometric rows in SMEM with coalesced loads; each lane
 // then runs the reference chain for its slot, and the 59 outputs are written back through SMEM
 // with coalesced stores.
 template <int DEG>
-__global__ void __launch_bounds__(kChainThreads) chain_kernel(SceneDev s, Cam cam, Win w, int64_t V,
+__global__ void __launch_bounds__(kChainThreads, GSS_CHAIN_MINB) chain_kernel(SceneDev s, Cam cam, Win w, int64_t V,
                                                               const SplatRec* recs, const float* sums,
                                                               float* gg, int64_t gstride,
                                                               float* gn, int64_t nstride, float* mean2d) {
