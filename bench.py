@@ -268,7 +268,7 @@ def run_imgpar(a, rank, world):
     del td, geo_t, ng_t
     torch.cuda.empty_cache()
     start = training_start(truth)
-    tr = IP.ShardTrainer(start, cams, gts, ex)
+    tr = IP.ShardTrainer(start, cams, gts, ex, pipelined=True)
     for _ in range(a.warmup):
         tr.step()
     if world > 1:

@@ -244,11 +244,16 @@ class ShardTrainer:
         -> render(g) [image-parallel over the exchange group] -> geo_update(g)
 
     Every stage is shard-local except the render's two all-to-allv exchanges. With one rank and
-    SelfExchange the trajectory equals OffloadEngine(pipelined=False) on the same shard."""
+    SelfExchange the trajectory equals OffloadEngine(pipelined=False) on the same shard. pipelined=True
+    runs forward_params(g) and lazy(g-1) on a second CUDA stream (the engine's stream H,
+    engine.hpp:464-522) so the lazy update overlaps render(g); the results are bitwise the same."""
 
     def __init__(self, init_rows: np.ndarray, cams, gts, ex=None, optim: Optional[G.OptimConfig] = None, *,
-                 sh_degree: int = 3, sh_warmup_step: int = 0, background=(0.0, 0.0, 0.0), device=None):
+                 sh_degree: int = 3, sh_warmup_step: int = 0, background=(0.0, 0.0, 0.0), device=None,
+                 pipelined: bool = False):
         self.ex = ex or SelfExchange()
+        self.pipelined = bool(pipelined)
+        self.sH = torch.cuda.Stream() if self.pipelined else None
         self.opt = optim or G.OptimConfig()
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         rows = torch.from_numpy(np.ascontiguousarray(init_rows, np.float32)).to(dev)
@@ -273,9 +278,24 @@ class ShardTrainer:
         gt = gt if gt is not None else self.gts[g % len(self.cams)]
         vp = G.viewport_full(cam.width, cam.height)
         ids = G.frustum_cull(self.geo.w, self.n, cam, vp)                      # cull(g)
-        fwd = G.restore_view(self.ng, ids, self.pending)                       # forward_params(g)
-        if self.pending is not None:                                           # lazy(g-1)
-            G.deferred_update(self.ng, self.pending, want_touched=False, check_invariants=False)
+        if self.pipelined:
+            main, sH = torch.cuda.current_stream(), self.sH
+            sH.wait_stream(main)  # ids(g) and the pending grads(g-1) are ready
+            ids.record_stream(sH)
+            with torch.cuda.stream(sH):
+                fwd = G.restore_view(self.ng, ids, self.pending, stream=sH)    # forward_params(g)
+                ev_fp = torch.cuda.Event()
+                ev_fp.record(sH)
+                if self.pending is not None:                                   # lazy(g-1), overlaps render(g)
+                    self.pending.ids.record_stream(sH)
+                    self.pending.rows.record_stream(sH)
+                    G.deferred_update(self.ng, self.pending, want_touched=False, check_invariants=False, stream=sH)
+            fwd.record_stream(main)
+            main.wait_event(ev_fp)
+        else:
+            fwd = G.restore_view(self.ng, ids, self.pending)                   # forward_params(g)
+            if self.pending is not None:                                       # lazy(g-1)
+                G.deferred_update(self.ng, self.pending, want_touched=False, check_invariants=False)
         deg = min(self.sh_degree, g // self.sh_warmup_step) if self.sh_warmup_step > 0 else self.sh_degree
         sc = G.RenderScene(ids=ids, geo=self.geo.w, nongeo=fwd, nongeo_compact=True, sh_degree=deg,
                            background=self.background)
@@ -288,9 +308,13 @@ class ShardTrainer:
         return loss
 
     def drain(self) -> None:
+        if self.pipelined:
+            torch.cuda.current_stream().wait_stream(self.sH)
         if self.pending is not None:
             G.deferred_update(self.ng, self.pending, want_touched=False, check_invariants=False)
             self.pending = None
+        if self.pipelined:  # the non-geometric arena was last written on stream H
+            torch.cuda.current_stream().wait_stream(self.sH)
 
     def state(self):
         return dict(geo_w=self.geo.w, ng_w=self.ng.w, ng_m=self.ng.m, ng_v=self.ng.v, ng_counter=self.ng.counter)

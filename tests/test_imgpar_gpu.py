@@ -191,9 +191,10 @@ def test_two_process_render_step_equals_simulation():
     assert np.array_equal(bits(full), bits(image.cpu().numpy()))
 
 
-def test_shard_trainer_world1_equals_engine():
+@pytest.mark.parametrize("pipelined", [False, True])
+def test_shard_trainer_world1_equals_engine(pipelined):
     rows, cams, gts = scene(13, 4000, 80, 64)
-    tr = IP.ShardTrainer(rows, cams, gts)
+    tr = IP.ShardTrainer(rows, cams, gts, pipelined=pipelined)
     losses = [tr.step() for _ in range(6)]
     tr.drain()
     torch.cuda.synchronize()
