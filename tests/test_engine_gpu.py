@@ -9,6 +9,7 @@
 """
 import numpy as np
 import pytest
+import torch
 
 import oracles as O
 import paper_2509_15645_b200 as G
@@ -121,3 +122,30 @@ def test_host_offload_tier_equals_hbm_bitwise(pipelined):
     sh, sd = eh.state(), ed.state()
     for k in ("geo_w", "ng_w", "ng_m", "ng_v", "ng_counter"):
         assert np.array_equal(np.asarray(sh[k]).view(np.uint8), np.asarray(sd[k]).view(np.uint8)), k
+
+
+def test_c1_config_twenty_iterations_track_reference(ref):
+    """BASELINE.json configs[0]: 100K Gaussians, 256x256 views, 8 cameras, the full
+    step (cull + forwarding gather + render forward/backward + geo Adam + deferred Adam, MAX=15) for
+    20 iterations: every loss within 1e-4 of the reference CPU engine's and the final snapshot within
+    the accumulated tolerance."""
+    import bench
+
+    cfg = G.SynthConfig(seed=1, n=100_000, cams=8, width=256, height=256, radius_min=1.5, radius_max=3.0,
+                        scale_min=0.003, scale_max=0.01, fov_deg=30.0)
+    truth, cams = G.synth_scene_params(cfg)
+    td = torch.from_numpy(truth).cuda()
+    gts = np.stack([G.render_view(td, c, 3).cpu().numpy() for c in cams])
+    del td
+    start = bench.training_start(truth)
+    e = G.OffloadEngine(start, cams, gts, pipelined=True)
+    losses, valid = e.run(20)
+    snap = e.snapshot()
+    e.close()
+    r = O.RefEngine(start, np.stack([O.cam_from_struct(c) for c in cams]), gts, pipelined=True, workers=8)
+    rl, rv = r.run(20)
+    assert np.array_equal(valid, rv)  # identical culls every iteration
+    assert np.all(np.abs(losses - rl) <= 1e-4 * np.maximum(1.0, np.abs(rl))), np.abs(losses - rl).max()
+    assert losses[0] == rl[0]  # the first forward sees identical parameters: bit-identical loss
+    dev = float(O.rel_err(snap, r.snapshot()).max())
+    assert dev <= 1e-3, dev
