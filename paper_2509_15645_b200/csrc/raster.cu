@@ -258,21 +258,41 @@ __global__ void duplicate_kernel(const SplatRec* recs, const int32_t* order, con
                                  const int32_t* offsets, Win w, int64_t V, uint32_t* keys, int32_t* vals,
                                  SplatRec* recs_rw, int32_t* slot_off) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= V) return;
-  const int32_t k = order[i];
-  const int32_t off = offsets[i];
-  recs_rw[k].off = off;
-  slot_off[k] = off;
-  if (ntiles[k] == 0) return;
-  const SplatRec r = recs[k];
-  int tx0, ty0, ntx, nty;
-  tile_box(r, w, tx0, ty0, ntx, nty);
-  int j = 0;
-  for (int ty = ty0; ty < ty0 + nty; ++ty)
-    for (int tx = tx0; tx < tx0 + ntx; ++tx, ++j) {
-      keys[off + j] = (uint32_t)(ty * w.tw + tx);
-      vals[off + j] = k;
+  const int lane = threadIdx.x & 31;
+  if (i - lane >= V) return;  // whole warp past the end
+  const bool valid = i < V;
+  int32_t k = 0, off = 0, nt = 0;
+  int tx0 = 0, ty0 = 0, ntx = 1, nty = 0;
+  if (valid) {
+    k = order[i];
+    off = offsets[i];
+    recs_rw[k].off = off;
+    slot_off[k] = off;
+    nt = ntiles[k];
+    if (nt > 0) tile_box(recs[k], w, tx0, ty0, ntx, nty);
+  }
+  if (nt > 0 && nt <= 4) {  // small splats: this lane writes its own keys (row-major tile order)
+    int j = 0;
+    for (int ty = ty0; ty < ty0 + nty; ++ty)
+      for (int tx = tx0; tx < tx0 + ntx; ++tx, ++j) {
+        keys[off + j] = (uint32_t)(ty * w.tw + tx);
+        vals[off + j] = k;
+      }
+  }
+  // large splats (near the camera: hundreds of tiles) are written by the whole warp, coalesced
+  unsigned big = __ballot_sync(0xffffffffu, nt > 4);
+  while (big) {
+    const int b = __ffs(big) - 1;
+    big &= big - 1;
+    const int32_t bk = __shfl_sync(0xffffffffu, k, b), boff = __shfl_sync(0xffffffffu, off, b);
+    const int bnt = __shfl_sync(0xffffffffu, nt, b), btx0 = __shfl_sync(0xffffffffu, tx0, b);
+    const int bty0 = __shfl_sync(0xffffffffu, ty0, b), bntx = __shfl_sync(0xffffffffu, ntx, b);
+    for (int j = lane; j < bnt; j += 32) {
+      const int ty = bty0 + j / bntx, tx = btx0 + j - (j / bntx) * bntx;
+      keys[boff + j] = (uint32_t)(ty * w.tw + tx);
+      vals[boff + j] = bk;
     }
+  }
 }
 
 // ntiles in sorted order (0 at position V), for the instance-offset scan: offsets[V] = I.
