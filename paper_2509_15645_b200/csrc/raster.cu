@@ -32,6 +32,24 @@ namespace gssd {
 constexpr int kTileSize = 16;
 constexpr int kTilePix = kTileSize * kTileSize;  // 256 threads per CTA
 constexpr int kFwdBatch = 256;
+// Minimum resident blocks per SM for the composite / sweep kernels (0 = no bound: the compiler
+// chooses the registers; the backward sweep then takes 78).
+#ifndef GSS_FWD_MINB
+#define GSS_FWD_MINB 0
+#endif
+#ifndef GSS_BWD_MINB
+#define GSS_BWD_MINB 0
+#endif
+#if GSS_FWD_MINB > 0
+#define GSS_FWD_BOUNDS __launch_bounds__(kTilePix, GSS_FWD_MINB)
+#else
+#define GSS_FWD_BOUNDS __launch_bounds__(kTilePix)
+#endif
+#if GSS_BWD_MINB > 0
+#define GSS_BWD_BOUNDS __launch_bounds__(kBwdThreads, GSS_BWD_MINB)
+#else
+#define GSS_BWD_BOUNDS __launch_bounds__(kBwdThreads)
+#endif
 constexpr int kBwdBatch = 64;
 
 struct __align__(16) SplatRec {
@@ -339,7 +357,7 @@ __device__ __forceinline__ void load_rec(SplatRec* dst, const SplatRec* recs, in
 // Each warp owns an 8x4 pixel block of the 16x16 tile. After a batch of records is staged in
 // SMEM, the warp ballots which records' pixel boxes intersect its block and walks only those
 // (warp-uniform loop); the per-pixel box test then reproduces the CSR membership exactly.
-__global__ void __launch_bounds__(kTilePix) forward_kernel(const SplatRec* __restrict__ recs,
+__global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
                                                            const int32_t* __restrict__ vals,
                                                            const int2* __restrict__ ranges, Win w, float bg0,
                                                            float bg1, float bg2, float* image, float* fT_out,
@@ -597,7 +615,7 @@ constexpr int kBwdPPT = GSS_BWD_PPT;              // pixels per thread
 constexpr int kBwdThreads = kTilePix / kBwdPPT;
 constexpr int kBwdWarps = kBwdThreads / 32;
 constexpr int kBand = 2 * kBwdPPT;                // rows per warp band
-__global__ void __launch_bounds__(kBwdThreads) backward_kernel(const SplatRec* __restrict__ recs,
+__global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs,
                                                                const int32_t* __restrict__ vals,
                                                                const int2* __restrict__ ranges, Win w, float bg0,
                                                                float bg1, float bg2, const float* __restrict__ fT_in,
