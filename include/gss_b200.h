@@ -251,6 +251,13 @@ int gss_engine_run(gss_engine* e, int32_t iters, float* losses, int32_t* valid_c
  * copied H2D inside the call) returning the loss to the host — the end-to-end entry point. */
 int gss_engine_step(gss_engine* e, const gss_camera* cam, const float* gt_host, float* loss_host,
                     int32_t* valid_count_host);
+/* gss_engine_step without the final wait: enqueues the iteration and returns; *loss_host (pinned
+ * host memory, required) receives the loss when the iteration's render completes, and gt_host must
+ * stay unchanged until then (gss_engine_drain waits for both). *valid_count_host is set on return.
+ * Consecutive async steps overlap step g+1's ground-truth copy and host work with step g's kernels;
+ * the trajectory is bit-identical to gss_engine_step / gss_engine_run. */
+int gss_engine_step_async(gss_engine* e, const gss_camera* cam, const float* gt_host, float* loss_host,
+                          int32_t* valid_count_host);
 /* Applies the lazy update still owed by an open step() segment (run() always drains itself). */
 int gss_engine_drain(gss_engine* e);
 /* snapshot (engine.hpp:91-111): restored parameters, host n x 59. */

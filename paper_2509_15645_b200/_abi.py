@@ -159,6 +159,7 @@ SIGNATURES = {
     "gss_engine_destroy": (None, [P]),
     "gss_engine_run": (C.c_int, [P, I32, P, P]),
     "gss_engine_step": (C.c_int, [P, C.POINTER(GssCamera), P, P, P]),
+    "gss_engine_step_async": (C.c_int, [P, C.POINTER(GssCamera), P, P, P]),
     "gss_engine_drain": (C.c_int, [P]),
     "gss_engine_snapshot": (C.c_int, [P, P]),
     "gss_engine_state": (C.c_int, [P, P, P, P, P, P, P]),

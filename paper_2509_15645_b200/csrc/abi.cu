@@ -59,7 +59,8 @@ gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss
                           const gss_engine_config* cfg);
 void engine_destroy(gss_engine* e);
 void engine_run(gss_engine* e, int iters, float* losses, int32_t* valid);
-void engine_step(gss_engine* e, const gss_camera* cam, const float* gt_host, float* loss_host, int32_t* valid_host);
+void engine_step(gss_engine* e, const gss_camera* cam, const float* gt_host, float* loss_host, int32_t* valid_host,
+                 bool wait);
 void engine_drain(gss_engine* e);
 void engine_snapshot(gss_engine* e, float* rows_out);
 void engine_state(gss_engine* e, float* geo_w, float* ng_w, float* ng_m, float* ng_v, uint8_t* ng_counter,
@@ -332,7 +333,15 @@ GSS_API int gss_engine_run(gss_engine* e, int32_t iters, float* losses, int32_t*
 }
 GSS_API int gss_engine_step(gss_engine* e, const gss_camera* cam, const float* gt_host, float* loss_host,
                             int32_t* valid_count_host) {
-  return guarded([&] { engine_step(e, cam, gt_host, loss_host, valid_count_host); });
+  return guarded([&] { engine_step(e, cam, gt_host, loss_host, valid_count_host, true); });
+}
+
+GSS_API int gss_engine_step_async(gss_engine* e, const gss_camera* cam, const float* gt_host, float* loss_host,
+                                  int32_t* valid_count_host) {
+  return guarded([&] {
+    require_device();
+    engine_step(e, cam, gt_host, loss_host, valid_count_host, false);
+  });
 }
 GSS_API int gss_engine_drain(gss_engine* e) {
   return guarded([&] { engine_drain(e); });

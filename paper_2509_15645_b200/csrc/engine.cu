@@ -145,14 +145,15 @@ struct gss_engine {
   gss_render_ctx* rctx = nullptr;
   float* image = nullptr;
   float* d_img = nullptr;
-  float* gt_step = nullptr;
+  float* gt_step[2] = {nullptr, nullptr};  // step(): double-buffered ground truth
+  int gt_cur = 0;
   float* loss_dev = nullptr;  // per iteration of a run
   int loss_cap = 0;
   double* accum_norm = nullptr;
   int32_t* accum_cnt = nullptr;
   // streams / events
   cudaStream_t sD = nullptr, sH = nullptr, sC = nullptr;  // sC: host->device ground-truth copies of step()
-  gssd::Ev ev_cull[3], ev_fp[2], ev_handoff[2], ev_lazy[2], ev_render[2], ev_gt;
+  gssd::Ev ev_cull[3], ev_fp[2], ev_handoff[2], ev_lazy[2], ev_render[2], ev_gt, ev_gt_done[2];
   bool gt_pending = false;  // render must wait for ev_gt (the step's ground truth in flight)
   struct TimeRec {
     int stage;
@@ -229,6 +230,23 @@ void collect_times(gss_engine* e) {
   }
   cudaGetLastError();
   e->pending_times.clear();
+}
+// Streaming (step()) without a drain: fold the intervals that have completed, so the event pool
+// stays bounded however long the host streams steps between drains.
+void collect_completed(gss_engine* e) {
+  std::vector<gss_engine::TimeRec> keep;
+  for (auto& r : e->pending_times) {
+    if (cudaEventQuery(r.b) != cudaSuccess) {
+      keep.push_back(r);
+      continue;
+    }
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) e->stage_ms[r.stage] += ms;
+    e->ev_free.push_back(r.a);
+    e->ev_free.push_back(r.b);
+  }
+  cudaGetLastError();
+  e->pending_times.swap(keep);
 }
 
 // engine.hpp:255-278 (no split cameras: the split machinery is §8f "next").
@@ -307,11 +325,13 @@ void stage_render(gss_engine* e, int g, const gss_camera& cam, const float* gt_d
     // grads[b] is free once lazy(g-2) consumed it
     GSS_CUDA(cudaStreamWaitEvent(s, e->ev_lazy[b].e, 0));
   }
-  if (e->gt_pending) {  // step(): the ground truth was copied in on sC, overlapping cull/geometry/gather
+  const bool step_gt = e->gt_pending;
+  if (step_gt) {  // step(): the ground truth was copied in on sC, overlapping cull/geometry/gather
     GSS_CUDA(cudaStreamWaitEvent(s, e->ev_gt.e, 0));
     e->gt_pending = false;
   }
   rasterize_forward_finish(e->rctx, e->image, gt_dev, full, e->d_img, loss_out, s);
+  if (step_gt) GSS_CUDA(cudaEventRecord(e->ev_gt_done[e->gt_cur].e, s));  // its buffer is free again
   rasterize_backward(e->rctx, e->d_img, e->g_geo[b], kGeoDim, e->g_ng[b], kNgGradStride, e->g_m2d[b], s);
   e->g_plan[b] = p;
   stage_end(e, kRender, s, b);
@@ -511,7 +531,8 @@ gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss
   const size_t img = (size_t)maxW * maxH * 3;
   e->image = dmalloc<float>(img);
   e->d_img = dmalloc<float>(img);
-  e->gt_step = dmalloc<float>(img);
+  e->gt_step[0] = dmalloc<float>(img);
+  e->gt_step[1] = dmalloc<float>(img);
   if (gts && ncams > 0) {
     e->gts_dev = dmalloc<float>(img * ncams);
     size_t off = 0;
@@ -541,7 +562,7 @@ void engine_destroy(gss_engine* e) {
   f(e->cull_ws);
   for (int b = 0; b < 2; ++b) { f(e->fwd[b]); f(e->g_geo[b]); f(e->g_ng[b]); f(e->g_m2d[b]); }
   render_ctx_destroy(e->rctx);
-  f(e->image); f(e->d_img); f(e->gt_step); f(e->loss_dev); f(e->accum_norm); f(e->accum_cnt);
+  f(e->image); f(e->d_img); f(e->gt_step[0]); f(e->gt_step[1]); f(e->loss_dev); f(e->accum_norm); f(e->accum_cnt);
   collect_times(e);
   for (auto ev : e->ev_free) cudaEventDestroy(ev);
   if (e->sD) cudaStreamDestroy(e->sD);
@@ -581,30 +602,43 @@ void engine_run(gss_engine* e, int iters, float* losses, int32_t* valid) {
 
 // Streaming entry point: one iteration with a host camera + ground truth. The segment stays open
 // (the lazy update of this iteration is applied by the next step, exactly as inside run()).
-void engine_step(gss_engine* e, const gss_camera* cam, const float* gt_host, float* loss_host, int32_t* valid_host) {
+// Synchronous: returns this step's loss. Asynchronous (wait = false): returns after enqueueing; the
+// loss lands in *loss_host (pinned) when the iteration's render is done (gss_engine_drain waits), so
+// the host prepares step g+1 — and its ground-truth copy — while step g still renders.
+void engine_step(gss_engine* e, const gss_camera* cam, const float* gt_host, float* loss_host, int32_t* valid_host,
+                 bool wait) {
   require(e && cam && gt_host, "engine_step: null argument");
   require(cam->width <= e->W && cam->height <= e->H, "engine_step: camera larger than the engine's image buffers");
   require(cam->near_plane > 0 && cam->far_plane > cam->near_plane, "camera: require 0 < near < far");
+  require(wait || loss_host, "engine_step: an asynchronous step needs a (pinned) loss destination");
   const int64_t l0 = launches();
   ensure_loss(e, 1);
+  if (e->pending_times.size() > 512) collect_completed(e);
   const int g = e->next_iter;
   if (e->open_pending < 0) {
     e->seg_begin = g;
     e->valid_counts.clear();
   }
   const size_t bytes = (size_t)cam->width * cam->height * 3 * 4;
-  // The previous step's composite has finished (step() synchronises on its loss), so the single
-  // ground-truth buffer is free; the copy runs on its own stream and only the composite waits for it.
-  GSS_CUDA(cudaMemcpyAsync(e->gt_step, gt_host, bytes, cudaMemcpyHostToDevice, e->sC));
+  // Double-buffered ground truth: buffer gb is free once the composite of step g-2 (its last reader)
+  // is done; the copy runs on its own stream and only this step's composite waits for it.
+  const int gb = g & 1;
+  GSS_CUDA(cudaStreamWaitEvent(e->sC, e->ev_gt_done[gb].e, 0));
+  GSS_CUDA(cudaMemcpyAsync(e->gt_step[gb], gt_host, bytes, cudaMemcpyHostToDevice, e->sC));
   GSS_CUDA(cudaEventRecord(e->ev_gt.e, e->sC));
   e->gt_pending = true;
-  iteration(e, g, *cam, e->gt_step, e->loss_dev);
+  e->gt_cur = gb;
+  iteration(e, g, *cam, e->gt_step[gb], e->loss_dev);
   e->next_iter = g + 1;
-  float l = 0.0f;
-  GSS_CUDA(cudaMemcpyAsync(&l, e->loss_dev, 4, cudaMemcpyDeviceToHost, e->sD));
-  GSS_CUDA(cudaStreamSynchronize(e->sD));
-  if (loss_host) *loss_host = l;
   if (valid_host) *valid_host = (int32_t)e->count_host[g % 3];
+  if (wait) {
+    float l = 0.0f;
+    GSS_CUDA(cudaMemcpyAsync(&l, e->loss_dev, 4, cudaMemcpyDeviceToHost, e->sD));
+    GSS_CUDA(cudaStreamSynchronize(e->sD));
+    if (loss_host) *loss_host = l;
+  } else {
+    GSS_CUDA(cudaMemcpyAsync(loss_host, e->loss_dev, 4, cudaMemcpyDeviceToHost, e->sD));
+  }
   e->launches_last = launches() - l0;
 }
 

@@ -686,6 +686,22 @@ class OffloadEngine:
         check(lib().gss_engine_step(self.h, C.byref(cam), gt.ctypes.data, C.byref(loss), C.byref(valid)))
         return float(loss.value), int(valid.value)
 
+    def step_async(self, cam: GssCamera, gt_host, loss_out) -> int:
+        """gss_engine_step_async: enqueue one iteration and return its valid count. gt_host and
+        loss_out are pinned host torch tensors (loss_out a float32 element, e.g. losses[i:i+1]);
+        both are owned by the step until drain()."""
+        for t in (gt_host, loss_out):
+            if not (isinstance(t, torch.Tensor) and t.is_pinned() and t.is_contiguous()):
+                raise ValueError("step_async: gt_host / loss_out must be contiguous pinned host tensors")
+        if gt_host.dtype != torch.float32 or loss_out.dtype != torch.float32 or loss_out.numel() < 1:
+            raise ValueError("step_async: float32 tensors required")
+        if gt_host.numel() != cam.width * cam.height * 3:
+            raise ValueError("step_async: gt_host must hold height*width*3 floats")
+        valid = C.c_int32(0)
+        check(lib().gss_engine_step_async(self.h, C.byref(cam), gt_host.data_ptr(), loss_out.data_ptr(),
+                                          C.byref(valid)))
+        return int(valid.value)
+
     def drain(self):
         check(lib().gss_engine_drain(self.h))
 

@@ -90,6 +90,24 @@ def test_step_api_equals_run(ref):
     assert np.array_equal(a.snapshot().view(np.uint32), b.snapshot().view(np.uint32))
 
 
+def test_step_async_equals_run():
+    """gss_engine_step_async (no per-step wait, double-buffered GT copies) is bit-identical to run()."""
+    start, cams, gts = scene()
+    a = engine(start, cams, gts)
+    b = engine(start, cams, None)
+    la, va = a.run(15)
+    gt_pin = [torch.from_numpy(gts[i]).contiguous().pin_memory() for i in range(len(cams))]
+    lb = torch.zeros(15, dtype=torch.float32).pin_memory()
+    vb = [b.step_async(G.camera_from_bytes(cams[g % len(cams)].tobytes()), gt_pin[g % len(cams)], lb[g:g + 1])
+          for g in range(15)]
+    b.drain()
+    assert np.array_equal(la.view(np.uint32), lb.numpy().view(np.uint32))
+    assert np.array_equal(va, np.array(vb))
+    assert np.array_equal(a.snapshot().view(np.uint32), b.snapshot().view(np.uint32))
+    with pytest.raises(ValueError):
+        b.step_async(G.camera_from_bytes(cams[0].tobytes()), torch.from_numpy(gts[0]), lb[:1])
+
+
 def test_empty_frustum_iteration(ref):
     """test_offload.cpp:214-233: zero valid ids, finite loss, counters advance."""
     cfg = G.SynthConfig(n=20, cams=1, width=8, height=8, seed=3)
