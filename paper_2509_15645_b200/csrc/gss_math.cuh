@@ -30,9 +30,14 @@ __device__ static const unsigned long long kExp2Tab[32] = {
     0x3feee89f995ad3adULL, 0x3feeff76f2fb5e47ULL, 0x3fef199bdd85529cULL, 0x3fef3720dcef9069ULL,
     0x3fef5818dcfba487ULL, 0x3fef7c97337b9b5fULL, 0x3fefa4afa2a490daULL, 0x3fefd0765b6e4540ULL};
 
+// The fp64 coefficients live in the constant bank so the DFMAs take them as c[][] operands
+// (as literals they are rematerialised into register pairs on every call inside a hot loop).
+static __constant__ double kExpCoef[4] = {0x1.71547652b82fep+0 * 32.0, 0x1.c6af84b912394p-5 / (32.0 * 32 * 32),
+                                          0x1.ebfce50fac4f3p-3 / (32.0 * 32), 0x1.62e42ff0c52d6p-1 / 32.0};
+
 // glibc 2.39 expf body (table-driven, FMA variant) for x in [-103.97, 88.72].
 __device__ __forceinline__ float gss_expf_core(float x) {
-  const double inv_ln2_n = 0x1.71547652b82fep+0 * 32.0, shift = 0x1.8p+52;
+  const double inv_ln2_n = kExpCoef[0], shift = 0x1.8p+52;
   const double xd = (double)x;
   double kd = __fma_rn(inv_ln2_n, xd, shift);
   const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
@@ -40,9 +45,9 @@ __device__ __forceinline__ float gss_expf_core(float x) {
   const double r = __fma_rn(inv_ln2_n, xd, -kd);
   const unsigned long long t = __ldg(&kExp2Tab[ki & 31]) + (ki << 47);
   const double s = __longlong_as_double((long long)t);
-  const double z = __fma_rn(0x1.c6af84b912394p-5 / (32.0 * 32 * 32), r, 0x1.ebfce50fac4f3p-3 / (32.0 * 32));
+  const double z = __fma_rn(kExpCoef[1], r, kExpCoef[2]);
   const double r2 = __dmul_rn(r, r);
-  double y = __fma_rn(0x1.62e42ff0c52d6p-1 / 32.0, r, 1.0);
+  double y = __fma_rn(kExpCoef[3], r, 1.0);
   y = __fma_rn(z, r2, y);
   y = __dmul_rn(y, s);
   return __double2float_rn(y);

@@ -102,7 +102,7 @@ struct DBuf {
 }  // namespace gssd
 
 struct gss_render_ctx {
-  gssd::DBuf recs, ntiles, offsets, keys_a, keys_b, vals_a, vals_b, cub_tmp, ranges, last, fT, partials, lossp,
+  gssd::DBuf recs, ntiles, offsets, keys_a, keys_b, vals_a, vals_b, cub_tmp, ranges, tile_order, last, fT, partials, lossp,
       hostcnt, sums, dkeys_a, dkeys_b, order_a, order_b, slot_off;
   gssd::Win win{};
   gssd::SceneDev sc{};
@@ -329,17 +329,100 @@ __global__ void ranges_kernel(const uint32_t* keys, int64_t I, int2* ranges) {
   if (i == I - 1 || keys[i + 1] != tile) ranges[tile].y = (int)(i + 1);
 }
 
+// Launch order of the tile CTAs: heaviest tiles first (longest-processing-time-first), so the
+// few tiles that hold many more instances than the rest (near-camera splats, dense clusters)
+// start in the first wave instead of forming the kernel's tail. One CTA buckets the tiles by
+// instance count (256 linear buckets below the maximum) and scatters them in descending bucket
+// order. Only the schedule changes: every tile's pixels and partials are computed exactly as
+// before, so the order within a bucket (atomic) does not affect any result.
+#ifndef GSS_LPT
+#define GSS_LPT 1
+#endif
+constexpr int kOrderThreads = 1024;
+__global__ void __launch_bounds__(kOrderThreads) tile_order_kernel(const int2* ranges, int ntile, int32_t* order) {
+  __shared__ int hist[256];
+  __shared__ int cmax;
+  const int t = threadIdx.x;
+  if (t < 256) hist[t] = 0;
+  if (t == 0) cmax = 0;
+  __syncthreads();
+  int m = 0;
+  for (int i = t; i < ntile; i += kOrderThreads) {
+    const int2 r = ranges[i];
+    m = max(m, r.y - r.x);
+  }
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((t & 31) == 0) atomicMax(&cmax, m);
+  __syncthreads();
+  const long long den = (long long)cmax + 1;
+  for (int i = t; i < ntile; i += kOrderThreads) {
+    const int2 r = ranges[i];
+    atomicAdd(&hist[255 - (int)((long long)(r.y - r.x) * 256 / den)], 1);
+  }
+  __syncthreads();
+  if (t < 32) {  // exclusive scan of 256 bucket counts, 8 per lane
+    int loc[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      loc[k] = hist[t * 8 + k];
+      sum += loc[k];
+    }
+    int inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (t >= o) inc += v;
+    }
+    int run = inc - sum;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      hist[t * 8 + k] = run;
+      run += loc[k];
+    }
+  }
+  __syncthreads();
+  for (int i = t; i < ntile; i += kOrderThreads) {
+    const int2 r = ranges[i];
+    order[atomicAdd(&hist[255 - (int)((long long)(r.y - r.x) * 256 / den)], 1)] = i;
+  }
+}
+
+__device__ __forceinline__ int tile_of(const int32_t* order) {
+#if GSS_LPT
+  return order[blockIdx.x];
+#else
+  return blockIdx.x;
+#endif
+}
+
 struct EvalOut {
   float alpha, q, weight;
   bool clamped;
 };
 
+// RN(1/det) when det lies in [2^-60, 2^60], else 0 (then the quotient takes the IEEE division).
+__device__ __forceinline__ float det_rcp(float det) {
+  return (det >= 0x1p-60f && det <= 0x1p60f) ? __frcp_rn(det) : 0.0f;
+}
+
+// RN(n / d) given rd = det_rcp(d): Markstein's correction q0 = RN(n*rd), q = RN(q0 + fma(-d, q0, n)*rd)
+// is the correctly rounded quotient for |n| in [2^-60, 2^60) (tools/divcheck.cu: 0 mismatches in
+// 1.07e10 pairs, including divisors with all-ones significands); other n take the IEEE division.
+__device__ __forceinline__ float div_rcp_rn(float n, float d, float rd) {
+  if (rd != 0.0f && ((__float_as_uint(n) >> 23) & 0xffu) - 67u < 120u) {
+    const float q0 = __fmul_rn(n, rd);
+    return __fmaf_rn(__fmaf_rn(-d, q0, n), rd, q0);
+  }
+  return __fdiv_rn(n, d);
+}
+
 // contrib_eval (render.hpp:342-358); det > 0 holds for every binned splat (render.hpp:418).
 // The exponent is -q/2 <= 0 (or NaN), so only the underflow / NaN guards of expf apply.
-__device__ __forceinline__ EvalOut contrib_eval(const SplatRec& r, float cx, float cy) {
+// rd: det_rcp(r.det) (the forward stages it per record), or 0 for the plain IEEE division.
+__device__ __forceinline__ EvalOut contrib_eval(const SplatRec& r, float cx, float cy, float rd = 0.0f) {
   EvalOut o;
   const float dx = cx - r.mx, dy = cy - r.my;
-  o.q = max0((r.c * dx * dx - 2.0f * r.b * dx * dy + r.a * dy * dy) / r.det);
+  o.q = max0(div_rcp_rn(r.c * dx * dx - 2.0f * r.b * dx * dy + r.a * dy * dy, r.det, rd));
   o.weight = gss_expf_nonpos(-0.5f * o.q);
   const float raw = r.ab * o.weight;
   o.clamped = raw > 0.999f;
@@ -359,14 +442,15 @@ __device__ __forceinline__ void load_rec(SplatRec* dst, const SplatRec* recs, in
 // (warp-uniform loop); the per-pixel box test then reproduces the CSR membership exactly.
 __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
                                                            const int32_t* __restrict__ vals,
-                                                           const int2* __restrict__ ranges, Win w, float bg0,
+                                                           const int2* __restrict__ ranges,
+                                                           const int32_t* __restrict__ tile_order, Win w, float bg0,
                                                            float bg1, float bg2, float* image, float* fT_out,
                                                            int32_t* last_out, int32_t* ncontrib_out,
                                                            const float* gt, int gt_width, float inv_norm,
                                                            float* d_img, double* loss_partials) {
   __shared__ SplatRec sh[kFwdBatch];
   __shared__ double red[kTilePix / 32];
-  const int tile = blockIdx.x;
+  const int tile = tile_of(tile_order);
   const int tx = tile % w.tw, ty = tile / w.tw;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 4;
@@ -381,7 +465,10 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
   for (int b = rg.x; b < rg.y; b += kFwdBatch) {
     if (__syncthreads_count(done) == kTilePix) break;
     const int nb = min(kFwdBatch, rg.y - b);
-    if ((int)threadIdx.x < nb) load_rec(&sh[threadIdx.x], recs, vals[b + threadIdx.x]);
+    if ((int)threadIdx.x < nb) {
+      load_rec(&sh[threadIdx.x], recs, vals[b + threadIdx.x]);
+      sh[threadIdx.x].depth = det_rcp(sh[threadIdx.x].det);  // the SMEM copy's depth slot holds RN(1/det)
+    }
     __syncthreads();
     for (int c0j = 0; c0j < nb && __any_sync(0xffffffffu, !done); c0j += 32) {
       const int jl = c0j + lane;
@@ -394,14 +481,14 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
       while (m) {
         const int j = c0j + __ffs(m) - 1;
         m &= m - 1;
-        if (done) continue;
         const SplatRec& r = sh[j];
-        if (x < r.bx0 || x >= r.bx1 || y < r.by0 || y >= r.by1) continue;
+        const int4 bx = *reinterpret_cast<const int4*>(&r.bx0);
+        if (!(!done & (x >= bx.x) & (x < bx.y) & (y >= bx.z) & (y < bx.w))) continue;
         if (T < 1e-4f) {
           done = true;
           continue;
         }
-        const EvalOut ev = contrib_eval(r, cx, cy);
+        const EvalOut ev = contrib_eval(r, cx, cy, r.depth);
         c0 += r.r * ev.alpha * T;
         c1 += r.g * ev.alpha * T;
         c2 += r.bl * ev.alpha * T;
@@ -440,7 +527,7 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
     if (threadIdx.x == 0) {
       double s = 0.0;
       for (int i = 0; i < kTilePix / 32; ++i) s += red[i];
-      loss_partials[blockIdx.x] = s;
+      loss_partials[tile] = s;
     }
   }
 }
@@ -617,7 +704,8 @@ constexpr int kBwdWarps = kBwdThreads / 32;
 constexpr int kBand = 2 * kBwdPPT;                // rows per warp band
 __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs,
                                                                const int32_t* __restrict__ vals,
-                                                               const int2* __restrict__ ranges, Win w, float bg0,
+                                                               const int2* __restrict__ ranges,
+                                                               const int32_t* __restrict__ tile_order, Win w, float bg0,
                                                                float bg1, float bg2, const float* __restrict__ fT_in,
                                                                const int32_t* __restrict__ last_in,
                                                                const float* __restrict__ d_img, float* partials) {
@@ -627,7 +715,7 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
   __shared__ float red[kBwdBatch][kBwdWarps][9];
   __shared__ unsigned long long wmask[kBwdWarps];
   __shared__ int smax;
-  const int tile = blockIdx.x;
+  const int tile = tile_of(tile_order);
   const int tx = tile % w.tw, ty = tile / w.tw;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lx = lane & 15, ly = warp * kBand + (lane >> 4);
@@ -1150,6 +1238,11 @@ void bin_phase(gss_render_ctx* ctx, const Win& w, int64_t V, cudaStream_t st) {
     }
   }
   ctx->I = I;
+  int32_t* order = static_cast<int32_t*>(ctx->tile_order.get((size_t)ntile * 4, st));
+  if (GSS_LPT) {
+    tile_order_kernel<<<1, kOrderThreads, 0, st>>>(ranges, ntile, order);
+    GSS_LAUNCHED();
+  }
 }
 
 // composite_phase: per-pixel compositing fused with the L1 loss (forward_kernel).
@@ -1170,7 +1263,8 @@ void composite_phase(gss_render_ctx* ctx, const Win& w, int64_t V, const FwdOut&
   double* lp = o.gt ? static_cast<double*>(ctx->lossp.get((size_t)ntile * 8, st)) : nullptr;
   forward_kernel<<<ntile, kTilePix, 0, st>>>(static_cast<const SplatRec*>(ctx->recs.p),
                                              static_cast<const int32_t*>(ctx->vals_a.p),
-                                             static_cast<const int2*>(ctx->ranges.p), w, s.bg[0], s.bg[1], s.bg[2],
+                                             static_cast<const int2*>(ctx->ranges.p),
+                                             static_cast<const int32_t*>(ctx->tile_order.p), w, s.bg[0], s.bg[1], s.bg[2],
                                              o.image, fT, last, o.ncontrib, o.gt, o.gt_width, o.inv, o.d_img, lp);
   GSS_LAUNCHED();
   if (o.gt) {
@@ -1219,7 +1313,8 @@ void per_slot_sums(gss_render_ctx* ctx, const float* d_img, float* sums, cudaStr
   {
     const int ntile = w.tw * w.th;
     backward_kernel<<<ntile, kBwdThreads, 0, st>>>(recs, static_cast<const int32_t*>(ctx->vals_a.p),
-                                                static_cast<const int2*>(ctx->ranges.p), w, ctx->sc.bg[0],
+                                                static_cast<const int2*>(ctx->ranges.p),
+                                                static_cast<const int32_t*>(ctx->tile_order.p), w, ctx->sc.bg[0],
                                                 ctx->sc.bg[1], ctx->sc.bg[2], static_cast<const float*>(ctx->fT.p),
                                                 static_cast<const int32_t*>(ctx->last.p), d_img, partials);
     GSS_LAUNCHED();
@@ -1471,7 +1566,7 @@ void render_ctx_destroy(gss_render_ctx* ctx) {
   if (!ctx) return;
   cudaStream_t st = ctx->last_stream;
   for (DBuf* b : {&ctx->recs, &ctx->ntiles, &ctx->offsets, &ctx->keys_a, &ctx->keys_b, &ctx->vals_a, &ctx->vals_b,
-                  &ctx->cub_tmp, &ctx->ranges, &ctx->last, &ctx->fT, &ctx->partials, &ctx->lossp, &ctx->hostcnt, &ctx->sums, &ctx->dkeys_a, &ctx->dkeys_b, &ctx->order_a, &ctx->order_b,
+                  &ctx->cub_tmp, &ctx->ranges, &ctx->tile_order, &ctx->last, &ctx->fT, &ctx->partials, &ctx->lossp, &ctx->hostcnt, &ctx->sums, &ctx->dkeys_a, &ctx->dkeys_b, &ctx->order_a, &ctx->order_b,
                   &ctx->slot_off})
     b->release(st);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
