@@ -667,26 +667,45 @@ __device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k
   return true;
 }
 
-// Warp reduce-scatter of 9 values (padded to 16): 16 shuffles instead of 9 x 5 butterflies.
-// Afterwards lane l holds the warp total of value index ((l>>4)&1)*8 + ((l>>3)&1)*4 +
-// ((l>>2)&1)*2 + ((l>>1)&1) (lanes 2k and 2k+1 hold the same total). Fixed order: deterministic.
+// Warp reduce-scatter of 9 values in 12 shuffles (9 x 5 butterflies would take 45; padding to 16
+// takes 16): the value set is halved per lane bit with minimal padding, 10 -> 5 -> 3 -> 2 -> 1
+// (bits 4, 3, 2, 1), then lanes 2k and 2k+1 add. Afterwards lane l holds the warp total of value
+// index reduce_scatter9_index(l) (-1: a padding slot). Fixed order: deterministic.
+__device__ __forceinline__ int reduce_scatter9_index(int lane) {
+  const int j3 = ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);  // of the 3-set (3 = padding)
+  const int j5 = ((lane >> 3) & 1) * 3 + j3;                   // of the 5-set (5.. = padding)
+  const int j10 = ((lane >> 4) & 1) * 5 + j5;                  // of the 10 values (9 = padding)
+  return (j3 < 3 && j5 < 5 && j10 < 9) ? j10 : -1;
+}
 __device__ __forceinline__ float warp_reduce_scatter9(const float v[9], int lane) {
-  float x[16];
+  float x[5];
+  {  // bit 4: 10 values -> 5
+    const bool up = (lane & 16) != 0;
 #pragma unroll
-  for (int i = 0; i < 9; ++i) x[i] = v[i];
-#pragma unroll
-  for (int i = 9; i < 16; ++i) x[i] = 0.0f;
-#pragma unroll
-  for (int o = 16, n = 16; o >= 2; o >>= 1, n >>= 1) {
-    const bool up = (lane & o) != 0;
-#pragma unroll
-    for (int i = 0; i < n / 2; ++i) {
-      const float send = up ? x[i] : x[i + n / 2];
-      const float keep = up ? x[i + n / 2] : x[i];
-      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    for (int i = 0; i < 5; ++i) {
+      const float lo = v[i], hi = i + 5 < 9 ? v[i + 5] : 0.0f;
+      x[i] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, 16);
     }
   }
-  return x[0] + __shfl_xor_sync(0xffffffffu, x[0], 1);
+  float y[3];
+  {  // bit 3: 5 values (+1 padding) -> 3
+    const bool up = (lane & 8) != 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const float lo = x[i], hi = i + 3 < 5 ? x[i + 3] : 0.0f;
+      y[i] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, 8);
+    }
+  }
+  float z[2];
+  {  // bit 2: 3 values (+1 padding) -> 2
+    const bool up = (lane & 4) != 0;
+    const float hi1 = 0.0f;
+    z[0] = (up ? y[2] : y[0]) + __shfl_xor_sync(0xffffffffu, up ? y[0] : y[2], 4);
+    z[1] = (up ? hi1 : y[1]) + __shfl_xor_sync(0xffffffffu, up ? y[1] : hi1, 4);
+  }
+  const bool up = (lane & 2) != 0;  // bit 1: 2 values -> 1
+  const float u = (up ? z[1] : z[0]) + __shfl_xor_sync(0xffffffffu, up ? z[0] : z[1], 2);
+  return u + __shfl_xor_sync(0xffffffffu, u, 1);
 }
 
 // Reverse sweep (render.hpp:542-589) per 16x16 tile: 128 threads, 2 pixels each (rows ly and
@@ -753,7 +772,7 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
   if (lane == 0 && wl > 0) atomicMax(&smax, wl);
   __syncthreads();
   const int Lmax = smax;
-  const int vidx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+  const int vidx = reduce_scatter9_index(lane);
   for (int bend = Lmax; bend > 0; bend -= kBwdBatch) {
     const int bstart = max(0, bend - kBwdBatch);
     const int nb = bend - bstart;
@@ -790,7 +809,7 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
       for (int h = 0; h < kBwdPPT; ++h) act |= bwd_contrib(r, k, bstart + jj, px[h], v);
       if (__any_sync(0xffffffffu, act)) {
         const float tot = warp_reduce_scatter9(v, lane);
-        if ((lane & 1) == 0 && vidx < 9) red[jj][warp][vidx] = tot;
+        if ((lane & 1) == 0 && vidx >= 0) red[jj][warp][vidx] = tot;
       } else if (lane < 9) {
         red[jj][warp][lane] = 0.0f;
       }
