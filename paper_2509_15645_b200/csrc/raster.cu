@@ -50,7 +50,11 @@ constexpr int kFwdBatch = 256;
 #else
 #define GSS_BWD_BOUNDS __launch_bounds__(kBwdThreads)
 #endif
-constexpr int kBwdBatch = 64;
+#ifndef GSS_BWD_BATCH
+#define GSS_BWD_BATCH 64
+#endif
+constexpr int kBwdBatch = GSS_BWD_BATCH;  // records per SMEM batch of the backward sweep
+constexpr int kBwdMasks = kBwdBatch / 64;  // 64-bit record masks per warp and batch
 
 struct __align__(16) SplatRec {
   float mx, my, a, b;
@@ -630,19 +634,22 @@ __device__ __forceinline__ float rcp_fast(float x) {
 // the 0.999 clamp decision, which selects the reference's branch (render.hpp:560-573), is
 // recomputed with the forward's exact arithmetic whenever the fast alpha is within 1e-4 of the
 // threshold, so both passes always take the same branch.
+// Predicated form: every lane evaluates the contribution and a lane whose pixel is outside the
+// record's box (or past its last index) adds exact zeros and keeps its state, so the two pixels of
+// a thread form one branch-free block the scheduler can interleave.
 __device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k, int jpos, PixB& p, float v[9]) {
-  if (!(jpos < p.L && p.x >= r.bx0 && p.x < r.bx1 && p.y >= r.by0 && p.y < r.by1)) return false;
+  const bool ok = (jpos < p.L) & (p.x >= r.bx0) & (p.x < r.bx1) & (p.y >= r.by0) & (p.y < r.by1);
   const float dx = p.cx - r.mx, dy = p.cy - r.my;
   const float mdxy2 = -2.0f * dx * dy;
   float q = __fmaf_rn(k.ia * dx, dx, __fmaf_rn(k.ic * dy, dy, k.ib * mdxy2));
-  q = q < 0.0f ? 0.0f : q;
+  q = (q < 0.0f || !ok) ? 0.0f : q;  // an idle lane evaluates at q = 0: every term stays finite
   const float weight = ex2_fast(-0.72134752f * q);  // exp(-q/2)
   float raw = r.ab * weight;
-  if (fabsf(raw - 0.999f) < 1e-4f) raw = contrib_eval(r, p.cx, p.cy).clamped ? 1.0f : 0.0f;
+  if (ok && fabsf(raw - 0.999f) < 1e-4f) raw = contrib_eval(r, p.cx, p.cy).clamped ? 1.0f : 0.0f;
   const bool clamped = raw > 0.999f;
-  const float alpha = clamped ? 0.999f : r.ab * weight;
+  const float alpha = ok ? (clamped ? 0.999f : r.ab * weight) : 0.0f;
   const float inv1m = rcp_fast(1.0f - alpha);
-  const float Tb = p.T * inv1m;  // transmittance before this contribution
+  const float Tb = ok ? p.T * inv1m : p.T;  // transmittance before this contribution
   const float w_rgb = alpha * Tb;
   v[0] = __fmaf_rn(w_rgb, p.g0, v[0]);
   v[1] = __fmaf_rn(w_rgb, p.g1, v[1]);
@@ -654,17 +661,16 @@ __device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k
   p.s1 = __fmaf_rn(r.g, w_rgb, p.s1);
   p.s2 = __fmaf_rn(r.bl, w_rgb, p.s2);
   p.T = Tb;
-  if (!clamped) {  // render.hpp:572-586
-    v[8] = __fmaf_rn(weight, d_alpha, v[8]);
-    const float dqi = alpha * d_alpha * k.nh;
-    const float b2 = 2.0f * r.b;
-    v[5] = __fmaf_rn(dqi, __fmaf_rn(-q, r.c, dy * dy), v[5]);
-    v[6] = __fmaf_rn(dqi, __fmaf_rn(q, b2, mdxy2), v[6]);
-    v[7] = __fmaf_rn(dqi, __fmaf_rn(-q, r.a, dx * dx), v[7]);
-    v[3] = __fmaf_rn(dqi, __fmaf_rn(b2, dy, -2.0f * r.c * dx), v[3]);
-    v[4] = __fmaf_rn(dqi, __fmaf_rn(b2, dx, -2.0f * r.a * dy), v[4]);
-  }
-  return true;
+  const float gsel = (ok && !clamped) ? 1.0f : 0.0f;  // render.hpp:572-586 only when not clamped
+  v[8] = __fmaf_rn(weight * gsel, d_alpha, v[8]);
+  const float dqi = alpha * d_alpha * k.nh * gsel;
+  const float b2 = 2.0f * r.b;
+  v[5] = __fmaf_rn(dqi, __fmaf_rn(-q, r.c, dy * dy), v[5]);
+  v[6] = __fmaf_rn(dqi, __fmaf_rn(q, b2, mdxy2), v[6]);
+  v[7] = __fmaf_rn(dqi, __fmaf_rn(-q, r.a, dx * dx), v[7]);
+  v[3] = __fmaf_rn(dqi, __fmaf_rn(b2, dy, -2.0f * r.c * dx), v[3]);
+  v[4] = __fmaf_rn(dqi, __fmaf_rn(b2, dx, -2.0f * r.a * dy), v[4]);
+  return ok;
 }
 
 // Warp reduce-scatter of 9 values in 12 shuffles (9 x 5 butterflies would take 45; padding to 16
@@ -728,11 +734,11 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
                                                                float bg1, float bg2, const float* __restrict__ fT_in,
                                                                const int32_t* __restrict__ last_in,
                                                                const float* __restrict__ d_img, float* partials) {
-  static_assert(kBwdBatch == 64, "one 64-bit record mask per warp");
+  static_assert(kBwdBatch % 64 == 0, "whole 64-bit record masks per warp");
   __shared__ SplatRec sh[kBwdBatch];
   __shared__ BwdConic shk[kBwdBatch];
   __shared__ float red[kBwdBatch][kBwdWarps][9];
-  __shared__ unsigned long long wmask[kBwdWarps];
+  __shared__ unsigned long long wmask[kBwdWarps][kBwdMasks];
   __shared__ int smax;
   const int tile = tile_of(tile_order);
   const int tx = tile % w.tw, ty = tile / w.tw;
@@ -784,7 +790,7 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
       shk[j] = BwdConic{r.c * inv, r.b * inv, r.a * inv, -0.5f * inv};
     }
     __syncthreads();
-    unsigned long long m = 0;
+    unsigned long long mk[kBwdMasks];
 #pragma unroll
     for (int h = 0; h < kBwdBatch / 32; ++h) {
       const int jl = h * 32 + lane;
@@ -793,25 +799,32 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
         const int4 bx = *reinterpret_cast<const int4*>(&sh[jl].bx0);
         hit = bx.x <= bx0w + 15 && bx.y > bx0w && bx.z <= by0w + kBand - 1 && bx.w > by0w;
       }
-      m |= (unsigned long long)__ballot_sync(0xffffffffu, hit) << (32 * h);
+      const unsigned long long bal = (unsigned long long)__ballot_sync(0xffffffffu, hit) << (32 * (h & 1));
+      mk[h >> 1] = (h & 1) ? (mk[h >> 1] | bal) : bal;
     }
-    if (lane == 0) wmask[warp] = m;
-    while (m) {
-      const int jj = 63 - __clzll(m);  // reverse order: back to front
-      m &= ~(1ull << jj);
-      const SplatRec r = sh[jj];
-      const BwdConic k = shk[jj];
-      float v[9];
+    if (lane == 0) {
 #pragma unroll
-      for (int i = 0; i < 9; ++i) v[i] = 0.0f;
-      bool act = false;
+      for (int h = 0; h < kBwdMasks; ++h) wmask[warp][h] = mk[h];
+    }
 #pragma unroll
-      for (int h = 0; h < kBwdPPT; ++h) act |= bwd_contrib(r, k, bstart + jj, px[h], v);
-      if (__any_sync(0xffffffffu, act)) {
-        const float tot = warp_reduce_scatter9(v, lane);
-        if ((lane & 1) == 0 && vidx >= 0) red[jj][warp][vidx] = tot;
-      } else if (lane < 9) {
-        red[jj][warp][lane] = 0.0f;
+    for (int h = kBwdMasks - 1; h >= 0; --h) {
+      for (unsigned long long m = mk[h]; m;) {
+        const int jj = h * 64 + 63 - __clzll(m);  // reverse order: back to front
+        m &= ~(1ull << (jj & 63));
+        const SplatRec r = sh[jj];
+        const BwdConic k = shk[jj];
+        float v[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) v[i] = 0.0f;
+        bool act = false;
+#pragma unroll
+        for (int q = 0; q < kBwdPPT; ++q) act |= bwd_contrib(r, k, bstart + jj, px[q], v);
+        if (__any_sync(0xffffffffu, act)) {
+          const float tot = warp_reduce_scatter9(v, lane);
+          if ((lane & 1) == 0 && vidx >= 0) red[jj][warp][vidx] = tot;
+        } else if (lane < 9) {
+          red[jj][warp][lane] = 0.0f;
+        }
       }
     }
     __syncthreads();
@@ -822,7 +835,7 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
       float s = 0.0f;
 #pragma unroll
       for (int q = 0; q < kBwdWarps; ++q)
-        if ((wmask[q] >> jj) & 1ull) s += red[jj][q][i];
+        if ((wmask[q][jj >> 6] >> (jj & 63)) & 1ull) s += red[jj][q][i];
       const SplatRec& r = sh[jj];
       int tx0, ty0, ntx, nty;
       tile_box(r, w, tx0, ty0, ntx, nty);
