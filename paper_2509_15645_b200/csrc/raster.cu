@@ -714,14 +714,14 @@ __device__ __forceinline__ float warp_reduce_scatter9(const float v[9], int lane
   return u + __shfl_xor_sync(0xffffffffu, u, 1);
 }
 
-// Reverse sweep (render.hpp:542-589) per 16x16 tile: 128 threads, 2 pixels each (rows ly and
-// ly + 2 of a 4-row warp band), so a splat's 9 gradient terms are pre-summed per lane and
-// reduced once per warp. Per batch, each warp ballots which records can reach its band (pixel
+// Reverse sweep (render.hpp:542-589) per 16x16 tile: 64 threads, 4 pixels each (rows ly, ly + 2,
+// ly + 4, ly + 6 of an 8-row warp band), so a splat's 9 gradient terms are pre-summed per lane
+// over 4 pixels (predicated, interleavable) and reduced once per warp. Per batch, each warp ballots which records can reach its band (pixel
 // box intersects the band and sweep position < the band's largest last-contribution index) and
 // walks only those. One partial SlotAcc per (splat, tile) instance, fixed-order sums (no float
 // atomics, deterministic). partial layout: [instance][9] = rgb3, m2d2, cov3, ab.
 #ifndef GSS_BWD_PPT
-#define GSS_BWD_PPT 2
+#define GSS_BWD_PPT 4
 #endif
 constexpr int kBwdPPT = GSS_BWD_PPT;              // pixels per thread
 constexpr int kBwdThreads = kTilePix / kBwdPPT;
