@@ -32,6 +32,14 @@ namespace gssd {
 constexpr int kTileSize = 16;
 constexpr int kTilePix = kTileSize * kTileSize;  // 256 threads per CTA
 constexpr int kFwdBatch = 256;
+// Forward composite: pixels per thread (a warp owns an 8 x (4 * kFwdPPT) pixel block).
+#ifndef GSS_FWD_PPT
+#define GSS_FWD_PPT 2
+#endif
+constexpr int kFwdPPT = GSS_FWD_PPT;
+constexpr int kFwdThreads = kTilePix / kFwdPPT;
+constexpr int kFwdWarps = kFwdThreads / 32;
+constexpr int kFwdBlockRows = 4 * kFwdPPT;
 // Minimum resident blocks per SM for the composite / sweep kernels (0 = no bound: the compiler
 // chooses the registers; the backward sweep then takes 78).
 #ifndef GSS_FWD_MINB
@@ -41,9 +49,9 @@ constexpr int kFwdBatch = 256;
 #define GSS_BWD_MINB 0
 #endif
 #if GSS_FWD_MINB > 0
-#define GSS_FWD_BOUNDS __launch_bounds__(kTilePix, GSS_FWD_MINB)
+#define GSS_FWD_BOUNDS __launch_bounds__(kFwdThreads, GSS_FWD_MINB)
 #else
-#define GSS_FWD_BOUNDS __launch_bounds__(kTilePix)
+#define GSS_FWD_BOUNDS __launch_bounds__(kFwdThreads)
 #endif
 #if GSS_BWD_MINB > 0
 #define GSS_BWD_BOUNDS __launch_bounds__(kBwdThreads, GSS_BWD_MINB)
@@ -441,7 +449,8 @@ __device__ __forceinline__ void load_rec(SplatRec* dst, const SplatRec* recs, in
 }
 
 // Forward composite (render.hpp:438-462) fused with the L1 loss (render.hpp:497-511).
-// Each warp owns an 8x4 pixel block of the 16x16 tile. After a batch of records is staged in
+// Each warp owns an 8 x 8 pixel block of the 16x16 tile (2 pixels per thread, rows 4 apart, so the
+// per-record SMEM loads and bookkeeping serve two pixels). After a batch of records is staged in
 // SMEM, the warp ballots which records' pixel boxes intersect its block and walks only those
 // (warp-uniform loop); the per-pixel box test then reproduces the CSR membership exactly.
 __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
@@ -453,33 +462,44 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
                                                            const float* gt, int gt_width, float inv_norm,
                                                            float* d_img, double* loss_partials) {
   __shared__ SplatRec sh[kFwdBatch];
-  __shared__ double red[kTilePix / 32];
+  __shared__ double red[kFwdWarps];
   const int tile = tile_of(tile_order);
   const int tx = tile % w.tw, ty = tile / w.tw;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 4;
+  const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * kFwdBlockRows;
   const int fx0 = w.px0 + tx * kTileSize + wx0, fy0 = w.py0 + ty * kTileSize + wy0;  // warp block origin
-  const int x = fx0 + (lane & 7), y = fy0 + (lane >> 3);
-  const bool inside = x < w.px0 + w.pw && y < w.py0 + w.ph;
-  const float cx = (float)x + 0.5f, cy = (float)y + 0.5f;
+  const int x = fx0 + (lane & 7);
+  const float cx = (float)x + 0.5f;
   const int2 rg = ranges[tile];
-  float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
-  int used = 0, last = 0;
-  bool done = !inside;
+  // Pixel h of this thread: row fy0 + (lane >> 3) + 4h of the warp's 8 x kFwdBlockRows block.
+  int y[kFwdPPT], used[kFwdPPT], last[kFwdPPT];
+  float cy[kFwdPPT], T[kFwdPPT], c0[kFwdPPT], c1[kFwdPPT], c2[kFwdPPT];
+  bool done[kFwdPPT];
+  bool all_done = true;
+#pragma unroll
+  for (int h = 0; h < kFwdPPT; ++h) {
+    y[h] = fy0 + (lane >> 3) + 4 * h;
+    cy[h] = (float)y[h] + 0.5f;
+    T[h] = 1.0f;
+    c0[h] = c1[h] = c2[h] = 0.0f;
+    used[h] = last[h] = 0;
+    done[h] = !(x < w.px0 + w.pw && y[h] < w.py0 + w.ph);
+    all_done &= done[h];
+  }
   for (int b = rg.x; b < rg.y; b += kFwdBatch) {
-    if (__syncthreads_count(done) == kTilePix) break;
+    if (__syncthreads_count(all_done) == kFwdThreads) break;
     const int nb = min(kFwdBatch, rg.y - b);
-    if ((int)threadIdx.x < nb) {
-      load_rec(&sh[threadIdx.x], recs, vals[b + threadIdx.x]);
-      sh[threadIdx.x].depth = det_rcp(sh[threadIdx.x].det);  // the SMEM copy's depth slot holds RN(1/det)
+    for (int t = threadIdx.x; t < nb; t += kFwdThreads) {
+      load_rec(&sh[t], recs, vals[b + t]);
+      sh[t].depth = det_rcp(sh[t].det);  // the SMEM copy's depth slot holds RN(1/det)
     }
     __syncthreads();
-    for (int c0j = 0; c0j < nb && __any_sync(0xffffffffu, !done); c0j += 32) {
+    for (int c0j = 0; c0j < nb && __any_sync(0xffffffffu, !all_done); c0j += 32) {
       const int jl = c0j + lane;
       bool hit = false;
       if (jl < nb) {
         const int4 bx = *reinterpret_cast<const int4*>(&sh[jl].bx0);
-        hit = bx.x <= fx0 + 7 && bx.y > fx0 && bx.z <= fy0 + 3 && bx.w > fy0;
+        hit = bx.x <= fx0 + 7 && bx.y > fx0 && bx.z <= fy0 + kFwdBlockRows - 1 && bx.w > fy0;
       }
       unsigned m = __ballot_sync(0xffffffffu, hit);
       while (m) {
@@ -487,34 +507,43 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
         m &= m - 1;
         const SplatRec& r = sh[j];
         const int4 bx = *reinterpret_cast<const int4*>(&r.bx0);
-        if (!(!done & (x >= bx.x) & (x < bx.y) & (y >= bx.z) & (y < bx.w))) continue;
-        if (T < 1e-4f) {
-          done = true;
-          continue;
+        const bool xin = (x >= bx.x) & (x < bx.y);
+#pragma unroll
+        for (int h = 0; h < kFwdPPT; ++h) {
+          if (!(!done[h] & xin & (y[h] >= bx.z) & (y[h] < bx.w))) continue;
+          if (T[h] < 1e-4f) {
+            done[h] = true;
+            continue;
+          }
+          const EvalOut ev = contrib_eval(r, cx, cy[h], r.depth);
+          c0[h] += r.r * ev.alpha * T[h];
+          c1[h] += r.g * ev.alpha * T[h];
+          c2[h] += r.bl * ev.alpha * T[h];
+          T[h] *= (1.0f - ev.alpha);
+          ++used[h];
+          last[h] = b + j - rg.x + 1;
         }
-        const EvalOut ev = contrib_eval(r, cx, cy, r.depth);
-        c0 += r.r * ev.alpha * T;
-        c1 += r.g * ev.alpha * T;
-        c2 += r.bl * ev.alpha * T;
-        T *= (1.0f - ev.alpha);
-        ++used;
-        last = b + j - rg.x + 1;
       }
+      all_done = true;
+#pragma unroll
+      for (int h = 0; h < kFwdPPT; ++h) all_done &= done[h];
     }
     __syncthreads();
   }
   double acc = 0.0;
-  if (inside) {
-    const int64_t pix = (int64_t)(y - w.py0) * w.pw + (x - w.px0);
-    const float o0 = c0 + T * bg0, o1 = c1 + T * bg1, o2 = c2 + T * bg2;
+#pragma unroll
+  for (int h = 0; h < kFwdPPT; ++h) {
+    if (!(x < w.px0 + w.pw && y[h] < w.py0 + w.ph)) continue;
+    const int64_t pix = (int64_t)(y[h] - w.py0) * w.pw + (x - w.px0);
+    const float o0 = c0[h] + T[h] * bg0, o1 = c1[h] + T[h] * bg1, o2 = c2[h] + T[h] * bg2;
     image[pix * 3 + 0] = o0;
     image[pix * 3 + 1] = o1;
     image[pix * 3 + 2] = o2;
-    fT_out[pix] = T;
-    last_out[pix] = last;
-    if (ncontrib_out) ncontrib_out[pix] = used;
+    fT_out[pix] = T[h];
+    last_out[pix] = last[h];
+    if (ncontrib_out) ncontrib_out[pix] = used[h];
     if (gt) {
-      const float* gp = gt + ((int64_t)y * gt_width + x) * 3;
+      const float* gp = gt + ((int64_t)y[h] * gt_width + x) * 3;
       const float o[3] = {o0, o1, o2};
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -530,7 +559,7 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
     __syncthreads();
     if (threadIdx.x == 0) {
       double s = 0.0;
-      for (int i = 0; i < kTilePix / 32; ++i) s += red[i];
+      for (int i = 0; i < kFwdWarps; ++i) s += red[i];
       loss_partials[tile] = s;
     }
   }
@@ -1293,7 +1322,7 @@ void composite_phase(gss_render_ctx* ctx, const Win& w, int64_t V, const FwdOut&
   }
   const int ntile = w.tw * w.th;
   double* lp = o.gt ? static_cast<double*>(ctx->lossp.get((size_t)ntile * 8, st)) : nullptr;
-  forward_kernel<<<ntile, kTilePix, 0, st>>>(static_cast<const SplatRec*>(ctx->recs.p),
+  forward_kernel<<<ntile, kFwdThreads, 0, st>>>(static_cast<const SplatRec*>(ctx->recs.p),
                                              static_cast<const int32_t*>(ctx->vals_a.p),
                                              static_cast<const int2*>(ctx->ranges.p),
                                              static_cast<const int32_t*>(ctx->tile_order.p), w, s.bg[0], s.bg[1], s.bg[2],
