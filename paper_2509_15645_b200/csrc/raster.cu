@@ -31,7 +31,10 @@ namespace gssd {
 
 constexpr int kTileSize = 16;
 constexpr int kTilePix = kTileSize * kTileSize;  // 256 threads per CTA
-constexpr int kFwdBatch = 256;
+#ifndef GSS_FWD_BATCH
+#define GSS_FWD_BATCH 256
+#endif
+constexpr int kFwdBatch = GSS_FWD_BATCH;
 // Forward composite: pixels per thread (a warp owns an 8 x (4 * kFwdPPT) pixel block).
 #ifndef GSS_FWD_PPT
 #define GSS_FWD_PPT 2
