@@ -649,9 +649,15 @@ bool vector_rows(const gss_arena& a) {
 // slot is a binary search in SMEM instead of a dependent search through global memory. Then the
 // flattened (id, column) walk reads the arena rows with consecutive lanes on consecutive columns.
 constexpr int kRestoreChunk = kUpdThreads;
+#ifndef GSS_RESTORE_MINB
+#define GSS_RESTORE_MINB 3
+#endif
+#ifndef GSS_RESTORE_KV
+#define GSS_RESTORE_KV 2
+#endif
 constexpr int kSeg = 2048;
 template <int K>
-__global__ void __launch_bounds__(kUpdThreads, 3) restore_kernel(ArenaDev a, const int32_t* ids, int64_t count,
+__global__ void __launch_bounds__(kUpdThreads, GSS_RESTORE_MINB) restore_kernel(ArenaDev a, const int32_t* ids, int64_t count,
                                                               const int64_t* count_dev, GradsDev pend,
                                                               const int32_t* pbstart, int has_pending,
                                                               const __grid_constant__ LutArgs<K> L, float* out,
@@ -725,7 +731,7 @@ __global__ void __launch_bounds__(kUpdThreads, 3) restore_kernel(ArenaDev a, con
       const int dq = 32 / nq, dr = 32 - dq * nq;
       const int64_t my_base = j < nk ? (int64_t)my_id * a.stride : -1;
       int r = lane / nq, q = lane - (lane / nq) * nq;
-      constexpr int kV = 2;
+      constexpr int kV = GSS_RESTORE_KV;  // 16-byte units of w, m and v in flight per lane
       for (int i0 = 0; i0 < nq; i0 += kV) {
         float4 w[kV], m[kV], v[kV];
         float gv[kV][4];
@@ -1080,6 +1086,111 @@ void adam_flush(gss_arena* ap, cudaStream_t st) {
     launch_update<256, kFlush>(a, GradsDev{}, t, nullptr, nullptr, st);
 }
 
+// Split restore_view for row-interleaved arenas: a resolve pass turns each visible id into its
+// (pending slot, delay) once — the counter byte and a binary search of the pending ids within the
+// id's 1024-row block (index bstart) — and the walk pass then streams the rows with no barriers or
+// per-chunk prologue, each warp 32 ids at a time in 16-byte units (as walk4_kernel).
+#ifndef GSS_RESTORE_SPLIT
+#define GSS_RESTORE_SPLIT 1
+#endif
+__global__ void restore_resolve_kernel(ArenaDev a, const int32_t* ids, int64_t count, const int64_t* count_dev,
+                                       GradsDev pend, const int32_t* pbstart, int2* res) {
+  const int64_t cnt = count_dev ? *count_dev : count;
+  const int64_t pcnt = pend.ids ? grads_count(pend) : 0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < cnt; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t id = ids[k];
+    int32_t slot = -1;
+    if (pcnt > 0) {
+      const int64_t b = id / kRowsPerBlock;
+      int64_t lo = pbstart[b], hi = pbstart[b + 1];
+      lo = lo < 0 ? 0 : lo;
+      hi = hi > pcnt ? pcnt : hi;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (pend.ids[mid] < id) lo = mid + 1; else hi = mid;
+      }
+      if (lo < pcnt && pend.ids[lo] == id) slot = (int32_t)lo;
+    }
+    res[k] = make_int2(slot, (int)a.counter[id]);
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kUpdThreads, GSS_RESTORE_MINB) restore_walk_kernel(
+    ArenaDev a, const int32_t* ids, int64_t count, const int64_t* count_dev, GradsDev pend, const int2* res,
+    int has_pending, const __grid_constant__ LutArgs<K> L, float* out) {
+  __shared__ PackedLuts<K> lut;
+  load_packed_luts<K>(lut, L, a.dim);
+  __syncthreads();
+  const int64_t cnt = count_dev ? *count_dev : count;
+  const int dim = a.dim;
+  const int lane = threadIdx.x & 31;
+  const int nq = (dim + 3) >> 2;
+  const int dq = 32 / nq, dr = 32 - dq * nq;
+  const int64_t warps = (int64_t)gridDim.x * (kUpdThreads / 32);
+  for (int64_t k0 = (blockIdx.x * (int64_t)(kUpdThreads / 32) + (threadIdx.x >> 5)) * 32; k0 < cnt; k0 += warps * 32) {
+    const int64_t j = k0 + lane;
+    int64_t my_base = -1;
+    int2 my_res = make_int2(-1, 0);
+    if (j < cnt) {
+      my_base = (int64_t)ids[j] * a.stride;
+      my_res = res[j];
+    }
+    int r = lane / nq, q = lane - (lane / nq) * nq;
+    constexpr int kV = GSS_RESTORE_KV;
+    for (int i0 = 0; i0 < nq; i0 += kV) {
+      float4 w[kV], m[kV], v[kV];
+      float gv[kV][4];
+      int dd[kV], c0[kV], rr4[kV];
+      bool ok[kV];
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        const int rr = r < 32 ? r : 31;
+        const int64_t base = __shfl_sync(0xffffffffu, my_base, rr);
+        const int32_t sl = has_pending ? __shfl_sync(0xffffffffu, my_res.x, rr) : -1;
+        dd[u] = __shfl_sync(0xffffffffu, my_res.y, rr);
+        c0[u] = 4 * q;
+        rr4[u] = rr;
+        ok[u] = i0 + u < nq && base >= 0;
+        const int64_t o = ok[u] ? base + c0[u] : 0;
+        w[u] = ok[u] ? ld4(a.w + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+        m[u] = ok[u] ? ld4(a.m + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[u] = ok[u] ? ld4(a.v + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float* prow = pend.rows + (int64_t)sl * pend.stride + pend.col0 + c0[u];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) gv[u][i] = (ok[u] && sl >= 0 && c0[u] + i < dim) ? prow[i] : 0.0f;
+        r += dq;
+        q += dr;
+        if (q >= nq) {
+          q -= nq;
+          ++r;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        if (!ok[u]) continue;
+        float* orow = out + (size_t)(k0 + rr4[u]) * dim + c0[u];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (c0[u] + i >= dim) break;
+          const int g = lut.col_group[c0[u] + i];
+          const float4 gd = lut.gd[g][dd[u]];
+          float ww = at(w[u], i);
+          if (has_pending) {
+            float mm = at(m[u], i), vv = at(v[u], i);
+            deferred_scalar_fast(ww, mm, vv, gv[u][i], gd, lut.sc[g], lut.eps[g]);
+          } else {
+            const float num = gd.x * at(m[u], i);
+            ww = (num == 0.0f && at(v[u], i) >= 0.0f) ? ww - num
+                                                      : ww - div_rn(num, sqrt_rn(at(v[u], i)) + lut.eps[g]);
+          }
+          orow[i] = ww;
+        }
+      }
+    }
+  }
+}
+
 void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const int64_t* count_dev,
                   const gss_sparse_grads* pending, float* out, cudaStream_t st) {
   require(ap != nullptr, "arena: null");
@@ -1096,12 +1207,23 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
   const int64_t cap = count_dev ? std::max<int64_t>(count, a.n) : count;
   int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kRestoreChunk), (int64_t)sms * 64));
   if (host_resident(a)) blocks = std::min(blocks, kHostTierBlocks);
+  const size_t pb_bytes = ((size_t)(ceil_div(a.n, kRowsPerBlock) + 1) * 4 + 255) / 256 * 256;
+  const bool split = GSS_RESTORE_SPLIT && vector_rows(a) && a.defer_max < 16 && !host_resident(a);
+  char* scr = arena_scratch(a, 1, pb_bytes + (split ? (size_t)std::max<int64_t>(cap, 1) * sizeof(int2) : 0), st);
   int32_t* pbstart = nullptr;
-  if (pending && pd.ids)
-    pbstart = build_index(a, pd, err_flag_for(a),
-                          reinterpret_cast<int32_t*>(arena_scratch(a, 1, (size_t)(ceil_div(a.n, kRowsPerBlock) + 1) * 4, st)),
-                          st);
-  if (a.defer_max < 16) {
+  if (pending && pd.ids) pbstart = build_index(a, pd, err_flag_for(a), reinterpret_cast<int32_t*>(scr), st);
+  if (split) {
+    int2* res = reinterpret_cast<int2*>(scr + pb_bytes);
+    auto L = std::make_unique<LutArgs<16>>();
+    std::memset(L.get(), 0, sizeof(LutArgs<16>));
+    fill_luts<16>(a, t, false, *L);
+    const int rb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, 256), (int64_t)sms * 16));
+    restore_resolve_kernel<<<rb, 256, 0, st>>>(arena_dev(a), ids, count, count_dev, pd, pbstart, res);
+    GSS_LAUNCHED();
+    const int wb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kUpdThreads), (int64_t)sms * GSS_RESTORE_MINB));
+    restore_walk_kernel<16><<<wb, kUpdThreads, 0, st>>>(arena_dev(a), ids, count, count_dev, pd, res, pending ? 1 : 0,
+                                                         *L, out);
+  } else if (a.defer_max < 16) {
     auto L = std::make_unique<LutArgs<16>>();
     std::memset(L.get(), 0, sizeof(LutArgs<16>));
     fill_luts<16>(a, t, false, *L);
