@@ -79,13 +79,49 @@ def training_start(truth: np.ndarray) -> np.ndarray:
 
 
 class Clocks:
-    """nvidia-smi sampler running only during the timed region."""
+    """SM clock / throttle-reason sampler running only during the timed region: NVML polled every
+    5 ms from a thread (the timed regions are ~0.1 s, too short for nvidia-smi's process start and
+    100 ms period), with nvidia-smi as the fallback when NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NVML_REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                    "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
+        self.p = self.t = None
+        self.samples, self.reasons, self.mx = [], set(), 0.0
+        try:
+            import threading
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                ent = vis.split(",")[index].strip()
+                h = nv.nvmlDeviceGetHandleByUUID(ent) if ent.startswith("GPU-") else nv.nvmlDeviceGetHandleByIndex(int(ent))
+            else:
+                h = nv.nvmlDeviceGetHandleByIndex(index)
+            self.mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.stop_ev = threading.Event()
+            first = threading.Event()
+
+            def run():
+                while not self.stop_ev.is_set():
+                    self.samples.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for nm, bit in self.NVML_REASONS.items():
+                        if r & bit:
+                            self.reasons.add(nm)
+                    first.set()
+                    time.sleep(0.005)
+
+            self.t = threading.Thread(target=run, daemon=True)
+            self.t.start()
+            first.wait(1.0)
+            return
+        except Exception:
+            self.t = None
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
@@ -95,6 +131,13 @@ class Clocks:
             self.p = None
 
     def stop(self):
+        if self.t is not None:
+            self.stop_ev.set()
+            self.t.join()
+            if not self.samples:
+                return None
+            return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.mx,
+                    "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
         if self.p is None:
             return None
         self.p.terminate()
@@ -117,7 +160,8 @@ class Clocks:
         os.unlink(self.f.name)
         if not sm:
             return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvidia-smi"}
 
 
 def peaks():
