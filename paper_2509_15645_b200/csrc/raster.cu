@@ -838,11 +838,32 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
 #pragma unroll
       for (int h = 0; h < kBwdMasks; ++h) wmask[warp][h] = mk[h];
     }
+#if GSS_BWD_BATCH == 64
+    // One 64-record batch walked as two 32-bit halves (32-bit find-last-set on the uniform
+    // datapath instead of 64-bit arithmetic per record): high half first, back to front.
+    {
+      const unsigned ml = (unsigned)mk[0];
+      unsigned m = (unsigned)(mk[0] >> 32);
+      int hb = 32;
+      if (m == 0) {
+        m = ml;
+        hb = 0;
+      }
+      while (m) {
+        const int bit = 31 - __clz(m);
+        const int jj = hb + bit;
+        m ^= 1u << bit;
+        if (m == 0 && hb == 32) {
+          m = ml;
+          hb = 0;
+        }
+#else
 #pragma unroll
     for (int h = kBwdMasks - 1; h >= 0; --h) {
       for (unsigned long long m = mk[h]; m;) {
         const int jj = h * 64 + 63 - __clzll(m);  // reverse order: back to front
         m &= ~(1ull << (jj & 63));
+#endif
         const SplatRec r = sh[jj];
         const BwdConic k = shk[jj];
         float v[9];
