@@ -769,6 +769,7 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
   static_assert(kBwdBatch % 64 == 0, "whole 64-bit record masks per warp");
   __shared__ SplatRec sh[kBwdBatch];
   __shared__ BwdConic shk[kBwdBatch];
+  __shared__ int32_t sinst[kBwdBatch];  // the record's (splat, this tile) instance index
   __shared__ float red[kBwdBatch][kBwdWarps][9];
   __shared__ unsigned long long wmask[kBwdWarps][kBwdMasks];
   __shared__ int smax;
@@ -820,6 +821,9 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
       const SplatRec& r = sh[j];
       const float inv = 1.0f / r.det;  // det > 0 for every binned splat
       shk[j] = BwdConic{r.c * inv, r.b * inv, r.a * inv, -0.5f * inv};
+      int tx0, ty0, ntx, nty;
+      tile_box(r, w, tx0, ty0, ntx, nty);
+      sinst[j] = r.off + (ty - ty0) * ntx + (tx - tx0);
     }
     __syncthreads();
     unsigned long long mk[kBwdMasks];
@@ -889,11 +893,7 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
 #pragma unroll
       for (int q = 0; q < kBwdWarps; ++q)
         if ((wmask[q][jj >> 6] >> (jj & 63)) & 1ull) s += red[jj][q][i];
-      const SplatRec& r = sh[jj];
-      int tx0, ty0, ntx, nty;
-      tile_box(r, w, tx0, ty0, ntx, nty);
-      const int64_t inst = (int64_t)r.off + (int64_t)(ty - ty0) * ntx + (tx - tx0);
-      partials[inst * 9 + i] = s;
+      partials[(int64_t)sinst[jj] * 9 + i] = s;
     }
   }
 }
