@@ -873,15 +873,11 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
         float v[9];
 #pragma unroll
         for (int i = 0; i < 9; ++i) v[i] = 0.0f;
-        bool act = false;
 #pragma unroll
-        for (int q = 0; q < kBwdPPT; ++q) act |= bwd_contrib(r, k, bstart + jj, px[q], v);
-        if (__any_sync(0xffffffffu, act)) {
-          const float tot = warp_reduce_scatter9(v, lane);
-          if ((lane & 1) == 0 && vidx >= 0) red[jj][warp][vidx] = tot;
-        } else if (lane < 9) {
-          red[jj][warp][lane] = 0.0f;
-        }
+        for (int q = 0; q < kBwdPPT; ++q) bwd_contrib(r, k, bstart + jj, px[q], v);
+        // A record no lane contributed to reduces exact zeros: the same partial without a vote.
+        const float tot = warp_reduce_scatter9(v, lane);
+        if ((lane & 1) == 0 && vidx >= 0) red[jj][warp][vidx] = tot;
       }
     }
     __syncthreads();
