@@ -30,7 +30,7 @@
 namespace gssd {
 
 constexpr int kTileSize = 16;
-constexpr int kTilePix = kTileSize * kTileSize;  // 256 threads per CTA
+constexpr int kTilePix = kTileSize * kTileSize;  // pixels per tile
 #ifndef GSS_FWD_BATCH
 #define GSS_FWD_BATCH 256
 #endif
