@@ -336,12 +336,33 @@ struct SortedCount {
   __host__ __device__ int32_t operator()(int32_t i) const { return i < V ? nt[order[i]] : 0; }
 };
 
+// Tile ranges of the sorted instance keys: thread t owns keys [4t, 4t + 4) (one 16-byte load; the
+// neighbours across the thread boundary come from the adjacent lanes, the warp edges from memory).
 __global__ void ranges_kernel(const uint32_t* keys, int64_t I, int2* ranges) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= I) return;
-  const uint32_t tile = keys[i];
-  if (i == 0 || keys[i - 1] != tile) ranges[tile].x = (int)i;
-  if (i == I - 1 || keys[i + 1] != tile) ranges[tile].y = (int)(i + 1);
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t i0 = 4 * t;
+  const int lane = threadIdx.x & 31;
+  uint32_t k[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+  if (i0 + 3 < I) {
+    const uint4 q = *reinterpret_cast<const uint4*>(keys + i0);
+    k[0] = q.x; k[1] = q.y; k[2] = q.z; k[3] = q.w;
+  } else {
+    for (int j = 0; j < 4; ++j)
+      if (i0 + j < I) k[j] = keys[i0 + j];
+  }
+  uint32_t prev = __shfl_up_sync(0xffffffffu, k[3], 1);
+  uint32_t next = __shfl_down_sync(0xffffffffu, k[0], 1);
+  if (lane == 0 && i0 > 0 && i0 - 1 < I) prev = keys[i0 - 1];
+  if (lane == 31 && i0 + 4 < I) next = keys[i0 + 4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t i = i0 + j;
+    if (i >= I) break;
+    const uint32_t before = j == 0 ? prev : k[j - 1];
+    const uint32_t after = j == 3 ? next : k[j + 1];
+    if (i == 0 || before != k[j]) ranges[k[j]].x = (int)i;
+    if (i == I - 1 || after != k[j]) ranges[k[j]].y = (int)(i + 1);
+  }
 }
 
 // Launch order of the tile CTAs: heaviest tiles first (longest-processing-time-first), so the
@@ -1313,7 +1334,7 @@ void bin_phase(gss_render_ctx* ctx, const Win& w, int64_t V, cudaStream_t st) {
       // keep the sorted arrays addressable (vals_a) for composite and backward
       if (dk.Current() != ka) std::swap(ctx->keys_a, ctx->keys_b);
       if (dv.Current() != va) std::swap(ctx->vals_a, ctx->vals_b);
-      ranges_kernel<<<(unsigned)ceil_div(I, 256), 256, 0, st>>>(static_cast<const uint32_t*>(ctx->keys_a.p), I,
+      ranges_kernel<<<(unsigned)ceil_div(ceil_div(I, 4), 256), 256, 0, st>>>(static_cast<const uint32_t*>(ctx->keys_a.p), I,
                                                                 ranges);
       GSS_LAUNCHED();
     }
