@@ -626,10 +626,36 @@ def ref_gts(O, truth, cam_arr, a):
         np.zeros((len(cam_arr), a.height, a.width, 3), np.float32)
 
 
+def spawn_ranks(a) -> int:
+    """`--gpus N` (N > 1) without a torchrun environment: launch N ranks of this script on this
+    node through torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1), or fail
+    loudly when fewer than N GPUs are visible — never silently run one rank."""
+    import socket
+
+    if a.impl == "ours":
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < a.gpus:
+            sys.stderr.write(f"bench.py: --gpus {a.gpus} requested but only {have} CUDA device(s) visible\n")
+            return 1
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     a = parse()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        sys.exit(spawn_ranks(a))
+    if world != a.gpus and "WORLD_SIZE" in os.environ:
+        sys.stderr.write(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(1)
     if world > 1:
         import torch.distributed as dist
 

@@ -95,6 +95,9 @@ int gss_expf_device(const float* x, float* y, int64_t n, gss_stream_t stream);
  * before its first use; every call leaves it ready for the next one (no per-call memset). One
  * workspace must not be used by two calls in flight at the same time. */
 size_t gss_cull_workspace_bytes(int64_t n);
+/* Forgets the host-side epoch of a workspace about to be freed (its look-back states are then
+ * never compared again); call after its last gss_cull has been enqueued. */
+void gss_cull_workspace_release(const void* workspace);
 /* ids_out: capacity n, receives the kept ids ascending (bit-exact with frustum_cull);
  * mask_opt: optional bit mask, ceil(n/32) words, bit i of word i/32 = kept(i);
  * count_dev: device int64 receiving the kept count. geo rows are read with `stride` floats per
@@ -127,6 +130,11 @@ int gss_flush_deferred(gss_arena* arena, gss_stream_t stream);
  * returns GSS_ERR_INVARIANT if grad ids were unsorted/out of range (adam.hpp:231) or a
  * counter exceeded defer_max (adam.hpp:154-158). Synchronises the stream. */
 int gss_arena_check(const gss_arena* arena, gss_stream_t stream);
+/* Releases the library's per-arena scratch and sticky error flag (both keyed by arena->counter);
+ * call before freeing an arena's buffers. Lifetime: the scratch and the flag are created by the
+ * first gss_deferred_update / gss_restore_view / gss_arena_check on the arena and live until this
+ * call (synchronises the device). */
+int gss_arena_release(const gss_arena* arena);
 
 /* ---- rasterizer (render.hpp:361-640) ---------------------------------------------------- */
 /* A render context is the device-side RenderResult (render.hpp:284-289): it owns the splat

@@ -137,6 +137,8 @@ SIGNATURES = {
     "gss_restore_view": (C.c_int, [C.POINTER(GssArena), P, I64, P, C.POINTER(GssSparseGrads), P, P]),
     "gss_flush_deferred": (C.c_int, [C.POINTER(GssArena), P]),
     "gss_arena_check": (C.c_int, [C.POINTER(GssArena), P]),
+    "gss_arena_release": (C.c_int, [C.POINTER(GssArena)]),
+    "gss_cull_workspace_release": (None, [P]),
     "gss_render_ctx_create": (P, []),
     "gss_render_ctx_destroy": (None, [P]),
     "gss_rasterize_forward": (C.c_int, [P, C.POINTER(GssRenderScene), C.POINTER(GssCamera),

@@ -23,6 +23,8 @@ void adam_flush(gss_arena* ap, cudaStream_t st);
 void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const int64_t* count_dev,
                   const gss_sparse_grads* pending, float* out, cudaStream_t st);
 int arena_check(const gss_arena* ap, cudaStream_t st);
+void arena_release(const gss_arena* ap);
+void cull_workspace_release(const void* ws);
 // raster.cu
 gss_render_ctx* render_ctx_create();
 void render_ctx_destroy(gss_render_ctx* ctx);
@@ -96,6 +98,32 @@ void require_device() {
   }
 }
 }  // namespace
+
+constexpr int kMaxDevices = 64;
+std::atomic<int> g_sms[kMaxDevices];
+
+int sm_count() {
+  int dev = 0;
+  GSS_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) {
+    int sms = 0;
+    GSS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    return sms;
+  }
+  int sms = g_sms[dev].load(std::memory_order_relaxed);
+  if (sms == 0) {
+    GSS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    g_sms[dev].store(sms, std::memory_order_relaxed);
+  }
+  return sms;
+}
+
+void set_max_dynamic_smem(const void* fn, int bytes) {
+  cudaFuncAttributes fa{};
+  GSS_CUDA(cudaFuncGetAttributes(&fa, fn));
+  if (fa.maxDynamicSharedSizeBytes < bytes)
+    GSS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
 
 void set_error(const std::string& msg) { t_err = msg; }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -185,6 +213,12 @@ GSS_API int gss_arena_check(const gss_arena* arena, gss_stream_t stream) {
     arena_check(arena, as_stream(stream));
   });
 }
+
+GSS_API int gss_arena_release(const gss_arena* arena) {
+  return guarded([&] { arena_release(arena); });
+}
+
+GSS_API void gss_cull_workspace_release(const void* workspace) { cull_workspace_release(workspace); }
 
 GSS_API gss_render_ctx* gss_render_ctx_create(void) {
   gss_render_ctx* c = nullptr;

@@ -875,15 +875,6 @@ GradsDev grads_dev(const gss_sparse_grads* g) {
 // Per-arena device error flag (keyed by the counter buffer), allocated lazily.
 int* err_flag_for(const gss_arena& a);
 
-int sm_count() {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    GSS_CUDA(cudaGetDevice(&dev));
-    GSS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
-  return sms;
-}
 
 // Per-arena scratch (keyed by the counter buffer, like the error flag), grown on demand from the
 // stream-ordered pool and kept: a pass allocates and frees nothing. Slot 0 serves the update passes
@@ -1237,6 +1228,30 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
                                                         pending ? 1 : 0, *L, out, vector_rows(a) ? 1 : 0);
   }
   GSS_LAUNCHED();
+}
+
+// Frees the per-arena scratch and error flag (keyed by the counter buffer). Called when an arena's
+// buffers are released, so a later arena at a recycled address starts with a clean flag and the
+// maps stay bounded by the live arenas.
+void arena_release(const gss_arena* ap) {
+  if (!ap || !ap->counter) return;
+  GSS_CUDA(cudaDeviceSynchronize());
+  {
+    std::lock_guard<std::mutex> lk(g_scr_mu);
+    for (auto& m : g_scr) {
+      auto it = m.find(ap->counter);
+      if (it != m.end()) {
+        if (it->second.first) GSS_CUDA(cudaFree(it->second.first));
+        m.erase(it);
+      }
+    }
+  }
+  std::lock_guard<std::mutex> lk(g_flag_mu);
+  auto it = g_flags.find(ap->counter);
+  if (it != g_flags.end()) {
+    GSS_CUDA(cudaFree(it->second));
+    g_flags.erase(it);
+  }
 }
 
 int arena_check(const gss_arena* ap, cudaStream_t st) {

@@ -41,6 +41,13 @@ int64_t launches();
 
 inline cudaStream_t as_stream(gss_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// SM count of the calling thread's current device (cached per device ordinal, thread-safe).
+int sm_count();
+// Raises kernel `fn`'s dynamic shared-memory limit to `bytes` on the current device. The
+// attribute belongs to the device context, so it is applied once per device (and again after
+// a cudaDeviceReset, which the cache detects through the attribute query).
+void set_max_dynamic_smem(const void* fn, int bytes);
+
 // Runs `fn`, mapping exceptions to C-ABI status codes.
 template <class Fn> int guarded(Fn&& fn) {
   try {

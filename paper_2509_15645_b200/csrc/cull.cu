@@ -367,15 +367,6 @@ __global__ void expf_kernel(const float* x, float* y, int64_t n) {
 // Per-workspace epoch (host side): look-back states of earlier calls never match the current one.
 std::mutex g_epoch_mu;
 std::unordered_map<const void*, unsigned> g_epochs;
-int sm_count() {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    GSS_CUDA(cudaGetDevice(&dev));
-    GSS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
-  return sms;
-}
 
 unsigned next_epoch(const void* ws) {
   std::lock_guard<std::mutex> lk(g_epoch_mu);
@@ -387,6 +378,11 @@ unsigned next_epoch(const void* ws) {
 
 
 }  // namespace
+
+void cull_workspace_release(const void* ws) {
+  std::lock_guard<std::mutex> lk(g_epoch_mu);
+  g_epochs.erase(ws);
+}
 
 size_t cull_workspace_bytes(int64_t n) {
   const int64_t ntiles = ceil_div(n > 0 ? n : 1, kTile);
@@ -438,11 +434,7 @@ void cull(const float* geo, int64_t n, int64_t stride, const gss_camera* cam, co
   const bool tma = stride == kGeo && (reinterpret_cast<uintptr_t>(geo) % 16 == 0);
   if (tma) {
     const size_t smem = (size_t)kStages * kTileBytes;
-    static bool attr = false;
-    if (!attr) {
-      GSS_CUDA(cudaFuncSetAttribute(cull_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
+    set_max_dynamic_smem(reinterpret_cast<const void*>(cull_kernel<true>), (int)smem);
     cull_kernel<true><<<grid, kThreads, smem, st>>>(a);
   } else {
     cull_kernel<false><<<grid, kThreads, (size_t)kTileBytes, st>>>(a);

@@ -45,6 +45,7 @@ void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int6
                         int64_t nstride, float* mean2d, cudaStream_t st);
 void render_ctx_destroy(gss_render_ctx* ctx);
 gss_render_ctx* render_ctx_create();
+void arena_release(const gss_arena* ap);
 }  // namespace gssd
 
 struct gss_render_ctx;
@@ -550,6 +551,11 @@ gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss
 void engine_destroy(gss_engine* e) {
   if (!e) return;
   cudaDeviceSynchronize();
+  try {
+    arena_release(&e->geo);
+    arena_release(&e->ng);
+  } catch (...) {
+  }
   auto f = [](void* p) { if (p) cudaFree(p); };
   f(e->gts_dev); f(e->gw); f(e->gm); f(e->gv); f(e->gcnt);
   if (e->ng_host) {
@@ -749,6 +755,8 @@ void engine_densify(gss_engine* e, const gss_densify_config* dc, double extent, 
   cudaFree(rows);
   cudaFree(surv);
   cudaFree(children);
+  arena_release(&e->geo);
+  arena_release(&e->ng);
   cudaFree(e->gw); cudaFree(e->gm); cudaFree(e->gv); cudaFree(e->gcnt);
   if (e->ng_host) {
     cudaFreeHost(e->nw); cudaFreeHost(e->ncnt);

@@ -2,10 +2,11 @@
 
 Partition: Gaussians and all their optimizer state by contiguous id range, so
 cull and both Adam passes are shard-local (no communication), and concatenating the per-shard
-ascending id lists in shard order reproduces the global cull list bit-exactly. Round 1 runs the
-shards as independent weak-scaling units (each rank trains its own scene shard; timing is the max
-over ranks); the image-parallel exchange of splat records / screen-space gradients is the next
-multi-GPU step.
+ascending id lists in shard order reproduces the global cull list bit-exactly. The image-parallel
+exchange of splat records / screen-space gradients (two all-to-allv per view) lives in imgpar.py;
+bench.py's N>1 default runs it (`--mode imgpar`), `--mode replicas` runs N independent engines
+(weak-scaling replicas, no collective). Only the gloo path and N=1 NCCL have run so far; no
+multi-GPU NCCL measurement exists.
 """
 from __future__ import annotations
 

@@ -92,14 +92,23 @@ def frustum_cull(geo: torch.Tensor, count: int, cam: GssCamera, vp: GssViewport,
     assert geo.is_cuda and geo.dtype == torch.float32
     stride = stride if stride is not None else (geo.shape[1] if geo.dim() == 2 else K_GEO_DIM)
     dev = geo.device
-    ids = torch.empty(max(count, 1), dtype=torch.int32, device=dev)
-    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-    ws = torch.zeros(cull_workspace_bytes(count), dtype=torch.uint8, device=dev)
-    mask = torch.empty(max((count + 31) // 32, 1), dtype=torch.int32, device=dev) if want_mask else None
-    check(lib().gss_cull(_ptr(geo), int(count), int(stride), C.byref(cam), C.byref(vp), float(low_pass), _ptr(mask),
-                         _ptr(ids), _ptr(cnt), _ptr(ws), ws.numel(), _stream(stream)))
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    if st != torch.cuda.current_stream(dev):
+        st.wait_stream(torch.cuda.current_stream(dev))  # geo written on the caller's stream
+    # Outputs and the zero-filled workspace are allocated (and zeroed) on the launch stream, so the
+    # caching allocator orders their reuse after the cull.
+    with torch.cuda.stream(st):
+        ids = torch.empty(max(count, 1), dtype=torch.int32, device=dev)
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        ws = torch.zeros(cull_workspace_bytes(count), dtype=torch.uint8, device=dev)
+        mask = torch.empty(max((count + 31) // 32, 1), dtype=torch.int32, device=dev) if want_mask else None
+        check(lib().gss_cull(_ptr(geo), int(count), int(stride), C.byref(cam), C.byref(vp), float(low_pass),
+                             _ptr(mask), _ptr(ids), _ptr(cnt), _ptr(ws), ws.numel(), st.cuda_stream))
+        lib().gss_cull_workspace_release(_ptr(ws))
+    geo.record_stream(st)
     if not sync:
         return ids, cnt, mask
+    st.synchronize()
     v = int(cnt.item())
     ids = ids[:v]
     return (ids, mask) if want_mask else ids
@@ -186,6 +195,17 @@ class Arena:
             self.v = torch.zeros((n, dim), dtype=torch.float32, device=dev)
         self.counter = torch.zeros(max(n, 1), dtype=torch.uint8, device=dev)[:n]
         self.step = 0
+
+    def __del__(self):
+        # the library's scratch + sticky error flag for this arena (keyed by the counter buffer)
+        c = getattr(self, "counter", None)
+        if c is not None:
+            try:
+                a = GssArena()
+                a.counter = _ptr(c)
+                lib().gss_arena_release(C.byref(a))
+            except Exception:
+                pass
 
     def c_struct(self) -> GssArena:
         a = GssArena()
@@ -683,6 +703,9 @@ class OffloadEngine:
         loss = C.c_float(0)
         valid = C.c_int32(0)
         gt = gt_host if isinstance(gt_host, np.ndarray) else gt_host.numpy()
+        gt = np.ascontiguousarray(gt, dtype=np.float32)
+        if gt.size != cam.width * cam.height * 3:
+            raise ConfigError(2, "step: gt_host must hold height*width*3 floats")
         check(lib().gss_engine_step(self.h, C.byref(cam), gt.ctypes.data, C.byref(loss), C.byref(valid)))
         return float(loss.value), int(valid.value)
 

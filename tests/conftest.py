@@ -48,3 +48,33 @@ def orc():
     if o is None:
         pytest.skip("oracle/_ref/libgss_oracle.so not built (make -C oracle oracle)")
     return o
+
+
+@pytest.fixture(scope="session")
+def parity_log():
+    """Records measured deviations per test (max rel_err / rel_err_floor / abs) into the JSON file
+    named by GSS_PARITY_OUT (default gpurun_out/parity.json when that directory exists), so the
+    numbers behind the tolerances are committed (profiles/parity_r02.json), not just the dots."""
+    import json
+    import os
+
+    path = os.environ.get("GSS_PARITY_OUT")
+    if path is None and (ROOT / "gpurun_out").is_dir():
+        path = str(ROOT / "gpurun_out" / "parity.json")
+    rec = {}
+
+    def log(name, **kv):
+        rec[name] = {k: (float(v) if hasattr(v, "__float__") and not isinstance(v, (int, bool)) else v)
+                     for k, v in kv.items()}
+        if path:
+            old = {}
+            try:
+                with open(path) as f:
+                    old = json.load(f)
+            except Exception:
+                pass
+            old.update(rec)
+            with open(path, "w") as f:
+                json.dump(old, f, indent=1, sort_keys=True)
+
+    return log

@@ -155,7 +155,7 @@ def orc_cull(geo: np.ndarray, cam: np.ndarray, vp, low_pass=0.3, stride=10) -> n
 
 
 def render(lib_name: str, ids, geo, nongeo, cam, vp, *, compact=False, sh_degree=3, bg=(0, 0, 0), gt=None,
-           normalizer=0, d_img=None, geo_stride=10):
+           normalizer=0, d_img=None, geo_stride=10, workers=1):
     """Runs ref_render / orc_render; returns a dict of outputs."""
     ids = np.ascontiguousarray(ids, np.int32)
     geo = np.ascontiguousarray(geo, np.float32)
@@ -181,7 +181,7 @@ def render(lib_name: str, ids, geo, nongeo, cam, vp, *, compact=False, sh_degree
     di = None if d_img is None else np.ascontiguousarray(d_img, np.float32)
     if lib_name == "ref":
         st = ref().ref_render(n, _p(ids), _p(geo), geo_stride, _p(nongeo), int(compact), sh_degree, _p(bga), _p(cam),
-                              _p(vpa), _p(gt_p), int(normalizer), _p(di), 1, _p(img), _p(fT), _p(ln), _p(loss),
+                              _p(vpa), _p(gt_p), int(normalizer), _p(di), int(workers), _p(img), _p(fT), _p(ln), _p(loss),
                               _p(dimg), _p(rows), _p(m2d), None, _p(meta))
     else:
         st = orc().orc_render(n, _p(ids), _p(geo), geo_stride, _p(nongeo), int(compact), sh_degree, _p(bga), _p(cam),
