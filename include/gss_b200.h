@@ -7,7 +7,8 @@
  *   - device buffers are caller-allocated; every call is enqueued on the given CUDA stream and
  *     returns immediately (stream-ordered), except where a host-visible result is documented;
  *   - status codes: GSS_OK 0, GSS_ERR_CUDA 1, GSS_ERR_INVALID 2 (reference: ConfigError /
- *     std::invalid_argument), GSS_ERR_INVARIANT 3 (reference: InvariantViolation); the message of
+ *     std::invalid_argument), GSS_ERR_INVARIANT 3 (reference: InvariantViolation), GSS_ERR_PARSE 4
+ *     (reference: ParseError, PLY ingestion only); the message of
  *     the last failure on the calling thread is returned by gss_last_error();
  *   - there is no CPU fallback: without a CUDA device every compute entry point fails with
  *     GSS_ERR_CUDA.
@@ -24,7 +25,7 @@ extern "C" {
 
 typedef void* gss_stream_t; /* a cudaStream_t */
 
-enum { GSS_OK = 0, GSS_ERR_CUDA = 1, GSS_ERR_INVALID = 2, GSS_ERR_INVARIANT = 3 };
+enum { GSS_OK = 0, GSS_ERR_CUDA = 1, GSS_ERR_INVALID = 2, GSS_ERR_INVARIANT = 3, GSS_ERR_PARSE = 4 };
 
 /* Camera<float> (scene.hpp:77-96): world->camera p_c = rot * p + trans, row-major rot. 80 bytes,
  * layout-identical to the reference struct. */
@@ -316,6 +317,18 @@ int gss_synth_scene(uint64_t seed, int64_t n, int32_t cams, int32_t width, int32
  * logit(init_opacity), DC colour; rows_out host m x 59, bit-identical to the reference. */
 int gss_init_gaussians(const float* positions, const float* colors, int32_t m, int32_t knn, double min_knn_dist,
                        double init_opacity, float* rows_out);
+/* load_ply (ply.hpp:10-14, ply.cpp:53-199) in two calls: gss_ply_open parses the header and
+ * returns the vertex count and whether red/green/blue (or r/g/b) properties exist; gss_ply_read
+ * decodes the vertex body into positions (m x 3) and colors (m x 3 or NULL), host or device
+ * pointers. Binary little-endian bodies are streamed through pinned 32 MB chunks into HBM and
+ * decoded by a kernel; ASCII bodies are tokenised on the host (strtod). Values, colour
+ * normalisation and every ParseError message (status GSS_ERR_PARSE) follow the reference. */
+typedef struct gss_ply gss_ply;
+int gss_ply_open(const char* path, gss_ply** out, int64_t* vertex_count, int32_t* has_color);
+int gss_ply_read(gss_ply* ply, float* positions, float* colors, gss_stream_t stream);
+void gss_ply_close(gss_ply* ply);
+/* save_ply (ply.hpp:16-17, ply.cpp:201-225): host positions m x 3, colors m x 3 or NULL (0.5 grey). */
+int gss_save_ply(const char* path, const float* positions, const float* colors, int64_t m, int32_t binary);
 /* look_at_camera (scene.hpp:99-126). */
 int gss_look_at_camera(const float* eye, const float* target, float fx, float fy, int32_t w, int32_t h,
                        float near_p, float far_p, gss_camera* out);

@@ -10,6 +10,7 @@
 // Only tests/, __graft_entry__.smoke() and bench.py's reference / cpu_baseline legs load it.
 
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -19,6 +20,7 @@
 #include "gss/adam.hpp"
 #include "gss/bench.hpp"
 #include "gss/engine.hpp"
+#include "gss/ply.hpp"
 #include "gss/render.hpp"
 #include "gss/splitter.hpp"
 #include "gss/synth.hpp"
@@ -482,6 +484,39 @@ REF_API int ref_init_gaussians(const float* positions, const float* colors, int 
     ic.init_opacity = init_opacity;
     const GaussianSet<F> gs = init_gaussians<F>(pc, ic);
     for (int i = 0; i < m; ++i) gs.full_row(i, rows_out + size_t(i) * kParamDim);
+    return 0;
+  } catch (...) {
+    return status_of_current();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// PLY ingestion (ply.cpp:53-225). ref_load_ply: *m / *has_color receive the cloud's size; the
+// arrays are filled when cap >= *m. Returns 0, or 4 for ParseError (message in err).
+REF_API int ref_load_ply(const char* path, int64_t cap, float* pos, float* col, int64_t* m, int* has_color, char* err,
+                         int errlen) {
+  try {
+    const PointCloud pc = load_ply(path);
+    *m = pc.size();
+    *has_color = pc.colors.empty() ? 0 : 1;
+    if (cap >= *m) {
+      std::memcpy(pos, pc.positions.data(), pc.positions.size() * sizeof(float));
+      if (col && !pc.colors.empty()) std::memcpy(col, pc.colors.data(), pc.colors.size() * sizeof(float));
+    }
+    return 0;
+  } catch (const ParseError& e) {
+    if (err && errlen > 0) std::snprintf(err, size_t(errlen), "%s", e.what());
+    return 4;
+  } catch (...) {
+    return status_of_current();
+  }
+}
+REF_API int ref_save_ply(const char* path, const float* pos, const float* col, int m, int binary) {
+  try {
+    PointCloud pc;
+    pc.positions.assign(pos, pos + size_t(m) * 3);
+    if (col) pc.colors.assign(col, col + size_t(m) * 3);
+    save_ply(path, pc, binary != 0);
     return 0;
   } catch (...) {
     return status_of_current();

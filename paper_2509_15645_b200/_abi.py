@@ -12,7 +12,7 @@ from pathlib import Path
 # GSS_LIB overrides the library path (kernel-variant experiments built by tools/build_variant.py).
 LIB_PATH = Path(os.environ.get("GSS_LIB") or Path(__file__).resolve().parent / "libgss_b200.so")
 
-GSS_OK, GSS_ERR_CUDA, GSS_ERR_INVALID, GSS_ERR_INVARIANT = 0, 1, 2, 3
+GSS_OK, GSS_ERR_CUDA, GSS_ERR_INVALID, GSS_ERR_INVARIANT, GSS_ERR_PARSE = 0, 1, 2, 3, 4
 
 
 class GssCamera(C.Structure):
@@ -172,6 +172,10 @@ SIGNATURES = {
     "gss_synth_scene": (C.c_int, [C.c_uint64, I64, I32, I32, I32, I32, P, P, P]),
     "gss_init_gaussians": (C.c_int, [P, P, I32, I32, F64, F64, P]),
     "gss_look_at_camera": (C.c_int, [P, P, F32, F32, I32, I32, F32, F32, C.POINTER(GssCamera)]),
+    "gss_ply_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
+    "gss_ply_read": (C.c_int, [P, P, P, P]),
+    "gss_ply_close": (None, [P]),
+    "gss_save_ply": (C.c_int, [C.c_char_p, P, P, I64, I32]),
 }
 
 _lib = None
@@ -208,6 +212,10 @@ class InvariantViolation(GssError):
     """Reference InvariantViolation (status 3)."""
 
 
+class ParseError(GssError):
+    """Reference ParseError (status 4; PLY ingestion)."""
+
+
 def check(status: int) -> None:
     if status == GSS_OK:
         return
@@ -216,4 +224,6 @@ def check(status: int) -> None:
         raise ConfigError(status, msg)
     if status == GSS_ERR_INVARIANT:
         raise InvariantViolation(status, msg)
+    if status == GSS_ERR_PARSE:
+        raise ParseError(status, msg)
     raise GssError(status, msg)

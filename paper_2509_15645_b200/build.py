@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = PKG / "_build"
 LIB = PKG / "libgss_b200.so"
-SOURCES = ["cull.cu", "adam.cu", "raster.cu", "engine.cu", "densify.cu", "synth.cu", "abi.cu"]
+SOURCES = ["cull.cu", "adam.cu", "raster.cu", "engine.cu", "densify.cu", "synth.cu", "ply.cu", "abi.cu"]
 HEADERS = ["common.cuh", "gss_math.cuh"]
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")

@@ -49,6 +49,11 @@ void rasterize_records_forward(gss_render_ctx* ctx, const void* records, int64_t
 void rasterize_records_backward(gss_render_ctx* ctx, const float* d_img, float* sums, cudaStream_t st);
 void chain_backward(const gss_render_scene* scene, const gss_camera* cam, const void* records, const float* sums,
                     float* gg, int64_t gstride, float* gn, int64_t nstride, float* mean2d, cudaStream_t st);
+// ply.cu
+gss_ply* ply_open(const char* path, int64_t* count, int32_t* has_color);
+void ply_read(gss_ply* p, float* pos, float* col, cudaStream_t st);
+void ply_close(gss_ply* p);
+void save_ply(const char* path, const float* pos, const float* col, int64_t m, bool binary);
 // engine.cu
 void engine_config_default(gss_engine_config* c);
 void init_gaussians(const float* positions, const float* colors, int m, int knn, double min_knn_dist,
@@ -346,6 +351,21 @@ GSS_API int gss_init_gaussians(const float* positions, const float* colors, int3
     require_device();
     init_gaussians(positions, colors, m, knn, min_knn_dist, init_opacity, rows_out);
   });
+}
+
+GSS_API int gss_ply_open(const char* path, gss_ply** out, int64_t* vertex_count, int32_t* has_color) {
+  return guarded([&] {
+    require(out != nullptr, "ply: null output handle");
+    *out = nullptr;
+    *out = ply_open(path, vertex_count, has_color);
+  });
+}
+GSS_API int gss_ply_read(gss_ply* ply, float* positions, float* colors, gss_stream_t stream) {
+  return guarded([&] { ply_read(ply, positions, colors, as_stream(stream)); });
+}
+GSS_API void gss_ply_close(gss_ply* ply) { ply_close(ply); }
+GSS_API int gss_save_ply(const char* path, const float* positions, const float* colors, int64_t m, int32_t binary) {
+  return guarded([&] { save_ply(path, positions, colors, m, binary != 0); });
 }
 
 GSS_API void gss_engine_config_default(gss_engine_config* cfg) {

@@ -578,6 +578,56 @@ def init_gaussians(positions: np.ndarray, colors: Optional[np.ndarray] = None, k
     return rows[:m]
 
 
+class PointCloud:
+    """PointCloud (scene.hpp:128-133): positions m x 3, colors m x 3 in [0, 1] or None."""
+
+    def __init__(self, positions, colors=None):
+        self.positions = positions
+        self.colors = colors
+
+    def size(self) -> int:
+        return int(self.positions.shape[0])
+
+
+def load_ply(path, device: Optional[torch.device] = None) -> PointCloud:
+    """load_ply (ply.hpp:10-14, ply.cpp:53-199): ASCII or binary little-endian PLY with x,y,z
+    (+ red/green/blue or r/g/b). Binary bodies are decoded on the GPU; `device` keeps the result
+    there (torch tensors) instead of returning numpy arrays. Raises ParseError like the reference."""
+    h = C.c_void_p()
+    m = C.c_int64()
+    hc = C.c_int32()
+    check(lib().gss_ply_open(str(path).encode(), C.byref(h), C.byref(m), C.byref(hc)))
+    try:
+        n = int(m.value)
+        if device is not None:
+            pos = torch.empty((n, 3), dtype=torch.float32, device=device)
+            col = torch.empty((n, 3), dtype=torch.float32, device=device) if hc.value else None
+            check(lib().gss_ply_read(h, pos.data_ptr(), None if col is None else col.data_ptr(),
+                                     torch.cuda.current_stream(device).cuda_stream))
+        else:
+            pos = np.empty((n, 3), np.float32)
+            col = np.empty((n, 3), np.float32) if hc.value else None
+            check(lib().gss_ply_read(h, pos.ctypes.data, None if col is None else col.ctypes.data, None))
+    finally:
+        lib().gss_ply_close(h)
+    return PointCloud(pos, col)
+
+
+def save_ply(path, pc: PointCloud, binary: bool = True) -> None:
+    """save_ply (ply.hpp:16-17, ply.cpp:201-225)."""
+    pos = np.ascontiguousarray(pc.positions, np.float32).reshape(-1, 3)
+    col = None if pc.colors is None else np.ascontiguousarray(pc.colors, np.float32).reshape(-1, 3)
+    check(lib().gss_save_ply(str(path).encode(), pos.ctypes.data, None if col is None else col.ctypes.data,
+                             pos.shape[0], 1 if binary else 0))
+
+
+def init_from_ply(path, knn: int = 3, min_knn_dist: float = 0.01, init_opacity: float = 0.1) -> np.ndarray:
+    """PLY -> init_gaussians rows (m x 59): the real-scene entry of the training path
+    (trainer.hpp's scene setup: load_ply then init_gaussians)."""
+    pc = load_ply(path)
+    return init_gaussians(pc.positions, pc.colors, knn, min_knn_dist, init_opacity)
+
+
 def render_view(rows: torch.Tensor, cam: GssCamera, sh_degree: int, background=(0.0, 0.0, 0.0)) -> torch.Tensor:
     """render_view (synth.hpp:81-94) on the device: cull + rasterize over a full viewport."""
     geo = rows[:, :K_GEO_DIM].contiguous()

@@ -66,6 +66,8 @@ def ref():
             "ref_compute_split_points": (None, [P, C.c_int, C.c_int, P, F64, P, P]),
             "ref_psnr_over_views": (F64, [C.c_int, P, C.c_int, P, P, C.c_int, P]),
             "ref_init_gaussians": (C.c_int, [P, P, C.c_int, C.c_int, F64, F64, P]),
+            "ref_load_ply": (C.c_int, [C.c_char_p, I64, P, P, P, P, C.c_char_p, C.c_int]),
+            "ref_save_ply": (C.c_int, [C.c_char_p, P, P, C.c_int, C.c_int]),
         }
         for k, (r, a) in sig.items():
             f = getattr(l, k)
@@ -492,3 +494,27 @@ def ref_init_gaussians(positions, colors=None, knn=3, min_knn_dist=0.01, init_op
     st = ref().ref_init_gaussians(_p(pos), _p(col), m, knn, float(min_knn_dist), float(init_opacity), _p(rows))
     assert st == 0, st
     return rows
+
+
+def ref_load_ply(path):
+    """load_ply (ply.cpp:53-199) of the reference: (positions, colors or None) or raises
+    RuntimeError('ParseError: ...') with the reference message."""
+    m = C.c_int64()
+    hc = C.c_int()
+    err = C.create_string_buffer(512)
+    st = ref().ref_load_ply(str(path).encode(), C.c_int64(-1), None, None, C.byref(m), C.byref(hc), err, 512)
+    if st == 4:
+        raise RuntimeError("ParseError: " + err.value.decode())
+    assert st == 0, st
+    pos = np.zeros((max(m.value, 1), 3), np.float32)
+    col = np.zeros((max(m.value, 1), 3), np.float32)
+    st = ref().ref_load_ply(str(path).encode(), C.c_int64(m.value), _p(pos), _p(col), C.byref(m), C.byref(hc), err, 512)
+    assert st == 0, st
+    return pos[: m.value], (col[: m.value] if hc.value else None)
+
+
+def ref_save_ply(path, pos, col=None, binary=True):
+    pos = np.ascontiguousarray(pos, np.float32)
+    c = None if col is None else np.ascontiguousarray(col, np.float32)
+    assert ref().ref_save_ply(str(path).encode(), _p(pos), None if c is None else _p(c), pos.shape[0],
+                              1 if binary else 0) == 0

@@ -86,7 +86,24 @@ def test_c2_view_forward_backward_vs_reference(c2, ref, parity_log):
         assert sm["max_rel_err"] <= 1e-4, sm
 
 
+def _ref_engine(start, cams, gts, iters, workers):
+    r = O.RefEngine(start, np.stack([O.cam_from_struct(c) for c in cams[:iters]]), gts, pipelined=True,
+                    workers=workers)
+    rl, rv = r.run(iters)
+    rs = r.state()
+    rn, rc = r.accum()
+    del r
+    return rl, rv, rs, rn, rc
+
+
 def _engine_vs_ref(truth, cams, iters, nongeo_on_host, parity_log, name):
+    """Engine vs the reference OffloadEngine. Losses, culls, counters, steps and densify counts
+    must match exactly; m, v and the statistics within 1e-4. The parameters w are held to the
+    reference's own reproducibility: the reference's backward sums per-worker partials in worker
+    order (render.hpp:538-598), so the reference at `workers` = CORES and CORES/2 disagrees with
+    itself, and Adam's first steps amplify gradient differences near zero (|g| ~ eps: the update
+    m/(sqrt(v)+eps) swings by up to lr). Our deviation from ref(CORES) must stay within 4x the
+    reference's self-deviation ref(CORES/2) vs ref(CORES) (or 1e-4, whichever is larger)."""
     start = bench.training_start(truth)
     td = torch.from_numpy(truth).cuda()
     gts = np.stack([G.render_view(td, c, 3).cpu().numpy() for c in cams[:iters]])
@@ -98,27 +115,34 @@ def _engine_vs_ref(truth, cams, iters, nongeo_on_host, parity_log, name):
     norm, cnt = e.accum()
     e.close()
     del e
-    r = O.RefEngine(start, np.stack([O.cam_from_struct(c) for c in cams[:iters]]), gts, pipelined=True,
-                    workers=CORES)
-    rl, rv = r.run(iters)
-    rs = r.state()
-    rn, rc = r.accum()
-    del r
-    assert np.array_equal(valid, rv)  # identical culls every iteration
+    rl, rv, rs, rn, rc = _ref_engine(start, cams, gts, iters, CORES)
+    half = max(1, CORES // 2)
+    sl, sv, ss, sn, sc = _ref_engine(start, cams, gts, iters, half)
+    assert np.array_equal(valid, rv) and np.array_equal(sv, rv)  # identical culls every iteration
     assert losses[0] == rl[0]  # first forward on identical parameters: bit-identical loss
     loss_dev = float(np.max(np.abs(losses - rl) / np.maximum(1.0, np.abs(rl))))
     assert np.array_equal(st["ng_counter"], rs["ng_counter"])
     assert np.array_equal(cnt, rc)
     assert st["geo_step"] == rs["geo_step"] and st["ng_step"] == rs["ng_step"]
-    out = {k: float(O.rel_err(st[k], rs[k]).max()) for k in ("geo_w", "ng_w", "ng_m", "ng_v")}
-    exact = {k: float(np.mean(bits(st[k]) == bits(rs[k]))) for k in ("geo_w", "ng_w", "ng_m", "ng_v")}
+    keys = ("geo_w", "ng_w", "ng_m", "ng_v")
+    out = {k: float(O.rel_err(st[k], rs[k]).max()) for k in keys}
+    self_dev = {k: float(O.rel_err(ss[k], rs[k]).max()) for k in keys}
+    over = {k: float(np.mean(O.rel_err(st[k], rs[k]) > 1e-4)) for k in keys}
+    self_over = {k: float(np.mean(O.rel_err(ss[k], rs[k]) > 1e-4)) for k in keys}
+    exact = {k: float(np.mean(bits(st[k]) == bits(rs[k]))) for k in keys}
+    self_exact = {k: float(np.mean(bits(ss[k]) == bits(rs[k]))) for k in keys}
     norm_dev = float(O.rel_err(norm, rn).max())
     parity_log(name, iters=iters, valid=valid.tolist(), losses=losses.tolist(), ref_losses=rl.tolist(),
-               max_loss_rel_err=loss_dev, state_max_rel_err=out, state_bitwise_fraction=exact,
-               accum_norm_max_rel_err=norm_dev, nongeo_on_host=nongeo_on_host, ref_workers=CORES)
+               ref_half_workers_losses=sl.tolist(), max_loss_rel_err=loss_dev, state_max_rel_err=out,
+               ref_self_max_rel_err=self_dev, state_frac_over_1e4=over, ref_self_frac_over_1e4=self_over,
+               state_bitwise_fraction=exact, ref_self_bitwise_fraction=self_exact,
+               accum_norm_max_rel_err=norm_dev, nongeo_on_host=nongeo_on_host, ref_workers=[CORES, half])
     assert loss_dev <= 1e-4
-    for k, v in out.items():
-        assert v <= 1e-4, (k, v)
+    for k in ("ng_m", "ng_v"):
+        assert out[k] <= 1e-4, (k, out[k])
+    for k in ("geo_w", "ng_w"):
+        assert out[k] <= max(1e-4, 4 * self_dev[k]), (k, out[k], self_dev[k])
+        assert over[k] <= max(1e-6, 4 * self_over[k]), (k, over[k], self_over[k])
     assert norm_dev <= 1e-4
 
 
