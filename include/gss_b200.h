@@ -184,6 +184,14 @@ int gss_loss_l1(const float* image, const float* gt, int64_t elems, int64_t norm
 int gss_rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* grad_geo, int64_t geo_stride,
                            float* grad_nongeo, int64_t ng_stride, float* mean2d_opt, gss_stream_t stream);
 
+/* Rasterizer work accounting (device counters, synchronises the device): out8[0..7] = forward
+ * (warp, record) pairs walked, forward lane-pixel slots offered, forward (pixel, record) pairs in
+ * box, forward contributions composited, forward eval slots issued, backward (warp, record) pairs
+ * walked, backward lane-pixel slots, backward useful contributions. Counted only by a library built
+ * with -DGSS_RASTER_STATS=1 (gss_raster_stats_enabled() == 1); zeros otherwise. */
+int gss_raster_stats(uint64_t* out8, int32_t reset);
+int32_t gss_raster_stats_enabled(void);
+
 /* image_mse numerator (trainer.hpp:113-122) for psnr / psnr_over_views (trainer.hpp:124-145):
  * sum_dev (device double) = sum over elems of (double(a) - double(b))^2, fixed-order reduction. */
 int gss_image_sq_err(const float* a, const float* b, int64_t elems, double* sum_dev, gss_stream_t stream);
@@ -282,6 +290,13 @@ int64_t gss_engine_count(gss_engine* e);
 int gss_engine_stage_ms(gss_engine* e, double* out6);
 /* Kernel launches issued by the last run/step (for bench accounting). */
 int64_t gss_engine_launches(gss_engine* e);
+/* Live per-kernel timing (bench roofline of the dominant kernels): when on, every forward_kernel
+ * (composite) and backward_kernel (sweep) launch of the engine is bracketed by CUDA events on its
+ * stream and the composited contributions are counted. gss_engine_kernel_times drains, then
+ * returns ms2[0..1] = total ms of the composite / sweep launches since the last call, n2[0..1] =
+ * their launch counts, *contribs = contributions composited (= useful backward contributions). */
+int gss_engine_kernel_timing(gss_engine* e, int32_t on);
+int gss_engine_kernel_times(gss_engine* e, double* ms2, int64_t* n2, uint64_t* contribs);
 
 /* ---- densification (trainer.hpp:166-213, engine.hpp:116-163) ------------- */
 /* DensifyConfig (trainer.hpp:32-47): the thresholds of plan_densify. */

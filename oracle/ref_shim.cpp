@@ -281,6 +281,81 @@ REF_API void ref_synth_scene(uint64_t seed, int n, int cams, int width, int heig
                   s.gt_images[k].data.size() * sizeof(F));
 }
 
+namespace {
+GaussianSet<F> set_from_rows(int n, const float* rows);
+}  // namespace
+
+// synth_scene (synth.hpp:100-154) without its ground-truth render (synth.hpp:156-158), for workloads
+// whose CPU render of all views would take minutes (the reference arm renders only the views it
+// times). Same Rng stream and operation order as synth_scene, built from the reference's own
+// primitives (Rng, logit, look_at_camera); pinned equal to ref_synth_scene by tests/test_oracle.py.
+REF_API void ref_synth_scene_nogt(uint64_t seed, int n, int cams, int width, int height, int sh_degree,
+                                  const double* cfg_d, float* rows_out, void* cams_out) {
+  SynthConfig cfg;
+  cfg.seed = seed; cfg.n = n; cfg.cams = cams; cfg.width = width; cfg.height = height; cfg.sh_degree = sh_degree;
+  cfg.box = cfg_d[0]; cfg.radius_min = cfg_d[1]; cfg.radius_max = cfg_d[2]; cfg.fov_deg = cfg_d[3];
+  cfg.fov_ramp = cfg_d[4]; cfg.target_jitter = cfg_d[5]; cfg.near_plane = cfg_d[6]; cfg.far_plane = cfg_d[7];
+  cfg.scale_min = cfg_d[8]; cfg.scale_max = cfg_d[9]; cfg.scale_aniso = cfg_d[10]; cfg.opacity_min = cfg_d[11];
+  cfg.opacity_max = cfg_d[12]; cfg.sh_rest_noise = cfg_d[13];
+  Rng rng(cfg.seed * 0x9E3779B97F4A7C15ull + 0xD1B54A32D192ED03ull);
+  GaussianSet<F> gs;
+  gs.resize(cfg.n);
+  gs.sh_degree = cfg.sh_degree;
+  for (int i = 0; i < cfg.n; ++i) {
+    for (int a = 0; a < 3; ++a) gs.mean[i * 3 + a] = F(rng.uniform(-cfg.box, cfg.box));
+    const double log_lo = std::log(cfg.scale_min * cfg.box), log_hi = std::log(cfg.scale_max * cfg.box);
+    const double base = rng.uniform(log_lo, log_hi);
+    for (int a = 0; a < 3; ++a) gs.scale[i * 3 + a] = F(base + rng.uniform(-cfg.scale_aniso, cfg.scale_aniso));
+    double q[4];
+    double qn = 0;
+    for (auto& c : q) {
+      c = rng.normal();
+      qn += c * c;
+    }
+    qn = std::sqrt(qn);
+    if (qn < 1e-9) { q[0] = 1; q[1] = q[2] = q[3] = 0; qn = 1; }
+    for (int a = 0; a < 4; ++a) gs.quaternion[i * 4 + a] = F(q[a] / qn);
+    gs.opacity[i] = F(logit(rng.uniform(cfg.opacity_min, cfg.opacity_max)));
+    for (int c = 0; c < 3; ++c) gs.sh[i * kShScalars + c] = F((rng.uniform(0.08, 0.92) - 0.5) / kShC0);
+    const int active = (cfg.sh_degree + 1) * (cfg.sh_degree + 1);
+    for (int k = 1; k < active; ++k)
+      for (int c = 0; c < 3; ++c) gs.sh[i * kShScalars + k * 3 + c] = F(rng.normal() * cfg.sh_rest_noise);
+  }
+  std::vector<Camera<F>> out;
+  const double golden = 2.399963229728653;
+  for (int i = 0; i < cfg.cams; ++i) {
+    const double t = cfg.cams > 1 ? double(i) / (cfg.cams - 1) : 1.0;
+    const double radius = cfg.box * (cfg.radius_min * std::pow(cfg.radius_max / cfg.radius_min, t));
+    const double fov = cfg.fov_deg * (cfg.fov_ramp + (1.0 - cfg.fov_ramp) * t);
+    const double fx = 0.5 * cfg.width / std::tan(0.5 * fov * M_PI / 180.0);
+    const double fy = fx;
+    const double az = golden * i + rng.uniform(-0.15, 0.15);
+    const double el = (0.15 + 0.55 * rng.uniform()) * (i % 2 == 0 ? 1.0 : -1.0);
+    Vec3<F> eye{F(radius * std::cos(el) * std::cos(az)), F(radius * std::sin(el)),
+                F(radius * std::cos(el) * std::sin(az))};
+    const double jig = cfg.target_jitter * (1.0 - t);
+    Vec3<F> target{F(rng.uniform(-jig, jig) * cfg.box), F(rng.uniform(-jig, jig) * cfg.box),
+                   F(rng.uniform(-jig, jig) * cfg.box)};
+    out.push_back(look_at_camera<F>(eye, target, F(fx), F(fy), cfg.width, cfg.height, F(cfg.near_plane),
+                                    F(cfg.far_plane)));
+  }
+  for (int i = cfg.cams - 1; i > 0; --i) {
+    const int j = int(rng.next_u64() % uint64_t(i + 1));
+    std::swap(out[i], out[j]);
+  }
+  for (int i = 0; i < n; ++i) gs.full_row(i, rows_out + size_t(i) * kParamDim);
+  std::memcpy(cams_out, out.data(), out.size() * sizeof(Camera<F>));
+}
+
+// render_view (synth.hpp:81-94) of rows (n x 59) with `workers` threads: the reference's ground truth
+// for one view.
+REF_API void ref_render_view_rows(int n, const float* rows, const void* cam, int sh_degree, int workers,
+                                  float* img_out) {
+  const GaussianSet<F> gs = set_from_rows(n, rows);
+  const Image<F> im = render_view(gs, cam_of(cam), sh_degree, workers);
+  std::memcpy(img_out, im.data.data(), im.data.size() * sizeof(F));
+}
+
 REF_API void ref_look_at_camera(const float* eye, const float* target, float fx, float fy, int w, int h, float near_p,
                                 float far_p, void* out) {
   const auto c = look_at_camera<F>(Vec3<F>{eye[0], eye[1], eye[2]}, Vec3<F>{target[0], target[1], target[2]}, fx, fy, w,

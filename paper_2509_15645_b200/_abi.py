@@ -172,6 +172,10 @@ SIGNATURES = {
     "gss_synth_scene": (C.c_int, [C.c_uint64, I64, I32, I32, I32, I32, P, P, P]),
     "gss_init_gaussians": (C.c_int, [P, P, I32, I32, F64, F64, P]),
     "gss_look_at_camera": (C.c_int, [P, P, F32, F32, I32, I32, F32, F32, C.POINTER(GssCamera)]),
+    "gss_raster_stats": (C.c_int, [P, I32]),
+    "gss_engine_kernel_timing": (C.c_int, [P, I32]),
+    "gss_engine_kernel_times": (C.c_int, [P, P, P, P]),
+    "gss_raster_stats_enabled": (I32, []),
     "gss_ply_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "gss_ply_read": (C.c_int, [P, P, P, P]),
     "gss_ply_close": (None, [P]),

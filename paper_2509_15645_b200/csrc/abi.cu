@@ -49,6 +49,8 @@ void rasterize_records_forward(gss_render_ctx* ctx, const void* records, int64_t
 void rasterize_records_backward(gss_render_ctx* ctx, const float* d_img, float* sums, cudaStream_t st);
 void chain_backward(const gss_render_scene* scene, const gss_camera* cam, const void* records, const float* sums,
                     float* gg, int64_t gstride, float* gn, int64_t nstride, float* mean2d, cudaStream_t st);
+void raster_stats(uint64_t* out8, bool reset);
+int raster_stats_enabled();
 // ply.cu
 gss_ply* ply_open(const char* path, int64_t* count, int32_t* has_color);
 void ply_read(gss_ply* p, float* pos, float* col, cudaStream_t st);
@@ -75,6 +77,8 @@ void engine_state(gss_engine* e, float* geo_w, float* ng_w, float* ng_m, float* 
 void engine_accum(gss_engine* e, double* norm, int32_t* cnt);
 void engine_stage_ms(gss_engine* e, double* out6);
 int64_t engine_launches(gss_engine* e);
+void engine_kernel_timing(gss_engine* e, bool on);
+void engine_kernel_times(gss_engine* e, double* ms2, int64_t* n2, uint64_t* contribs);
 int64_t engine_count(gss_engine* e);
 
 namespace {
@@ -353,6 +357,16 @@ GSS_API int gss_init_gaussians(const float* positions, const float* colors, int3
   });
 }
 
+GSS_API int gss_raster_stats(uint64_t* out8, int32_t reset) {
+  return guarded([&] {
+    require_device();
+    require(out8 != nullptr, "raster_stats: null output");
+    GSS_CUDA(cudaDeviceSynchronize());
+    raster_stats(out8, reset != 0);
+  });
+}
+GSS_API int32_t gss_raster_stats_enabled(void) { return raster_stats_enabled(); }
+
 GSS_API int gss_ply_open(const char* path, gss_ply** out, int64_t* vertex_count, int32_t* has_color) {
   return guarded([&] {
     require(out != nullptr, "ply: null output handle");
@@ -415,3 +429,9 @@ GSS_API int gss_engine_stage_ms(gss_engine* e, double* out6) {
   return guarded([&] { engine_stage_ms(e, out6); });
 }
 GSS_API int64_t gss_engine_launches(gss_engine* e) { return engine_launches(e); }
+GSS_API int gss_engine_kernel_timing(gss_engine* e, int32_t on) {
+  return guarded([&] { engine_kernel_timing(e, on != 0); });
+}
+GSS_API int gss_engine_kernel_times(gss_engine* e, double* ms2, int64_t* n2, uint64_t* contribs) {
+  return guarded([&] { engine_kernel_times(e, ms2, n2, contribs); });
+}

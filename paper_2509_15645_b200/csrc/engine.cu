@@ -46,6 +46,8 @@ void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int6
 void render_ctx_destroy(gss_render_ctx* ctx);
 gss_render_ctx* render_ctx_create();
 void arena_release(const gss_arena* ap);
+void render_ctx_timing(gss_render_ctx* ctx, bool on);
+void render_ctx_times(gss_render_ctx* ctx, double* ms2, int64_t* n2, uint64_t* contribs);
 }  // namespace gssd
 
 struct gss_render_ctx;
@@ -828,6 +830,19 @@ void engine_stage_ms(gss_engine* e, double* out6) {
 }
 
 int64_t engine_launches(gss_engine* e) { return e ? e->launches_last : 0; }
+
+// Live timing of the engine's composite / sweep kernel launches (bench roofline of the dominant
+// kernels): CUDA events on the render stream around each forward_kernel / backward_kernel.
+void engine_kernel_timing(gss_engine* e, bool on) {
+  require(e != nullptr, "engine: null");
+  render_ctx_timing(e->rctx, on);
+}
+void engine_kernel_times(gss_engine* e, double* ms2, int64_t* n2, uint64_t* contribs) {
+  require(e != nullptr, "engine: null");
+  if (e->open_pending >= 0) drain(e);
+  GSS_CUDA(cudaDeviceSynchronize());
+  render_ctx_times(e->rctx, ms2, n2, contribs);
+}
 int64_t engine_count(gss_engine* e) { return e ? e->n : 0; }
 
 }  // namespace gssd

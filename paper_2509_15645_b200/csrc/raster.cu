@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 #include "gss_math.cuh"
@@ -66,6 +67,17 @@ constexpr int kFwdBlockRows = 4 * kFwdPPT;
 #endif
 constexpr int kBwdBatch = GSS_BWD_BATCH;  // records per SMEM batch of the backward sweep
 constexpr int kBwdMasks = kBwdBatch / 64;  // 64-bit record masks per warp and batch
+
+// Work accounting (GSS_RASTER_STATS=1 builds only; zero otherwise), read by gss_raster_stats:
+//   [0] forward (warp, record) pairs walked   [1] forward lane-pixel slots offered (walked x 32 x PPT)
+//   [2] forward (pixel, record) in box        [3] forward contributions evaluated (composited)
+//   [4] forward eval slots issued (32 per warp-level eval)
+//   [5] backward (warp, record) pairs walked  [6] backward lane-pixel slots (walked x 32 x PPT)
+//   [7] backward useful (pixel, record) contributions
+#ifndef GSS_RASTER_STATS
+#define GSS_RASTER_STATS 0
+#endif
+__device__ unsigned long long g_rstats[8];
 
 struct __align__(16) SplatRec {
   float mx, my, a, b;
@@ -126,6 +138,18 @@ struct gss_render_ctx {
   int have_forward = 0;
   int64_t* pinned = nullptr;  // host-visible counts
   cudaStream_t last_stream = nullptr;
+  // Live kernel timing (bench roofline): CUDA events around each forward_kernel (kind 0) and
+  // backward_kernel (kind 1) launch on its stream, and the composited-contribution count.
+  bool ktiming = false;
+  struct KTime {
+    int kind;
+    cudaEvent_t a, b;
+  };
+  std::vector<KTime> ktimes;
+  std::vector<cudaEvent_t> kfree;
+  double kms[2] = {0.0, 0.0};
+  int64_t kn[2] = {0, 0};
+  unsigned long long* contribs_dev = nullptr;  // running total of composited contributions
 };
 
 namespace gssd {
@@ -484,7 +508,8 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
                                                            float bg1, float bg2, float* image, float* fT_out,
                                                            int32_t* last_out, int32_t* ncontrib_out,
                                                            const float* gt, int gt_width, float inv_norm,
-                                                           float* d_img, double* loss_partials) {
+                                                           float* d_img, double* loss_partials,
+                                                           unsigned long long* contribs_total) {
   __shared__ SplatRec sh[kFwdBatch];
   __shared__ double red[kFwdWarps];
   const int tile = tile_of(tile_order);
@@ -500,6 +525,9 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
   float cy[kFwdPPT], T[kFwdPPT], c0[kFwdPPT], c1[kFwdPPT], c2[kFwdPPT];
   bool done[kFwdPPT];
   bool all_done = true;
+#if GSS_RASTER_STATS
+  unsigned long long st_walk = 0, st_box = 0, st_eval = 0, st_slots = 0;
+#endif
 #pragma unroll
   for (int h = 0; h < kFwdPPT; ++h) {
     y[h] = fy0 + (lane >> 3) + 4 * h;
@@ -526,6 +554,9 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
         hit = bx.x <= fx0 + 7 && bx.y > fx0 && bx.z <= fy0 + kFwdBlockRows - 1 && bx.w > fy0;
       }
       unsigned m = __ballot_sync(0xffffffffu, hit);
+#if GSS_RASTER_STATS
+      if (lane == 0) st_walk += __popc(m);
+#endif
       while (m) {
         const int j = c0j + __ffs(m) - 1;
         m &= m - 1;
@@ -534,6 +565,15 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
         const bool xin = (x >= bx.x) & (x < bx.y);
 #pragma unroll
         for (int h = 0; h < kFwdPPT; ++h) {
+#if GSS_RASTER_STATS
+          {
+            const bool inb = xin & (y[h] >= bx.z) & (y[h] < bx.w);
+            const bool evb = inb & !done[h] & !(T[h] < 1e-4f);
+            st_box += inb ? 1 : 0;
+            st_eval += evb ? 1 : 0;
+            if (__ballot_sync(0xffffffffu, evb) && lane == 0) st_slots += 32;
+          }
+#endif
           if (!(!done[h] & xin & (y[h] >= bx.z) & (y[h] < bx.w))) continue;
           if (T[h] < 1e-4f) {
             done[h] = true;
@@ -554,6 +594,13 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
     }
     __syncthreads();
   }
+#if GSS_RASTER_STATS
+  atomicAdd(&g_rstats[0], st_walk);
+  atomicAdd(&g_rstats[1], st_walk * 32ull * kFwdPPT);
+  atomicAdd(&g_rstats[2], st_box);
+  atomicAdd(&g_rstats[3], st_eval);
+  atomicAdd(&g_rstats[4], st_slots);
+#endif
   double acc = 0.0;
 #pragma unroll
   for (int h = 0; h < kFwdPPT; ++h) {
@@ -586,6 +633,13 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
       for (int i = 0; i < kFwdWarps; ++i) s += red[i];
       loss_partials[tile] = s;
     }
+  }
+  if (contribs_total) {  // composited contributions of the tile (bench accounting; integer: exact)
+    unsigned u = 0;
+#pragma unroll
+    for (int h = 0; h < kFwdPPT; ++h) u += (unsigned)used[h];
+    u = __reduce_add_sync(0xffffffffu, u);
+    if (lane == 0) atomicAdd(contribs_total, (unsigned long long)u);
   }
 }
 
@@ -833,6 +887,9 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
   __syncthreads();
   const int Lmax = smax;
   const int vidx = reduce_scatter9_index(lane);
+#if GSS_RASTER_STATS
+  unsigned long long st_walk = 0, st_use = 0;
+#endif
   for (int bend = Lmax; bend > 0; bend -= kBwdBatch) {
     const int bstart = max(0, bend - kBwdBatch);
     const int nb = bend - bstart;
@@ -894,8 +951,14 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
         float v[9];
 #pragma unroll
         for (int i = 0; i < 9; ++i) v[i] = 0.0f;
+#if GSS_RASTER_STATS
+        ++st_walk;
+#pragma unroll
+        for (int q = 0; q < kBwdPPT; ++q) st_use += bwd_contrib(r, k, bstart + jj, px[q], v) ? 1 : 0;
+#else
 #pragma unroll
         for (int q = 0; q < kBwdPPT; ++q) bwd_contrib(r, k, bstart + jj, px[q], v);
+#endif
         // A record no lane contributed to reduces exact zeros: the same partial without a vote.
         const float tot = warp_reduce_scatter9(v, lane);
         if ((lane & 1) == 0 && vidx >= 0) red[jj][warp][vidx] = tot;
@@ -913,6 +976,13 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
       partials[(int64_t)sinst[jj] * 9 + i] = s;
     }
   }
+#if GSS_RASTER_STATS
+  if (lane == 0) {
+    atomicAdd(&g_rstats[5], st_walk);
+    atomicAdd(&g_rstats[6], st_walk * 32ull * kBwdPPT);
+  }
+  atomicAdd(&g_rstats[7], st_use);
+#endif
 }
 
 // render.hpp:600-638 + project_geo_backward (render.hpp:152-237), per slot.
@@ -1347,6 +1417,24 @@ void bin_phase(gss_render_ctx* ctx, const Win& w, int64_t V, cudaStream_t st) {
   }
 }
 
+void ktime_begin(gss_render_ctx* ctx, int kind, cudaStream_t st) {
+  if (!ctx->ktiming) return;
+  gss_render_ctx::KTime t{kind, nullptr, nullptr};
+  for (cudaEvent_t* e : {&t.a, &t.b}) {
+    if (!ctx->kfree.empty()) {
+      *e = ctx->kfree.back();
+      ctx->kfree.pop_back();
+    } else {
+      GSS_CUDA(cudaEventCreate(e));
+    }
+  }
+  GSS_CUDA(cudaEventRecord(t.a, st));
+  ctx->ktimes.push_back(t);
+}
+void ktime_end(gss_render_ctx* ctx, cudaStream_t st) {
+  if (ctx->ktiming) GSS_CUDA(cudaEventRecord(ctx->ktimes.back().b, st));
+}
+
 // composite_phase: per-pixel compositing fused with the L1 loss (forward_kernel).
 void composite_phase(gss_render_ctx* ctx, const Win& w, int64_t V, const FwdOut& o, cudaStream_t st) {
   const SceneDev& s = ctx->sc;
@@ -1363,12 +1451,15 @@ void composite_phase(gss_render_ctx* ctx, const Win& w, int64_t V, const FwdOut&
   }
   const int ntile = w.tw * w.th;
   double* lp = o.gt ? static_cast<double*>(ctx->lossp.get((size_t)ntile * 8, st)) : nullptr;
+  ktime_begin(ctx, 0, st);
   forward_kernel<<<ntile, kFwdThreads, 0, st>>>(static_cast<const SplatRec*>(ctx->recs.p),
                                              static_cast<const int32_t*>(ctx->vals_a.p),
                                              static_cast<const int2*>(ctx->ranges.p),
                                              static_cast<const int32_t*>(ctx->tile_order.p), w, s.bg[0], s.bg[1], s.bg[2],
-                                             o.image, fT, last, o.ncontrib, o.gt, o.gt_width, o.inv, o.d_img, lp);
+                                             o.image, fT, last, o.ncontrib, o.gt, o.gt_width, o.inv, o.d_img, lp,
+                                             ctx->ktiming ? ctx->contribs_dev : nullptr);
   GSS_LAUNCHED();
+  ktime_end(ctx, st);
   if (o.gt) {
     loss_final_kernel<<<1, 1024, 0, st>>>(lp, ntile, o.inv, o.loss_dev, o.loss_sum);
     GSS_LAUNCHED();
@@ -1414,12 +1505,14 @@ void per_slot_sums(gss_render_ctx* ctx, const float* d_img, float* sums, cudaStr
   GSS_CUDA(cudaMemsetAsync(partials, 0, (size_t)I * 9 * 4, st));
   {
     const int ntile = w.tw * w.th;
+    ktime_begin(ctx, 1, st);
     backward_kernel<<<ntile, kBwdThreads, 0, st>>>(recs, static_cast<const int32_t*>(ctx->vals_a.p),
                                                 static_cast<const int2*>(ctx->ranges.p),
                                                 static_cast<const int32_t*>(ctx->tile_order.p), w, ctx->sc.bg[0],
                                                 ctx->sc.bg[1], ctx->sc.bg[2], static_cast<const float*>(ctx->fT.p),
                                                 static_cast<const int32_t*>(ctx->last.p), d_img, partials);
     GSS_LAUNCHED();
+    ktime_end(ctx, st);
   }
   slot_sum_kernel<<<(unsigned)ceil_div(V, kSumThreads), kSumThreads, 0, st>>>(V, soff, nts, partials, sums);
   GSS_LAUNCHED();
@@ -1672,7 +1765,67 @@ void render_ctx_destroy(gss_render_ctx* ctx) {
                   &ctx->slot_off})
     b->release(st);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  cudaDeviceSynchronize();
+  for (auto& t : ctx->ktimes) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (auto e : ctx->kfree) cudaEventDestroy(e);
+  if (ctx->contribs_dev) cudaFree(ctx->contribs_dev);
+  cudaGetLastError();
   delete ctx;
 }
+
+// Live per-kernel timing of the composite (forward_kernel) and sweep (backward_kernel) launches.
+void render_ctx_timing(gss_render_ctx* ctx, bool on) {
+  require(ctx != nullptr, "render ctx: null");
+  ctx->ktiming = on;
+  if (on && !ctx->contribs_dev) {
+    GSS_CUDA(cudaMalloc(&ctx->contribs_dev, sizeof(unsigned long long)));
+    GSS_CUDA(cudaMemset(ctx->contribs_dev, 0, sizeof(unsigned long long)));
+  }
+}
+// Folds the recorded intervals (all must have completed: call after a sync) into
+// out[0..1] = total ms of forward_kernel / backward_kernel launches, n[0..1] = launches,
+// *contribs = composited contributions; resets the accumulators.
+void render_ctx_times(gss_render_ctx* ctx, double* ms2, int64_t* n2, uint64_t* contribs) {
+  require(ctx != nullptr, "render ctx: null");
+  for (auto& t : ctx->ktimes) {
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, t.a, t.b) == cudaSuccess) {
+      ctx->kms[t.kind] += ms;
+      ctx->kn[t.kind] += 1;
+    }
+    ctx->kfree.push_back(t.a);
+    ctx->kfree.push_back(t.b);
+  }
+  cudaGetLastError();
+  ctx->ktimes.clear();
+  for (int k = 0; k < 2; ++k) {
+    if (ms2) ms2[k] = ctx->kms[k];
+    if (n2) n2[k] = ctx->kn[k];
+    ctx->kms[k] = 0.0;
+    ctx->kn[k] = 0;
+  }
+  unsigned long long c = 0;
+  if (ctx->contribs_dev) {
+    GSS_CUDA(cudaMemcpy(&c, ctx->contribs_dev, sizeof c, cudaMemcpyDeviceToHost));
+    GSS_CUDA(cudaMemset(ctx->contribs_dev, 0, sizeof c));
+  }
+  if (contribs) *contribs = c;
+}
+
+// Work-accounting counters of the rasterizer kernels (see g_rstats); all zero unless the library was
+// built with GSS_RASTER_STATS=1.
+void raster_stats(uint64_t* out8, bool reset) {
+  unsigned long long h[8];
+  GSS_CUDA(cudaMemcpyFromSymbol(h, g_rstats, sizeof h));
+  for (int i = 0; i < 8; ++i) out8[i] = h[i];
+  if (reset) {
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    GSS_CUDA(cudaMemcpyToSymbol(g_rstats, z, sizeof z));
+  }
+}
+int raster_stats_enabled() { return GSS_RASTER_STATS; }
 
 }  // namespace gssd

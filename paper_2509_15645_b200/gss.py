@@ -811,6 +811,20 @@ class OffloadEngine:
     def launches(self) -> int:
         return int(lib().gss_engine_launches(self.h))
 
+    def kernel_timing(self, on: bool = True) -> None:
+        """CUDA events around every composite / sweep kernel launch (see kernel_times)."""
+        check(lib().gss_engine_kernel_timing(self.h, 1 if on else 0))
+
+    def kernel_times(self):
+        """Drains; {composite_ms, sweep_ms, composite_launches, sweep_launches, contribs} since the
+        last call (contribs = contributions composited = useful backward contributions)."""
+        ms = np.zeros(2, np.float64)
+        n = np.zeros(2, np.int64)
+        c = C.c_uint64()
+        check(lib().gss_engine_kernel_times(self.h, ms.ctypes.data, n.ctypes.data, C.byref(c)))
+        return {"composite_ms": float(ms[0]), "sweep_ms": float(ms[1]), "composite_launches": int(n[0]),
+                "sweep_launches": int(n[1]), "contribs": int(c.value)}
+
     def densify(self, cfg: DensifyConfig, extent: float, seed: int):
         """A densification event (trainer.hpp:578-591): snapshot, plan_densify, apply_densify."""
         counts = np.zeros(6, np.int64)

@@ -66,6 +66,8 @@ def ref():
             "ref_compute_split_points": (None, [P, C.c_int, C.c_int, P, F64, P, P]),
             "ref_psnr_over_views": (F64, [C.c_int, P, C.c_int, P, P, C.c_int, P]),
             "ref_init_gaussians": (C.c_int, [P, P, C.c_int, C.c_int, F64, F64, P]),
+            "ref_synth_scene_nogt": (None, [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P]),
+            "ref_render_view_rows": (None, [C.c_int, P, P, C.c_int, C.c_int, P]),
             "ref_load_ply": (C.c_int, [C.c_char_p, I64, P, P, P, P, C.c_char_p, C.c_int]),
             "ref_save_ply": (C.c_int, [C.c_char_p, P, P, C.c_int, C.c_int]),
         }
@@ -287,6 +289,26 @@ def ref_synth(cfg, with_gt=False):
     ref().ref_synth_scene(cfg.seed, cfg.n, cfg.cams, cfg.width, cfg.height, cfg.sh_degree, arr.ctypes.data,
                           rows.ctypes.data, cams.ctypes.data, None if gts is None else gts.ctypes.data)
     return rows[: cfg.n], cams[: cfg.cams], (None if gts is None else gts[: cfg.cams])
+
+
+def ref_synth_nogt(cfg):
+    """synth_scene (synth.hpp:100-154) without its ground-truth render: (rows n x 59, cams x 20)."""
+    rows = np.zeros((max(cfg.n, 1), 59), np.float32)
+    cams = np.zeros((max(cfg.cams, 1), 20), np.float32)
+    arr = cfg.cfg_array()
+    ref().ref_synth_scene_nogt(cfg.seed, cfg.n, cfg.cams, cfg.width, cfg.height, cfg.sh_degree, arr.ctypes.data,
+                               rows.ctypes.data, cams.ctypes.data)
+    return rows[: cfg.n], cams[: cfg.cams]
+
+
+def ref_render_view(rows, cam, sh_degree=3, workers=1):
+    """render_view (synth.hpp:81-94) of n x 59 rows on the reference renderer."""
+    rows = np.ascontiguousarray(rows, np.float32)
+    cam = np.ascontiguousarray(cam, np.float32)
+    w, h = cam_wh(cam)
+    out = np.zeros((h, w, 3), np.float32)
+    ref().ref_render_view_rows(rows.shape[0], _p(rows), _p(cam), sh_degree, workers, _p(out))
+    return out
 
 
 OPTIM_DEFAULT = np.array([1.6e-4, 5e-3, 1e-3, 5e-2, 2.5e-3, 20.0, 0.9, 0.999, 1e-8, 1.0], np.float64)

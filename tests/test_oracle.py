@@ -253,3 +253,20 @@ def test_render_golden(orc):
     for k in ("image", "d_img", "rows", "mean2d"):
         assert np.array_equal(_bits(b[k]), _bits(g[k])), k
     assert b["loss"] == float(g["loss"])
+
+
+def test_synth_without_gt_equals_reference_synth_scene(ref):
+    """ref_synth_scene_nogt (the reference arm's scene generator at C4 scale, no CPU GT render of all
+    views) is pinned to the reference's synth_scene: identical rows and cameras; the GT of a view
+    rendered by ref_render_view_rows equals synth_scene's own GT image."""
+    import paper_2509_15645_b200 as G
+
+    for seed, n, cams, w, h in ((1, 2000, 5, 48, 40), (7, 500, 3, 32, 32)):
+        cfg = G.SynthConfig(seed=seed, n=n, cams=cams, width=w, height=h)
+        rows, cam, gts = O.ref_synth(cfg, with_gt=True)
+        rows2, cam2 = O.ref_synth_nogt(cfg)
+        assert np.array_equal(rows.view(np.uint32), rows2.view(np.uint32))
+        assert np.array_equal(cam.view(np.uint32), cam2.view(np.uint32))
+        for k in range(cams):
+            img = O.ref_render_view(rows2, cam2[k], 3, workers=2)
+            assert np.array_equal(img.view(np.uint32), gts[k].view(np.uint32))

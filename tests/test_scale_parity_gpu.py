@@ -86,6 +86,14 @@ def test_c2_view_forward_backward_vs_reference(c2, ref, parity_log):
         assert sm["max_rel_err"] <= 1e-4, sm
 
 
+def _col_lr(groups, dim):
+    """Learning rate of every column from the arena's group table (store.hpp:129-136)."""
+    lr = np.zeros(dim)
+    for g in groups:
+        lr[g.col0: g.col0 + g.dim] = g.hp.lr
+    return lr
+
+
 def _ref_engine(start, cams, gts, iters, workers):
     r = O.RefEngine(start, np.stack([O.cam_from_struct(c) for c in cams[:iters]]), gts, pipelined=True,
                     workers=workers)
@@ -97,13 +105,17 @@ def _ref_engine(start, cams, gts, iters, workers):
 
 
 def _engine_vs_ref(truth, cams, iters, nongeo_on_host, parity_log, name):
-    """Engine vs the reference OffloadEngine. Losses, culls, counters, steps and densify counts
-    must match exactly; m, v and the statistics within 1e-4. The parameters w are held to the
-    reference's own reproducibility: the reference's backward sums per-worker partials in worker
-    order (render.hpp:538-598), so the reference at `workers` = CORES and CORES/2 disagrees with
-    itself, and Adam's first steps amplify gradient differences near zero (|g| ~ eps: the update
-    m/(sqrt(v)+eps) swings by up to lr). Our deviation from ref(CORES) must stay within 4x the
-    reference's self-deviation ref(CORES/2) vs ref(CORES) (or 1e-4, whichever is larger)."""
+    """Engine vs the reference OffloadEngine. Culls, counters, steps and densify counts must match
+    exactly, losses within 1e-4 (measured: bit-identical), m, v and the statistics within 1e-4.
+
+    The parameters w: Adam's first steps map a gradient g to lr * g / (|g| + eps) (bias-corrected
+    m/sqrt(v) at t = 1), whose slope at g ~ 0 is lr / eps. Our gradients differ from the reference's
+    by <= 1.3e-8 absolute (a different, fixed summation order; gradients are checked separately at
+    rel <= 1e-4), which is eps-sized, so a coordinate whose gradient is ~0 can take a step of +lr
+    on one side and -lr on the other. The check is therefore: at most one element per million
+    beyond rel 1e-4, and none beyond the Adam step bound 4 * iters * lr of its column's group. The
+    reference's own reproducibility (workers = CORES vs CORES/2, whose per-worker partials sum in a
+    different grouping, render.hpp:538-598) is logged beside it."""
     start = bench.training_start(truth)
     td = torch.from_numpy(truth).cuda()
     gts = np.stack([G.render_view(td, c, 3).cpu().numpy() for c in cams[:iters]])
@@ -140,9 +152,11 @@ def _engine_vs_ref(truth, cams, iters, nongeo_on_host, parity_log, name):
     assert loss_dev <= 1e-4
     for k in ("ng_m", "ng_v"):
         assert out[k] <= 1e-4, (k, out[k])
+    lr = {"geo_w": _col_lr(G.OptimConfig().geo_groups(), 10), "ng_w": _col_lr(G.OptimConfig().nongeo_groups(), 49)}
     for k in ("geo_w", "ng_w"):
-        assert out[k] <= max(1e-4, 4 * self_dev[k]), (k, out[k], self_dev[k])
-        assert over[k] <= max(1e-6, 4 * self_over[k]), (k, over[k], self_over[k])
+        assert over[k] <= 1e-6, (k, over[k], self_over[k])
+        dev = np.abs(st[k].astype(np.float64) - rs[k].astype(np.float64))
+        assert np.all(dev <= 4 * iters * lr[k][None, :]), (k, float(dev.max()))
     assert norm_dev <= 1e-4
 
 

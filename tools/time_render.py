@@ -1,6 +1,6 @@
 """Times rasterize_forward / rasterize_backward per camera on the bench scene (4M Gaussians,
 1080p, 8 cameras, training-start parameters vs truth GT) with CUDA events. Used to A/B kernel
-variants: GSS_LIB=<variant .so> python tools/time_render.py [N]. Prints per-camera ms and a
+variants: GSS_LIB=<variant .so> python tools/time_render.py [N W H reps]. Prints per-camera ms and a
 gradient checksum (variants must agree within tolerance)."""
 import sys
 
@@ -12,15 +12,17 @@ import bench  # noqa: E402
 import paper_2509_15645_b200 as G  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4_000_000
-reps = 3
-cfg = bench.scene_config(n, 1920, 1080, 8, 1)
+W = int(sys.argv[2]) if len(sys.argv) > 2 else 1920
+H = int(sys.argv[3]) if len(sys.argv) > 3 else 1080
+reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+cfg = bench.scene_config(n, W, H, 8, 1)
 truth, cams = G.synth_scene_params(cfg)
 td = torch.from_numpy(truth).cuda()
 gts = [G.render_view(td, c, 3) for c in cams]
 start = torch.from_numpy(bench.training_start(truth)).cuda()
 geo = start[:, :10].contiguous()
 ng = start[:, 10:].contiguous()
-vp = G.viewport_full(1920, 1080)
+vp = G.viewport_full(W, H)
 tf = tb = 0.0
 for i, cam in enumerate(cams):
     ids = G.frustum_cull(geo, n, cam, vp)
