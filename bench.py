@@ -208,7 +208,7 @@ def tier_placement(a, n, dev) -> str:
     geo = n * (3 * 40 + 1)
     ng = n * (640 + 1)
     staging = n * 4 * (2 * (49 + 52 + 10 + 2) + 3)  # double-buffered forward/gradient stage + plans
-    render = a.width * a.height * 4 * 24 + 512 << 20
+    render = a.width * a.height * 4 * 24 + (512 << 20)
     return "hbm" if 1.25 * (geo + ng + staging + render) < free else "host"
 
 

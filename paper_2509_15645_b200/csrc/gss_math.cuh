@@ -53,6 +53,49 @@ __device__ __forceinline__ float gss_expf_core(float x) {
   return __double2float_rn(y);
 }
 
+// The same core with the polynomial coefficients in registers (a hot loop hoists them once).
+struct ExpCoef {
+  double c0, c1, c2, c3;
+};
+__device__ __forceinline__ ExpCoef exp_coef() { return ExpCoef{kExpCoef[0], kExpCoef[1], kExpCoef[2], kExpCoef[3]}; }
+// Register-resident copy for a hot loop: the values pass through an opaque move, so the compiler
+// keeps them in registers instead of reloading the constant bank before every DFMA.
+__device__ __forceinline__ ExpCoef exp_coef_regs(const ExpCoef& k) {
+  ExpCoef r;
+  asm("mov.b64 %0, %1;" : "=d"(r.c0) : "d"(k.c0));
+  asm("mov.b64 %0, %1;" : "=d"(r.c1) : "d"(k.c1));
+  asm("mov.b64 %0, %1;" : "=d"(r.c2) : "d"(k.c2));
+  asm("mov.b64 %0, %1;" : "=d"(r.c3) : "d"(k.c3));
+  return r;
+}
+// Host copy, for kernels that take the coefficients as a parameter (param-space operands of DFMA).
+inline ExpCoef exp_coef_host() {
+  return ExpCoef{0x1.71547652b82fep+0 * 32.0, 0x1.c6af84b912394p-5 / (32.0 * 32 * 32), 0x1.ebfce50fac4f3p-3 / (32.0 * 32),
+                 0x1.62e42ff0c52d6p-1 / 32.0};
+}
+__device__ __forceinline__ float gss_expf_core(float x, const ExpCoef& k) {
+  const double shift = 0x1.8p+52;
+  const double xd = (double)x;
+  double kd = __fma_rn(k.c0, xd, shift);
+  const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
+  kd = __dsub_rn(kd, shift);
+  const double r = __fma_rn(k.c0, xd, -kd);
+  const unsigned long long t = __ldg(&kExp2Tab[ki & 31]) + (ki << 47);
+  const double s = __longlong_as_double((long long)t);
+  const double z = __fma_rn(k.c1, r, k.c2);
+  const double r2 = __dmul_rn(r, r);
+  double y = __fma_rn(k.c3, r, 1.0);
+  y = __fma_rn(z, r2, y);
+  y = __dmul_rn(y, s);
+  return __double2float_rn(y);
+}
+// gss_expf_nonpos without a branch: the core runs for every x and the underflow guard selects 0
+// (x < -103.97, including -inf); NaN flows through the core (NaN in, NaN out, as glibc's x + x).
+__device__ __forceinline__ float gss_expf_nonpos_sel(float x, const ExpCoef& k) {
+  const float y = gss_expf_core(x, k);
+  return x < -0x1.9fe368p6f ? 0.0f : y;
+}
+
 __device__ __forceinline__ float gss_expf(float x) {
   if (!(x <= 0x1.62e42ep6f)) {                 // > 88.72 (overflow), +inf or NaN
     if (x != x) return x + x;

@@ -22,6 +22,7 @@
 #include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstring>
 #include <vector>
 
@@ -509,7 +510,20 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
                                                            int32_t* last_out, int32_t* ncontrib_out,
                                                            const float* gt, int gt_width, float inv_norm,
                                                            float* d_img, double* loss_partials,
-                                                           unsigned long long* contribs_total) {
+                                                           unsigned long long* contribs_total, ExpCoef ekp) {
+  // exp coefficients staged through SMEM into registers (kept there for the whole kernel instead
+  // of a constant-bank load before every DFMA)
+#ifndef GSS_FWD_COEF_SMEM
+#define GSS_FWD_COEF_SMEM 1
+#endif
+#if GSS_FWD_COEF_SMEM
+  __shared__ ExpCoef shek;
+  if (threadIdx.x == 0) shek = ekp;
+  __syncthreads();
+  const ExpCoef ek = shek;
+#else
+  const ExpCoef& ek = ekp;
+#endif
   __shared__ SplatRec sh[kFwdBatch];
   __shared__ double red[kFwdWarps];
   const int tile = tile_of(tile_order);
@@ -521,9 +535,11 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
   const float cx = (float)x + 0.5f;
   const int2 rg = ranges[tile];
   // Pixel h of this thread: row fy0 + (lane >> 3) + 4h of the warp's 8 x kFwdBlockRows block.
-  int y[kFwdPPT], used[kFwdPPT], last[kFwdPPT];
+  // yb: the row used by the box tests (a pixel outside the window never meets a box). A pixel is
+  // finished once T < 1e-4 (render.hpp:442): no later contribution changes T, so the T test alone
+  // is the reference's early stop.
+  int y[kFwdPPT], yb[kFwdPPT], used[kFwdPPT], last[kFwdPPT];
   float cy[kFwdPPT], T[kFwdPPT], c0[kFwdPPT], c1[kFwdPPT], c2[kFwdPPT];
-  bool done[kFwdPPT];
   bool all_done = true;
 #if GSS_RASTER_STATS
   unsigned long long st_walk = 0, st_box = 0, st_eval = 0, st_slots = 0;
@@ -535,8 +551,9 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
     T[h] = 1.0f;
     c0[h] = c1[h] = c2[h] = 0.0f;
     used[h] = last[h] = 0;
-    done[h] = !(x < w.px0 + w.pw && y[h] < w.py0 + w.ph);
-    all_done &= done[h];
+    const bool inwin = x < w.px0 + w.pw && y[h] < w.py0 + w.ph;
+    yb[h] = inwin ? y[h] : INT_MIN;
+    all_done &= !inwin;
   }
   for (int b = rg.x; b < rg.y; b += kFwdBatch) {
     if (__syncthreads_count(all_done) == kFwdThreads) break;
@@ -560,37 +577,57 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
       while (m) {
         const int j = c0j + __ffs(m) - 1;
         m &= m - 1;
-        const SplatRec& r = sh[j];
-        const int4 bx = *reinterpret_cast<const int4*>(&r.bx0);
+        // Record fields in registers once per record (both pixels of the lane share them):
+        // q0 = mx, my, a, b; q1 = c, ab, r, g; q2 = bl, RN(1/det), off, det; bx = box.
+        const float4* rp = reinterpret_cast<const float4*>(&sh[j]);
+        const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
+        const int4 bx = *reinterpret_cast<const int4*>(&sh[j].bx0);
         const bool xin = (x >= bx.x) & (x < bx.y);
+        // contrib_eval's numerator c*dx*dx - 2*b*dx*dy + a*dy*dy (render.hpp:346) in the reference's
+        // operation order; the x-only factors are shared by the lane's pixels (same column).
+        const float dx = cx - q0.x;
+        const float cdxdx = (q1.x * dx) * dx;
+        const float b2dx = (2.0f * q0.w) * dx;
+        const int lastv = b + j - rg.x + 1;
+        // Markstein quotient range (div_rcp_rn): |num| in [2^-60, 2^60) and a usable RN(1/det);
+        // a record without one (rd == 0) sends every quotient to the IEEE division.
+        const float lo = q2.y != 0.0f ? 0x1p-60f : __int_as_float(0x7f800000);
 #pragma unroll
         for (int h = 0; h < kFwdPPT; ++h) {
+          const bool inb = xin & (yb[h] >= bx.z) & (yb[h] < bx.w);
+          const bool ev = inb & !(T[h] < 1e-4f);  // render.hpp:442: T-stop before the contribution
 #if GSS_RASTER_STATS
-          {
-            const bool inb = xin & (y[h] >= bx.z) & (y[h] < bx.w);
-            const bool evb = inb & !done[h] & !(T[h] < 1e-4f);
-            st_box += inb ? 1 : 0;
-            st_eval += evb ? 1 : 0;
-            if (__ballot_sync(0xffffffffu, evb) && lane == 0) st_slots += 32;
-          }
+          st_box += inb ? 1 : 0;
+          st_eval += ev ? 1 : 0;
+          if (__ballot_sync(0xffffffffu, ev) && lane == 0) st_slots += 32;
 #endif
-          if (!(!done[h] & xin & (y[h] >= bx.z) & (y[h] < bx.w))) continue;
-          if (T[h] < 1e-4f) {
-            done[h] = true;
-            continue;
+          if (!__any_sync(0xffffffffu, ev)) continue;  // warp-uniform skip
+          const float dy = cy[h] - q0.y;
+          const float num = (cdxdx - b2dx * dy) + (q0.z * dy) * dy;
+          const float qf = __fmul_rn(num, q2.y);
+          float quo = __fmaf_rn(__fmaf_rn(-q2.w, qf, num), q2.y, qf);
+          const float an = fabsf(num);
+          const bool slow = !((an >= lo) & (an < 0x1p60f));
+          if (__any_sync(0xffffffffu, slow)) {  // rare: zero / extreme numerators, extreme det
+            if (slow) quo = __fdiv_rn(num, q2.w);
           }
-          const EvalOut ev = contrib_eval(r, cx, cy[h], r.depth);
-          c0[h] += r.r * ev.alpha * T[h];
-          c1[h] += r.g * ev.alpha * T[h];
-          c2[h] += r.bl * ev.alpha * T[h];
-          T[h] *= (1.0f - ev.alpha);
-          ++used[h];
-          last[h] = b + j - rg.x + 1;
+          const float xe = -0.5f * max0(quo);
+          const float wgt = gss_expf_nonpos_sel(xe, ek);
+          const float raw = q1.y * wgt;
+          const float alpha = raw > 0.999f ? 0.999f : raw;
+          if (ev) {
+            c0[h] += q1.z * alpha * T[h];
+            c1[h] += q1.w * alpha * T[h];
+            c2[h] += q2.x * alpha * T[h];
+            T[h] *= (1.0f - alpha);
+            ++used[h];
+            last[h] = lastv;
+          }
         }
       }
       all_done = true;
 #pragma unroll
-      for (int h = 0; h < kFwdPPT; ++h) all_done &= done[h];
+      for (int h = 0; h < kFwdPPT; ++h) all_done &= (yb[h] == INT_MIN) | (T[h] < 1e-4f);
     }
     __syncthreads();
   }
@@ -720,8 +757,8 @@ struct PixB {
 // Per-splat constants of the backward sweep, computed once per batch: the conic (inverse 2D
 // covariance) so the per-pixel exponent needs no division.
 struct BwdConic {
-  float ia, ib, ic;  // c/det, b/det, a/det
-  float nh;          // -0.5/det
+  float ia, ibm2, ic;  // c/det, -2*b/det, a/det
+  float nh;            // -0.5/det
 };
 
 __device__ __forceinline__ float ex2_fast(float x) {
@@ -735,6 +772,123 @@ __device__ __forceinline__ float rcp_fast(float x) {
   return r;
 }
 
+// One contribution of splat r (sweep position jpos) to pixel p of the reverse sweep
+// (render.hpp:554-589): steps the pixel's reverse state and accumulates 10 per-lane sums
+//   v[0..2] = sum alpha*T*g_rgb                      (rgb gradient)
+//   v[3]    = sum t,  t = weight * d_alpha (0 when the 0.999 clamp is active)   (alpha_base gradient)
+//   v[4..9] = sum t*q, t*dx^2, t*dy^2, t*dx*dy, t*dx, t*dy
+// from which the per-record combine (sweep_combine) forms the mean2d and cov gradients:
+// dq_i = alpha * d_alpha * (-0.5/det) = ab * nh * t, and the reference's per-contribution terms
+// dqi * (2b*dy - 2c*dx) ... are linear in these moments with per-splat coefficients. The arithmetic
+// runs on fast math with explicit FMAs (tolerance-checked); the 0.999 clamp decision,
+// which selects the reference's branch (render.hpp:560-573), is recomputed with the forward's exact
+// arithmetic whenever the fast alpha is within 1e-4 of the threshold, so both passes always take the
+// same branch. Predicated: a lane whose pixel is outside the record's box (or past its last index)
+// adds exact zeros and keeps its state.
+__device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k, bool xin, int jpos, PixB& p,
+                                            float v[10]) {
+  const bool ok = xin & (jpos < p.L) & (p.y >= r.by0) & (p.y < r.by1);
+  const float dx = p.cx - r.mx, dy = p.cy - r.my;
+  const float dxx = dx * dx, dyy = dy * dy, dxy = dx * dy;
+  float q = __fmaf_rn(k.ia, dxx, __fmaf_rn(k.ic, dyy, k.ibm2 * dxy));
+  q = (q < 0.0f || !ok) ? 0.0f : q;  // an idle lane evaluates at q = 0: every term stays finite
+  const float weight = ex2_fast(-0.72134752f * q);  // exp(-q/2)
+  float raw = r.ab * weight;
+  const bool near = ok && fabsf(raw - 0.999f) < 1e-4f;
+  if (__any_sync(0xffffffffu, near)) {
+    if (near) raw = contrib_eval(r, p.cx, p.cy).clamped ? 1.0f : 0.0f;
+  }
+  const bool clamped = raw > 0.999f;
+  const float alpha = ok ? (clamped ? 0.999f : r.ab * weight) : 0.0f;
+  const float inv1m = rcp_fast(1.0f - alpha);
+  const float Tb = ok ? p.T * inv1m : p.T;  // transmittance before this contribution
+  const float w_rgb = alpha * Tb;
+  v[0] = __fmaf_rn(w_rgb, p.g0, v[0]);
+  v[1] = __fmaf_rn(w_rgb, p.g1, v[1]);
+  v[2] = __fmaf_rn(w_rgb, p.g2, v[2]);
+  const float dot_c = __fmaf_rn(r.r, p.g0, __fmaf_rn(r.g, p.g1, r.bl * p.g2));
+  const float dot_suf = __fmaf_rn(p.s0, p.g0, __fmaf_rn(p.s1, p.g1, p.s2 * p.g2));
+  const float d_alpha = __fmaf_rn(Tb, dot_c, -dot_suf * inv1m);
+  p.s0 = __fmaf_rn(r.r, w_rgb, p.s0);
+  p.s1 = __fmaf_rn(r.g, w_rgb, p.s1);
+  p.s2 = __fmaf_rn(r.bl, w_rgb, p.s2);
+  p.T = Tb;
+  const float t = (ok && !clamped) ? weight * d_alpha : 0.0f;  // render.hpp:572-586 only when not clamped
+  v[3] += t;
+  v[4] = __fmaf_rn(t, q, v[4]);
+  v[5] = __fmaf_rn(t, dxx, v[5]);
+  v[6] = __fmaf_rn(t, dyy, v[6]);
+  v[7] = __fmaf_rn(t, dxy, v[7]);
+  v[8] = __fmaf_rn(t, dx, v[8]);
+  v[9] = __fmaf_rn(t, dy, v[9]);
+  return ok;
+}
+
+// The 9 SlotAcc terms (rgb3, mean2d2, cov3, alpha_base; render.hpp:538) of one record from its 10
+// swept sums (bwd_contrib): with f = ab * (-0.5/det),
+//   mean2d = f * (2b*Sy - 2c*Sx, 2b*Sx - 2a*Sy),  cov = f * (Syy - c*Sq, 2b*Sq - 2*Sxy, Sxx - a*Sq).
+__device__ __forceinline__ void sweep_combine(const SplatRec& r, const BwdConic& k, const float u[10], float o[9]) {
+  const float f = r.ab * k.nh, b2 = 2.0f * r.b;
+  o[0] = u[0];
+  o[1] = u[1];
+  o[2] = u[2];
+  o[3] = f * __fmaf_rn(b2, u[9], -2.0f * r.c * u[8]);
+  o[4] = f * __fmaf_rn(b2, u[8], -2.0f * r.a * u[9]);
+  o[5] = f * __fmaf_rn(-r.c, u[4], u[6]);
+  o[6] = f * __fmaf_rn(b2, u[4], -2.0f * u[7]);
+  o[7] = f * __fmaf_rn(-r.a, u[4], u[5]);
+  o[8] = u[3];
+}
+
+// Warp reduce-scatter of 10 values in 12 shuffles (10 x 5 butterflies would take 50; padding to 16
+// takes 16): the value set is halved per lane bit with minimal padding, 10 -> 5 -> 3 -> 2 -> 1
+// (bits 4, 3, 2, 1), then lanes 2k and 2k+1 add. Afterwards lane l holds the warp total of value
+// index reduce_scatter_index(l) (-1: a padding slot). Fixed order: deterministic.
+__device__ __forceinline__ int reduce_scatter_index(int lane) {
+  const int j3 = ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);  // of the 3-set (3 = padding)
+  const int j5 = ((lane >> 3) & 1) * 3 + j3;                   // of the 5-set (5.. = padding)
+  const int j10 = ((lane >> 4) & 1) * 5 + j5;                  // of the 10 values (9 = padding)
+  return (j3 < 3 && j5 < 5 && j10 < 10) ? j10 : -1;
+}
+__device__ __forceinline__ float warp_reduce_scatter10(const float v[10], int lane) {
+  float x[5];
+  {  // bit 4: 10 values -> 5
+    const bool up = (lane & 16) != 0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const float lo = v[i], hi = v[i + 5];
+      x[i] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, 16);
+    }
+  }
+  float y[3];
+  {  // bit 3: 5 values (+1 padding) -> 3
+    const bool up = (lane & 8) != 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const float lo = x[i], hi = i + 3 < 5 ? x[i + 3] : 0.0f;
+      y[i] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, 8);
+    }
+  }
+  float z[2];
+  {  // bit 2: 3 values (+1 padding) -> 2
+    const bool up = (lane & 4) != 0;
+    const float hi1 = 0.0f;
+    z[0] = (up ? y[2] : y[0]) + __shfl_xor_sync(0xffffffffu, up ? y[0] : y[2], 4);
+    z[1] = (up ? hi1 : y[1]) + __shfl_xor_sync(0xffffffffu, up ? y[1] : hi1, 4);
+  }
+  const bool up = (lane & 2) != 0;  // bit 1: 2 values -> 1
+  const float u = (up ? z[1] : z[0]) + __shfl_xor_sync(0xffffffffu, up ? z[0] : z[1], 2);
+  return u + __shfl_xor_sync(0xffffffffu, u, 1);
+}
+
+#ifndef GSS_BWD_MOMENTS
+#define GSS_BWD_MOMENTS 1
+#endif
+#ifndef GSS_BWD_SKIP
+#define GSS_BWD_SKIP 0
+#endif
+#if !GSS_BWD_MOMENTS
+// Round-1 sweep (A/B reference): 9 per-pixel gradient terms.
 // One contribution of splat r (sweep position jpos) to pixel p: accumulates its 9 screen-space
 // gradient terms into v and steps the pixel's reverse state. Returns whether it contributed.
 // The gradient arithmetic runs on fast math with explicit FMAs (tolerance-checked);
@@ -744,11 +898,11 @@ __device__ __forceinline__ float rcp_fast(float x) {
 // Predicated form: every lane evaluates the contribution and a lane whose pixel is outside the
 // record's box (or past its last index) adds exact zeros and keeps its state, so the two pixels of
 // a thread form one branch-free block the scheduler can interleave.
-__device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k, int jpos, PixB& p, float v[9]) {
+__device__ __forceinline__ bool bwd_contrib9(const SplatRec& r, const BwdConic& k, int jpos, PixB& p, float v[9]) {
   const bool ok = (jpos < p.L) & (p.x >= r.bx0) & (p.x < r.bx1) & (p.y >= r.by0) & (p.y < r.by1);
   const float dx = p.cx - r.mx, dy = p.cy - r.my;
   const float mdxy2 = -2.0f * dx * dy;
-  float q = __fmaf_rn(k.ia * dx, dx, __fmaf_rn(k.ic * dy, dy, k.ib * mdxy2));
+  float q = __fmaf_rn(k.ia * dx, dx, __fmaf_rn(k.ic * dy, dy, (-0.5f * k.ibm2) * mdxy2));
   q = (q < 0.0f || !ok) ? 0.0f : q;  // an idle lane evaluates at q = 0: every term stays finite
   const float weight = ex2_fast(-0.72134752f * q);  // exp(-q/2)
   float raw = r.ab * weight;
@@ -821,6 +975,8 @@ __device__ __forceinline__ float warp_reduce_scatter9(const float v[9], int lane
   return u + __shfl_xor_sync(0xffffffffu, u, 1);
 }
 
+#endif
+
 // Reverse sweep (render.hpp:542-589) per 16x16 tile: 64 threads, 4 pixels each (rows ly, ly + 2,
 // ly + 4, ly + 6 of an 8-row warp band), so a splat's 9 gradient terms are pre-summed per lane
 // over 4 pixels (predicated, interleavable) and reduced once per warp. Per batch, each warp ballots which records can reach its band (pixel
@@ -845,7 +1001,12 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
   __shared__ SplatRec sh[kBwdBatch];
   __shared__ BwdConic shk[kBwdBatch];
   __shared__ int32_t sinst[kBwdBatch];  // the record's (splat, this tile) instance index
-  __shared__ float red[kBwdBatch][kBwdWarps][9];
+#if GSS_BWD_MOMENTS
+  constexpr int kNv = 10;
+#else
+  constexpr int kNv = 9;
+#endif
+  __shared__ float red[kBwdBatch][kBwdWarps][kNv];
   __shared__ unsigned long long wmask[kBwdWarps][kBwdMasks];
   __shared__ int smax;
   const int tile = tile_of(tile_order);
@@ -886,7 +1047,11 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
   if (lane == 0 && wl > 0) atomicMax(&smax, wl);
   __syncthreads();
   const int Lmax = smax;
+#if GSS_BWD_MOMENTS
+  const int vidx = reduce_scatter_index(lane);
+#else
   const int vidx = reduce_scatter9_index(lane);
+#endif
 #if GSS_RASTER_STATS
   unsigned long long st_walk = 0, st_use = 0;
 #endif
@@ -898,7 +1063,7 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
       load_rec(&sh[j], recs, vals[rg.x + bstart + j]);
       const SplatRec& r = sh[j];
       const float inv = 1.0f / r.det;  // det > 0 for every binned splat
-      shk[j] = BwdConic{r.c * inv, r.b * inv, r.a * inv, -0.5f * inv};
+      shk[j] = BwdConic{r.c * inv, -2.0f * (r.b * inv), r.a * inv, -0.5f * inv};
       int tx0, ty0, ntx, nty;
       tile_box(r, w, tx0, ty0, ntx, nty);
       sinst[j] = r.off + (ty - ty0) * ntx + (tx - tx0);
@@ -948,25 +1113,43 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
 #endif
         const SplatRec r = sh[jj];
         const BwdConic k = shk[jj];
-        float v[9];
+        const bool xin = (px[0].x >= r.bx0) & (px[0].x < r.bx1);
+        float v[kNv];
 #pragma unroll
-        for (int i = 0; i < 9; ++i) v[i] = 0.0f;
-#if GSS_RASTER_STATS
+        for (int i = 0; i < kNv; ++i) v[i] = 0.0f;
+#if GSS_RASTER_STATS && GSS_BWD_MOMENTS
         ++st_walk;
 #pragma unroll
-        for (int q = 0; q < kBwdPPT; ++q) st_use += bwd_contrib(r, k, bstart + jj, px[q], v) ? 1 : 0;
-#else
+        for (int q = 0; q < kBwdPPT; ++q) st_use += bwd_contrib(r, k, xin, bstart + jj, px[q], v) ? 1 : 0;
+#elif GSS_BWD_MOMENTS && GSS_BWD_SKIP
+        // warp-uniform skip of the pixel slots (row pairs of the band) the record's box misses
+        {
+          const int r0 = r.by0 - by0w, r1 = r.by1 - by0w;  // box rows relative to the band
 #pragma unroll
-        for (int q = 0; q < kBwdPPT; ++q) bwd_contrib(r, k, bstart + jj, px[q], v);
+          for (int q = 0; q < kBwdPPT; ++q)
+            if (r0 < 2 * q + 2 && r1 > 2 * q) bwd_contrib(r, k, xin, bstart + jj, px[q], v);
+        }
+#elif GSS_BWD_MOMENTS
+#pragma unroll
+        for (int q = 0; q < kBwdPPT; ++q) bwd_contrib(r, k, xin, bstart + jj, px[q], v);
+#else
+        (void)xin;
+#pragma unroll
+        for (int q = 0; q < kBwdPPT; ++q) bwd_contrib9(r, k, bstart + jj, px[q], v);
 #endif
         // A record no lane contributed to reduces exact zeros: the same partial without a vote.
+#if GSS_BWD_MOMENTS
+        const float tot = warp_reduce_scatter10(v, lane);
+#else
         const float tot = warp_reduce_scatter9(v, lane);
+#endif
         if ((lane & 1) == 0 && vidx >= 0) red[jj][warp][vidx] = tot;
       }
     }
     __syncthreads();
-    // Fixed-order cross-warp sum over the warps that walked the record: one instance partial per
-    // splat of the batch.
+    // Fixed-order cross-warp sum over the warps that walked the record, then the record's 9 SlotAcc
+    // terms: one instance partial per splat of the batch (a thread per record).
+#if !GSS_BWD_MOMENTS
     for (int e = threadIdx.x; e < nb * 9; e += kBwdThreads) {
       const int jj = e / 9, i = e - jj * 9;
       float s = 0.0f;
@@ -975,6 +1158,23 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
         if ((wmask[q][jj >> 6] >> (jj & 63)) & 1ull) s += red[jj][q][i];
       partials[(int64_t)sinst[jj] * 9 + i] = s;
     }
+#else
+    for (int jj = threadIdx.x; jj < nb; jj += kBwdThreads) {
+      float u[10];
+#pragma unroll
+      for (int i = 0; i < 10; ++i) u[i] = 0.0f;
+#pragma unroll
+      for (int q = 0; q < kBwdWarps; ++q)
+        if ((wmask[q][jj >> 6] >> (jj & 63)) & 1ull)
+#pragma unroll
+          for (int i = 0; i < 10; ++i) u[i] += red[jj][q][i];
+      float o[9];
+      sweep_combine(sh[jj], shk[jj], u, o);
+      float* dst = partials + (int64_t)sinst[jj] * 9;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) dst[i] = o[i];
+    }
+#endif
   }
 #if GSS_RASTER_STATS
   if (lane == 0) {
@@ -1457,7 +1657,7 @@ void composite_phase(gss_render_ctx* ctx, const Win& w, int64_t V, const FwdOut&
                                              static_cast<const int2*>(ctx->ranges.p),
                                              static_cast<const int32_t*>(ctx->tile_order.p), w, s.bg[0], s.bg[1], s.bg[2],
                                              o.image, fT, last, o.ncontrib, o.gt, o.gt_width, o.inv, o.d_img, lp,
-                                             ctx->ktiming ? ctx->contribs_dev : nullptr);
+                                             ctx->ktiming ? ctx->contribs_dev : nullptr, exp_coef_host());
   GSS_LAUNCHED();
   ktime_end(ctx, st);
   if (o.gt) {

@@ -28,7 +28,7 @@ for i, cam in enumerate(cams):
     ids = G.frustum_cull(geo, n, cam, vp)
     sc = G.RenderScene(ids=ids, geo=geo, nongeo=ng)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    fms = bms = 0.0
+    fl, bl = [], []
     for r in range(reps + 1):
         ev[0].record()
         fw = G.rasterize_forward(sc, cam, vp, gt=gts[i])
@@ -37,8 +37,9 @@ for i, cam in enumerate(cams):
         ev[2].record()
         torch.cuda.synchronize()
         if r:
-            fms += ev[0].elapsed_time(ev[1]) / reps
-            bms += ev[1].elapsed_time(ev[2]) / reps
+            fl.append(ev[0].elapsed_time(ev[1]))
+            bl.append(ev[1].elapsed_time(ev[2]))
+    fms, bms = float(np.median(fl)), float(np.median(bl))  # median of the timed repetitions
     tf += fms
     tb += bms
     cs = float(gb.rows.double().abs().sum())
