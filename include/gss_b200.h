@@ -296,6 +296,23 @@ int64_t gss_engine_launches(gss_engine* e);
  * returns ms2[0..1] = total ms of the composite / sweep launches since the last call, n2[0..1] =
  * their launch counts, *contribs = contributions composited (= useful backward contributions). */
 int gss_engine_kernel_timing(gss_engine* e, int32_t on);
+/* TimelineRow (engine.hpp:22-28): one row per stage of every iteration since the timeline was
+ * enabled; stage 0..5 = cull, forward_params, render, geo_update, handoff, lazy_update; worker 0 =
+ * the device stream, 1 = the host-tier stream; t0/t1 = CUDA-event times in ns from the epoch
+ * recorded by gss_engine_timeline_enable; bytes = the stage's algorithmic bytes (lazy update: the
+ * reference tally 7*49*4 per touched row + n counter bytes, from the device touched count). */
+typedef struct {
+  int32_t iteration, stage, worker, pad;
+  int64_t t0_ns, t1_ns;
+  uint64_t bytes;
+} gss_timeline_row;
+int gss_engine_timeline_enable(gss_engine* e, int32_t on);
+/* Drains, copies min(count, cap) rows, returns the row count (negative status on error). */
+int64_t gss_engine_timeline(gss_engine* e, gss_timeline_row* rows, int64_t cap);
+/* Test instrumentation (the reference's EngineConfig::stage_hook, engine.hpp:42-43): a device-side
+ * sleep of ns[k % n] nanoseconds at the start of the k-th stage on that stage's stream, to shake the
+ * two-stream schedule; n = 0 disables. Results must not change (every edge is an event). */
+int gss_engine_stage_delays(gss_engine* e, const uint32_t* ns, int32_t n);
 int gss_engine_kernel_times(gss_engine* e, double* ms2, int64_t* n2, uint64_t* contribs);
 
 /* ---- densification (trainer.hpp:166-213, engine.hpp:116-163) ------------- */

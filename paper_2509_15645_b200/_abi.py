@@ -174,6 +174,9 @@ SIGNATURES = {
     "gss_look_at_camera": (C.c_int, [P, P, F32, F32, I32, I32, F32, F32, C.POINTER(GssCamera)]),
     "gss_raster_stats": (C.c_int, [P, I32]),
     "gss_engine_kernel_timing": (C.c_int, [P, I32]),
+    "gss_engine_timeline_enable": (C.c_int, [P, I32]),
+    "gss_engine_timeline": (I64, [P, P, I64]),
+    "gss_engine_stage_delays": (C.c_int, [P, P, I32]),
     "gss_engine_kernel_times": (C.c_int, [P, P, P, P]),
     "gss_raster_stats_enabled": (I32, []),
     "gss_ply_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),

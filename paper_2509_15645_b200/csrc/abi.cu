@@ -78,6 +78,9 @@ void engine_accum(gss_engine* e, double* norm, int32_t* cnt);
 void engine_stage_ms(gss_engine* e, double* out6);
 int64_t engine_launches(gss_engine* e);
 void engine_kernel_timing(gss_engine* e, bool on);
+void engine_timeline_enable(gss_engine* e, bool on);
+int64_t engine_timeline(gss_engine* e, gss_timeline_row* rows, int64_t cap);
+void engine_stage_delays(gss_engine* e, const uint32_t* ns, int n);
 void engine_kernel_times(gss_engine* e, double* ms2, int64_t* n2, uint64_t* contribs);
 int64_t engine_count(gss_engine* e);
 
@@ -431,6 +434,17 @@ GSS_API int gss_engine_stage_ms(gss_engine* e, double* out6) {
 GSS_API int64_t gss_engine_launches(gss_engine* e) { return engine_launches(e); }
 GSS_API int gss_engine_kernel_timing(gss_engine* e, int32_t on) {
   return guarded([&] { engine_kernel_timing(e, on != 0); });
+}
+GSS_API int gss_engine_timeline_enable(gss_engine* e, int32_t on) {
+  return guarded([&] { engine_timeline_enable(e, on != 0); });
+}
+GSS_API int64_t gss_engine_timeline(gss_engine* e, gss_timeline_row* rows, int64_t cap) {
+  int64_t n = 0;
+  const int st = guarded([&] { n = engine_timeline(e, rows, cap); });
+  return st == GSS_OK ? n : -st;
+}
+GSS_API int gss_engine_stage_delays(gss_engine* e, const uint32_t* ns, int32_t n) {
+  return guarded([&] { engine_stage_delays(e, ns, n); });
 }
 GSS_API int gss_engine_kernel_times(gss_engine* e, double* ms2, int64_t* n2, uint64_t* contribs) {
   return guarded([&] { engine_kernel_times(e, ms2, n2, contribs); });

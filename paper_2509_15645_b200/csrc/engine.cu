@@ -15,6 +15,8 @@
 // w/m/v + uint8 counters, defer_max) lives in HBM (scene fits: 180 GB) or, with
 // nongeo_on_host, in pinned host memory read by the forwarding gather through the PCIe/C2C
 // mapping and updated lazily in place (zero-copy), see DESIGN.md §offload.
+#include <nvtx3/nvToolsExt.h>
+
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -111,6 +113,20 @@ struct Ev {
 };
 
 enum Stage { kCull = 0, kFwd, kRender, kGeo, kHandoff, kLazy, kStages };
+const char* const kStageName[kStages] = {"cull", "forward_params", "render", "geo_update", "handoff", "lazy_update"};
+
+// Test instrumentation (the reference's EngineConfig::stage_hook delays, engine.hpp:42-43,
+// test_offload.cpp:268-285): a device-side sleep at the start of a stage on the stage's stream.
+__global__ void stage_delay_kernel(uint32_t ns) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 >= ns) break;
+    __nanosleep(1000);
+  }
+}
 
 }  // namespace
 }  // namespace gssd
@@ -161,10 +177,23 @@ struct gss_engine {
   struct TimeRec {
     int stage;
     cudaEvent_t a, b;
+    int iter;
+    int worker;      // 0: device stream (stream D), 1: host-tier stream (stream H), as TimelineRow::worker
+    uint64_t bytes;  // algorithmic bytes of the stage (lazy update from its touched count)
+    int touched_slot;
   };
   std::vector<cudaEvent_t> ev_free;
   std::vector<TimeRec> pending_times;
   double stage_ms[gssd::kStages] = {0, 0, 0, 0, 0, 0};
+  // Per-iteration timeline (engine.hpp:22-28, 230-237): rows are kept when enabled; times are
+  // CUDA-event offsets from the epoch event recorded when the timeline was enabled.
+  bool timeline_on = false;
+  cudaEvent_t epoch = nullptr;
+  std::vector<gss_timeline_row> timeline;
+  int64_t* touched_ring = nullptr;  // device: touched counts of the lazy updates in flight
+  int touched_next = 0;
+  std::vector<uint32_t> delays_ns;  // stage-delay injection (test instrumentation)
+  size_t delay_next = 0;
   // iteration bookkeeping
   int next_iter = 0;
   int seg_begin = 0;
@@ -211,23 +240,52 @@ cudaEvent_t take_event(gss_engine* e) {
   GSS_CUDA(cudaEventCreate(&ev));
   return ev;
 }
-void stage_begin(gss_engine* e, int st, cudaStream_t s, int) {
-  gss_engine::TimeRec r{st, take_event(e), take_event(e)};
+constexpr int kTouchedRing = 64;
+void stage_begin(gss_engine* e, int st, cudaStream_t s, int g, uint64_t bytes = 0, int touched_slot = -1) {
+  nvtxRangePushA(kStageName[st]);
+  if (!e->delays_ns.empty()) {
+    stage_delay_kernel<<<1, 1, 0, s>>>(e->delays_ns[e->delay_next++ % e->delays_ns.size()]);
+    GSS_LAUNCHED();
+  }
+  gss_engine::TimeRec r{st, take_event(e), take_event(e), g, s == e->sH ? 1 : 0, bytes, touched_slot};
   GSS_CUDA(cudaEventRecord(r.a, s));
   e->pending_times.push_back(r);
 }
 void stage_end(gss_engine* e, int st, cudaStream_t s, int) {
+  nvtxRangePop();
   for (auto it = e->pending_times.rbegin(); it != e->pending_times.rend(); ++it)
     if (it->stage == st) {
       GSS_CUDA(cudaEventRecord(it->b, s));
       return;
     }
 }
+void timeline_push(gss_engine* e, const gss_engine::TimeRec& r, const int64_t* touched_host) {
+  if (!e->timeline_on || !e->epoch) return;
+  float t0 = 0.0f, t1 = 0.0f;
+  if (cudaEventElapsedTime(&t0, e->epoch, r.a) != cudaSuccess || cudaEventElapsedTime(&t1, e->epoch, r.b) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  gss_timeline_row row{};
+  row.iteration = r.iter;
+  row.stage = r.stage;
+  row.worker = r.worker;
+  row.t0_ns = (int64_t)((double)t0 * 1e6);
+  row.t1_ns = (int64_t)((double)t1 * 1e6);
+  row.bytes = r.bytes;
+  if (r.touched_slot >= 0 && touched_host)  // adam.hpp:234-236: 7*dim*4 per touched row + 1 counter byte per row
+    row.bytes = (uint64_t)touched_host[r.touched_slot] * 7u * kNgDim * 4u + (uint64_t)e->n;
+  e->timeline.push_back(row);
+}
 // After a drain: fold the recorded stage intervals into stage_ms and recycle the events.
 void collect_times(gss_engine* e) {
+  int64_t touched[kTouchedRing] = {};
+  if (e->timeline_on && e->touched_ring)
+    GSS_CUDA(cudaMemcpy(touched, e->touched_ring, sizeof touched, cudaMemcpyDeviceToHost));
   for (auto& r : e->pending_times) {
     float ms = 0.0f;
     if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) e->stage_ms[r.stage] += ms;
+    timeline_push(e, r, touched);
     e->ev_free.push_back(r.a);
     e->ev_free.push_back(r.b);
   }
@@ -245,6 +303,7 @@ void collect_completed(gss_engine* e) {
     }
     float ms = 0.0f;
     if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) e->stage_ms[r.stage] += ms;
+    timeline_push(e, r, nullptr);
     e->ev_free.push_back(r.a);
     e->ev_free.push_back(r.b);
   }
@@ -256,7 +315,7 @@ void collect_completed(gss_engine* e) {
 void stage_cull(gss_engine* e, int g, const gss_camera& cam) {
   const int p = g % 3;
   cudaStream_t s = e->sD;
-  stage_begin(e, kCull, s, g & 1);
+  stage_begin(e, kCull, s, g, (uint64_t)e->n * 40u);  // + 4 V for the ids (V not host-known yet)
   const gss_viewport vp{0.0f, (float)cam.width, 0.0f, (float)cam.height};
   cull(e->gw, e->n, kGeoDim, &cam, &vp, e->cfg.low_pass, nullptr, e->ids[p], e->count[p], e->cull_ws,
        e->cull_ws_bytes, s);
@@ -279,9 +338,12 @@ void stage_forward_params(gss_engine* e, int g) {
   GSS_CUDA(cudaEventSynchronize(e->ev_cull[p].e));
   const int64_t V = e->count_host[p];
   ensure_rows(e, V);
-  stage_begin(e, kFwd, s, b);
   const int pb = (g - 1) % 2;
   const bool pending = g > e->seg_begin && e->g_iter[pb] == g - 1;
+  // V (3*196 + 1) + V_pend * 196 + V * 196
+  const uint64_t fbytes = (uint64_t)V * (3 * 196 + 1 + 196) +
+                          (pending ? (uint64_t)e->count_host[e->g_plan[pb]] * 196u : 0u);
+  stage_begin(e, kFwd, s, g, fbytes);
   gss_sparse_grads pg{};
   if (pending) {
     const int pp = e->g_plan[pb];
@@ -303,7 +365,7 @@ void stage_render(gss_engine* e, int g, const gss_camera& cam, const float* gt_d
   const int p = g % 3, b = g % 2;
   cudaStream_t s = e->sD;
   require(e->fwd_iter[b] == g, "render: forwarded buffer is not for this iteration", GSS_ERR_INVARIANT);
-  stage_begin(e, kRender, s, b);
+  stage_begin(e, kRender, s, g);
   const int64_t V = e->count_host[p];
   gss_render_scene sc{};
   sc.ids = e->ids[p];
@@ -345,7 +407,7 @@ void stage_render(gss_engine* e, int g, const gss_camera& cam, const float* gt_d
 void stage_geo_update(gss_engine* e, int g) {
   const int p = g % 3, b = g % 2;
   cudaStream_t s = e->sD;
-  stage_begin(e, kGeo, s, b);
+  stage_begin(e, kGeo, s, g, (uint64_t)e->n * 240u + (uint64_t)e->count_host[p] * 40u);
   gss_sparse_grads gr{};
   gr.ids = e->ids[p];
   gr.count = e->count_host[p];
@@ -362,7 +424,7 @@ void stage_geo_update(gss_engine* e, int g) {
 void stage_handoff(gss_engine* e, int g) {
   const int p = g % 3, b = g % 2;
   cudaStream_t s = e->sD;
-  stage_begin(e, kHandoff, s, b);
+  stage_begin(e, kHandoff, s, g, (uint64_t)e->count_host[p] * (8u + 12u + 8u + 4u));
   const int64_t V = e->count_host[p];
   if (V > 0) {
     const int blocks = (int)std::min<int64_t>(ceil_div(V, 256), 148 * 8);
@@ -380,7 +442,8 @@ void stage_lazy(gss_engine* e, int g) {
   cudaStream_t s = S(e, true);
   require(e->g_iter[b] == g, "lazy update: staging buffer holds a different iteration", GSS_ERR_INVARIANT);
   if (e->cfg.pipelined) GSS_CUDA(cudaStreamWaitEvent(s, e->ev_handoff[b].e, 0));
-  stage_begin(e, kLazy, s, b);
+  const int slot = e->timeline_on ? (e->touched_next++ % kTouchedRing) : -1;
+  stage_begin(e, kLazy, s, g, 0, slot);
   const int p = e->g_plan[b];
   gss_sparse_grads gr{};
   gr.ids = e->ids[p];
@@ -389,7 +452,7 @@ void stage_lazy(gss_engine* e, int g) {
   gr.rows = e->g_ng[b];
   gr.stride = kNgGradStride;
   gr.col0 = 0;
-  adam_update(&e->ng, &gr, nullptr, nullptr, s);
+  adam_update(&e->ng, &gr, nullptr, slot >= 0 ? e->touched_ring + slot : nullptr, s);
   stage_end(e, kLazy, s, b);
   GSS_CUDA(cudaEventRecord(e->ev_lazy[b].e, s));
 }
@@ -399,6 +462,7 @@ void stage_lazy(gss_engine* e, int g) {
 // fp(g) so it overlaps render(g) (engine.hpp:498-508). The data each stage reads is the same in
 // both orders, so the trajectories are bitwise identical.
 void iteration(gss_engine* e, int g, const gss_camera& cam, const float* gt_dev, float* loss_out) {
+  nvtxRangePushA("iteration");
   stage_cull(e, g, cam);
   stage_forward_params(e, g);
   const int owed = e->open_pending;
@@ -409,6 +473,7 @@ void iteration(gss_engine* e, int g, const gss_camera& cam, const float* gt_dev,
   stage_handoff(e, g);
   e->open_pending = g;
   e->valid_counts.push_back(e->count_host[g % 3]);
+  nvtxRangePop();
 }
 
 void drain(gss_engine* e) {
@@ -571,8 +636,11 @@ void engine_destroy(gss_engine* e) {
   for (int b = 0; b < 2; ++b) { f(e->fwd[b]); f(e->g_geo[b]); f(e->g_ng[b]); f(e->g_m2d[b]); }
   render_ctx_destroy(e->rctx);
   f(e->image); f(e->d_img); f(e->gt_step[0]); f(e->gt_step[1]); f(e->loss_dev); f(e->accum_norm); f(e->accum_cnt);
+  e->timeline_on = false;
   collect_times(e);
   for (auto ev : e->ev_free) cudaEventDestroy(ev);
+  if (e->epoch) cudaEventDestroy(e->epoch);
+  f(e->touched_ring);
   if (e->sD) cudaStreamDestroy(e->sD);
   if (e->sH) cudaStreamDestroy(e->sH);
   if (e->sC) cudaStreamDestroy(e->sC);
@@ -830,6 +898,37 @@ void engine_stage_ms(gss_engine* e, double* out6) {
 }
 
 int64_t engine_launches(gss_engine* e) { return e ? e->launches_last : 0; }
+
+// Per-iteration timeline (engine.hpp:22-28 TimelineRow, 230-237): enabling records an epoch event;
+// every stage interval collected afterwards (at each drain) becomes a row.
+void engine_timeline_enable(gss_engine* e, bool on) {
+  require(e != nullptr, "engine: null");
+  if (e->open_pending >= 0) drain(e);
+  GSS_CUDA(cudaDeviceSynchronize());
+  collect_times(e);
+  e->timeline.clear();
+  e->timeline_on = on;
+  if (on) {
+    if (!e->epoch) GSS_CUDA(cudaEventCreate(&e->epoch));
+    if (!e->touched_ring) e->touched_ring = dmalloc<int64_t>(kTouchedRing);
+    GSS_CUDA(cudaMemset(e->touched_ring, 0, kTouchedRing * sizeof(int64_t)));
+    e->touched_next = 0;
+    GSS_CUDA(cudaEventRecord(e->epoch, e->sD));
+  }
+}
+int64_t engine_timeline(gss_engine* e, gss_timeline_row* rows, int64_t cap) {
+  require(e != nullptr, "engine: null");
+  if (e->open_pending >= 0) drain(e);
+  const int64_t n = (int64_t)e->timeline.size();
+  if (rows) std::memcpy(rows, e->timeline.data(), (size_t)std::min(n, cap) * sizeof(gss_timeline_row));
+  return n;
+}
+// Stage-delay injection (test instrumentation, see stage_delay_kernel): delays cycle per stage start.
+void engine_stage_delays(gss_engine* e, const uint32_t* ns, int n) {
+  require(e != nullptr && (n == 0 || ns), "engine: null");
+  e->delays_ns.assign(ns, ns + n);
+  e->delay_next = 0;
+}
 
 // Live timing of the engine's composite / sweep kernel launches (bench roofline of the dominant
 // kernels): CUDA events on the render stream around each forward_kernel / backward_kernel.

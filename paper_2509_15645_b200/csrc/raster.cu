@@ -51,7 +51,7 @@ constexpr int kFwdBlockRows = 4 * kFwdPPT;
 #define GSS_FWD_MINB 0
 #endif
 #ifndef GSS_BWD_MINB
-#define GSS_BWD_MINB 0
+#define GSS_BWD_MINB 10  // 10 sweep CTAs per SM (96 registers, no spill): measured best
 #endif
 #if GSS_FWD_MINB > 0
 #define GSS_FWD_BOUNDS __launch_bounds__(kFwdThreads, GSS_FWD_MINB)
@@ -881,102 +881,6 @@ __device__ __forceinline__ float warp_reduce_scatter10(const float v[10], int la
   return u + __shfl_xor_sync(0xffffffffu, u, 1);
 }
 
-#ifndef GSS_BWD_MOMENTS
-#define GSS_BWD_MOMENTS 1
-#endif
-#ifndef GSS_BWD_SKIP
-#define GSS_BWD_SKIP 0
-#endif
-#if !GSS_BWD_MOMENTS
-// Round-1 sweep (A/B reference): 9 per-pixel gradient terms.
-// One contribution of splat r (sweep position jpos) to pixel p: accumulates its 9 screen-space
-// gradient terms into v and steps the pixel's reverse state. Returns whether it contributed.
-// The gradient arithmetic runs on fast math with explicit FMAs (tolerance-checked);
-// the 0.999 clamp decision, which selects the reference's branch (render.hpp:560-573), is
-// recomputed with the forward's exact arithmetic whenever the fast alpha is within 1e-4 of the
-// threshold, so both passes always take the same branch.
-// Predicated form: every lane evaluates the contribution and a lane whose pixel is outside the
-// record's box (or past its last index) adds exact zeros and keeps its state, so the two pixels of
-// a thread form one branch-free block the scheduler can interleave.
-__device__ __forceinline__ bool bwd_contrib9(const SplatRec& r, const BwdConic& k, int jpos, PixB& p, float v[9]) {
-  const bool ok = (jpos < p.L) & (p.x >= r.bx0) & (p.x < r.bx1) & (p.y >= r.by0) & (p.y < r.by1);
-  const float dx = p.cx - r.mx, dy = p.cy - r.my;
-  const float mdxy2 = -2.0f * dx * dy;
-  float q = __fmaf_rn(k.ia * dx, dx, __fmaf_rn(k.ic * dy, dy, (-0.5f * k.ibm2) * mdxy2));
-  q = (q < 0.0f || !ok) ? 0.0f : q;  // an idle lane evaluates at q = 0: every term stays finite
-  const float weight = ex2_fast(-0.72134752f * q);  // exp(-q/2)
-  float raw = r.ab * weight;
-  if (ok && fabsf(raw - 0.999f) < 1e-4f) raw = contrib_eval(r, p.cx, p.cy).clamped ? 1.0f : 0.0f;
-  const bool clamped = raw > 0.999f;
-  const float alpha = ok ? (clamped ? 0.999f : r.ab * weight) : 0.0f;
-  const float inv1m = rcp_fast(1.0f - alpha);
-  const float Tb = ok ? p.T * inv1m : p.T;  // transmittance before this contribution
-  const float w_rgb = alpha * Tb;
-  v[0] = __fmaf_rn(w_rgb, p.g0, v[0]);
-  v[1] = __fmaf_rn(w_rgb, p.g1, v[1]);
-  v[2] = __fmaf_rn(w_rgb, p.g2, v[2]);
-  const float dot_c = __fmaf_rn(r.r, p.g0, __fmaf_rn(r.g, p.g1, r.bl * p.g2));
-  const float dot_suf = __fmaf_rn(p.s0, p.g0, __fmaf_rn(p.s1, p.g1, p.s2 * p.g2));
-  const float d_alpha = __fmaf_rn(Tb, dot_c, -dot_suf * inv1m);
-  p.s0 = __fmaf_rn(r.r, w_rgb, p.s0);
-  p.s1 = __fmaf_rn(r.g, w_rgb, p.s1);
-  p.s2 = __fmaf_rn(r.bl, w_rgb, p.s2);
-  p.T = Tb;
-  const float gsel = (ok && !clamped) ? 1.0f : 0.0f;  // render.hpp:572-586 only when not clamped
-  v[8] = __fmaf_rn(weight * gsel, d_alpha, v[8]);
-  const float dqi = alpha * d_alpha * k.nh * gsel;
-  const float b2 = 2.0f * r.b;
-  v[5] = __fmaf_rn(dqi, __fmaf_rn(-q, r.c, dy * dy), v[5]);
-  v[6] = __fmaf_rn(dqi, __fmaf_rn(q, b2, mdxy2), v[6]);
-  v[7] = __fmaf_rn(dqi, __fmaf_rn(-q, r.a, dx * dx), v[7]);
-  v[3] = __fmaf_rn(dqi, __fmaf_rn(b2, dy, -2.0f * r.c * dx), v[3]);
-  v[4] = __fmaf_rn(dqi, __fmaf_rn(b2, dx, -2.0f * r.a * dy), v[4]);
-  return ok;
-}
-
-// Warp reduce-scatter of 9 values in 12 shuffles (9 x 5 butterflies would take 45; padding to 16
-// takes 16): the value set is halved per lane bit with minimal padding, 10 -> 5 -> 3 -> 2 -> 1
-// (bits 4, 3, 2, 1), then lanes 2k and 2k+1 add. Afterwards lane l holds the warp total of value
-// index reduce_scatter9_index(l) (-1: a padding slot). Fixed order: deterministic.
-__device__ __forceinline__ int reduce_scatter9_index(int lane) {
-  const int j3 = ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);  // of the 3-set (3 = padding)
-  const int j5 = ((lane >> 3) & 1) * 3 + j3;                   // of the 5-set (5.. = padding)
-  const int j10 = ((lane >> 4) & 1) * 5 + j5;                  // of the 10 values (9 = padding)
-  return (j3 < 3 && j5 < 5 && j10 < 9) ? j10 : -1;
-}
-__device__ __forceinline__ float warp_reduce_scatter9(const float v[9], int lane) {
-  float x[5];
-  {  // bit 4: 10 values -> 5
-    const bool up = (lane & 16) != 0;
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      const float lo = v[i], hi = i + 5 < 9 ? v[i + 5] : 0.0f;
-      x[i] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, 16);
-    }
-  }
-  float y[3];
-  {  // bit 3: 5 values (+1 padding) -> 3
-    const bool up = (lane & 8) != 0;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const float lo = x[i], hi = i + 3 < 5 ? x[i + 3] : 0.0f;
-      y[i] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, 8);
-    }
-  }
-  float z[2];
-  {  // bit 2: 3 values (+1 padding) -> 2
-    const bool up = (lane & 4) != 0;
-    const float hi1 = 0.0f;
-    z[0] = (up ? y[2] : y[0]) + __shfl_xor_sync(0xffffffffu, up ? y[0] : y[2], 4);
-    z[1] = (up ? hi1 : y[1]) + __shfl_xor_sync(0xffffffffu, up ? y[1] : hi1, 4);
-  }
-  const bool up = (lane & 2) != 0;  // bit 1: 2 values -> 1
-  const float u = (up ? z[1] : z[0]) + __shfl_xor_sync(0xffffffffu, up ? z[0] : z[1], 2);
-  return u + __shfl_xor_sync(0xffffffffu, u, 1);
-}
-
-#endif
-
 // Reverse sweep (render.hpp:542-589) per 16x16 tile: 64 threads, 4 pixels each (rows ly, ly + 2,
 // ly + 4, ly + 6 of an 8-row warp band), so a splat's 9 gradient terms are pre-summed per lane
 // over 4 pixels (predicated, interleavable) and reduced once per warp. Per batch, each warp ballots which records can reach its band (pixel
@@ -1001,11 +905,7 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
   __shared__ SplatRec sh[kBwdBatch];
   __shared__ BwdConic shk[kBwdBatch];
   __shared__ int32_t sinst[kBwdBatch];  // the record's (splat, this tile) instance index
-#if GSS_BWD_MOMENTS
-  constexpr int kNv = 10;
-#else
-  constexpr int kNv = 9;
-#endif
+  constexpr int kNv = 10;  // swept sums per record (bwd_contrib)
   __shared__ float red[kBwdBatch][kBwdWarps][kNv];
   __shared__ unsigned long long wmask[kBwdWarps][kBwdMasks];
   __shared__ int smax;
@@ -1047,11 +947,7 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
   if (lane == 0 && wl > 0) atomicMax(&smax, wl);
   __syncthreads();
   const int Lmax = smax;
-#if GSS_BWD_MOMENTS
   const int vidx = reduce_scatter_index(lane);
-#else
-  const int vidx = reduce_scatter9_index(lane);
-#endif
 #if GSS_RASTER_STATS
   unsigned long long st_walk = 0, st_use = 0;
 #endif
@@ -1117,48 +1013,22 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
         float v[kNv];
 #pragma unroll
         for (int i = 0; i < kNv; ++i) v[i] = 0.0f;
-#if GSS_RASTER_STATS && GSS_BWD_MOMENTS
+#if GSS_RASTER_STATS
         ++st_walk;
 #pragma unroll
         for (int q = 0; q < kBwdPPT; ++q) st_use += bwd_contrib(r, k, xin, bstart + jj, px[q], v) ? 1 : 0;
-#elif GSS_BWD_MOMENTS && GSS_BWD_SKIP
-        // warp-uniform skip of the pixel slots (row pairs of the band) the record's box misses
-        {
-          const int r0 = r.by0 - by0w, r1 = r.by1 - by0w;  // box rows relative to the band
-#pragma unroll
-          for (int q = 0; q < kBwdPPT; ++q)
-            if (r0 < 2 * q + 2 && r1 > 2 * q) bwd_contrib(r, k, xin, bstart + jj, px[q], v);
-        }
-#elif GSS_BWD_MOMENTS
+#else
 #pragma unroll
         for (int q = 0; q < kBwdPPT; ++q) bwd_contrib(r, k, xin, bstart + jj, px[q], v);
-#else
-        (void)xin;
-#pragma unroll
-        for (int q = 0; q < kBwdPPT; ++q) bwd_contrib9(r, k, bstart + jj, px[q], v);
 #endif
         // A record no lane contributed to reduces exact zeros: the same partial without a vote.
-#if GSS_BWD_MOMENTS
         const float tot = warp_reduce_scatter10(v, lane);
-#else
-        const float tot = warp_reduce_scatter9(v, lane);
-#endif
         if ((lane & 1) == 0 && vidx >= 0) red[jj][warp][vidx] = tot;
       }
     }
     __syncthreads();
     // Fixed-order cross-warp sum over the warps that walked the record, then the record's 9 SlotAcc
     // terms: one instance partial per splat of the batch (a thread per record).
-#if !GSS_BWD_MOMENTS
-    for (int e = threadIdx.x; e < nb * 9; e += kBwdThreads) {
-      const int jj = e / 9, i = e - jj * 9;
-      float s = 0.0f;
-#pragma unroll
-      for (int q = 0; q < kBwdWarps; ++q)
-        if ((wmask[q][jj >> 6] >> (jj & 63)) & 1ull) s += red[jj][q][i];
-      partials[(int64_t)sinst[jj] * 9 + i] = s;
-    }
-#else
     for (int jj = threadIdx.x; jj < nb; jj += kBwdThreads) {
       float u[10];
 #pragma unroll
@@ -1174,7 +1044,6 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
 #pragma unroll
       for (int i = 0; i < 9; ++i) dst[i] = o[i];
     }
-#endif
   }
 #if GSS_RASTER_STATS
   if (lane == 0) {

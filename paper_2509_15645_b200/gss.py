@@ -811,6 +811,36 @@ class OffloadEngine:
     def launches(self) -> int:
         return int(lib().gss_engine_launches(self.h))
 
+    TIMELINE_STAGES = ("cull", "forward_params", "render", "geo_update", "handoff", "lazy_update")
+
+    def timeline_enable(self, on: bool = True) -> None:
+        """Per-iteration stage timeline (engine.hpp:22-28): rows from now on, times from now."""
+        check(lib().gss_engine_timeline_enable(self.h, 1 if on else 0))
+
+    def timeline(self):
+        """TimelineRow list: dicts with iteration, stage, worker (0 device, 1 host tier), t0_ns,
+        t1_ns, bytes."""
+        n = int(lib().gss_engine_timeline(self.h, None, 0))
+        if n < 0:
+            check(-n)
+        rows = np.zeros((max(n, 1), 5), np.int64)  # gss_timeline_row: 40 bytes
+        m = int(lib().gss_engine_timeline(self.h, rows.ctypes.data, n))
+        if m < 0:
+            check(-m)
+        out = []
+        for r in rows[:n]:
+            it, st = int(r[0]) & 0xFFFFFFFF, int(r[0]) >> 32
+            wk = int(r[1]) & 0xFFFFFFFF
+            out.append({"iteration": it if it < 2 ** 31 else it - 2 ** 32, "stage": self.TIMELINE_STAGES[st],
+                        "worker": wk, "t0_ns": int(r[2]), "t1_ns": int(r[3]), "bytes": int(r[4]) & (2 ** 64 - 1)})
+        return out
+
+    def stage_delays(self, ns) -> None:
+        """Test instrumentation: device-side sleeps (ns) at each stage start, cycling (the
+        reference's EngineConfig::stage_hook delays). Empty list disables."""
+        arr = np.ascontiguousarray(np.asarray(ns, np.uint32))
+        check(lib().gss_engine_stage_delays(self.h, arr.ctypes.data if arr.size else None, int(arr.size)))
+
     def kernel_timing(self, on: bool = True) -> None:
         """CUDA events around every composite / sweep kernel launch (see kernel_times)."""
         check(lib().gss_engine_kernel_timing(self.h, 1 if on else 0))

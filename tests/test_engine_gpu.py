@@ -167,3 +167,52 @@ def test_c1_config_twenty_iterations_track_reference(ref):
     assert losses[0] == rl[0]  # the first forward sees identical parameters: bit-identical loss
     dev = float(O.rel_err(snap, r.snapshot()).max())
     assert dev <= 1e-3, dev
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5])
+def test_random_stage_delays_keep_pipelined_equal_to_serial(seed):
+    """test_offload.cpp:268-285 (randomized stage delays never violate buffer ownership), on the
+    device: a device-side sleep of 0-900 us at the start of every stage on its own stream shakes
+    the two-stream schedule; every cross-stream edge is an event, so the pipelined trajectory must
+    stay bitwise equal to the serial one (and the host-tier variant too)."""
+    start, cams, gts = scene(n=300, cams=4, img=32, seed=70 + seed)
+    opt = G.OptimConfig(defer_max=15)
+    es = engine(start, cams, gts, optim=opt, pipelined=False)
+    ls, vs = es.run(12)
+    rng = O.Rng(seed)
+    delays = [int(rng.next_u64() % 900) * 1000 for _ in range(64)]
+    for host in (False, True):
+        ep = engine(start, cams, gts, optim=opt, pipelined=True, nongeo_on_host=host)
+        ep.stage_delays(delays)
+        lp, vp = ep.run(12)
+        assert np.array_equal(ls.view(np.uint32), lp.view(np.uint32))
+        assert np.array_equal(vs, vp)
+        assert np.array_equal(es.snapshot().view(np.uint32), ep.snapshot().view(np.uint32))
+        ep.close()
+
+
+def test_timeline_rows():
+    """TimelineRow (engine.hpp:22-28): one row per stage per iteration, ordered within a stream,
+    the pipelined engine overlapping the host-tier stream with the device stream."""
+    start, cams, gts = scene(n=400, cams=4, img=48, seed=7)
+    e = engine(start, cams, gts, pipelined=True)
+    e.run(2)
+    e.timeline_enable(True)
+    e.run(6)
+    rows = e.timeline()
+    stages = {}
+    for r in rows:
+        stages.setdefault(r["iteration"], []).append(r["stage"])
+        assert r["t1_ns"] >= r["t0_ns"] >= 0
+    its = sorted(stages)
+    assert len(its) == 6
+    for it in its:
+        assert sorted(stages[it]) == sorted(["cull", "forward_params", "render", "geo_update", "handoff",
+                                             "lazy_update"])
+    lazy = [r for r in rows if r["stage"] == "lazy_update"]
+    assert all(r["worker"] == 1 for r in lazy) and all(r["bytes"] >= 400 for r in lazy)
+    cull = [r for r in rows if r["stage"] == "cull"]
+    assert all(r["worker"] == 0 and r["bytes"] == 400 * 40 for r in cull)
+    for st in ("cull", "render"):  # stream order on the device stream
+        t = [r["t0_ns"] for r in sorted((r for r in rows if r["stage"] == st), key=lambda r: r["iteration"])]
+        assert t == sorted(t)

@@ -8,6 +8,7 @@
 #include <vector>
 #include <algorithm>
 #include <random>
+#include <chrono>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e_), __LINE__); exit(1); } } while (0)
@@ -39,6 +40,35 @@ __global__ void rmw_rows(float4* host, const int32_t* ids, int64_t nids) {
     float4 v = host[(int64_t)ids[k] * kRowF4 + u];
     v.x += 1.0f;
     host[(int64_t)ids[k] * kRowF4 + u] = v;
+  }
+}
+
+// Few-CTA zero-copy row movers: each thread keeps 8 independent 16-byte transfers in flight, so a
+// small grid (leaving the other SMs to compute) can still saturate the link.
+template <bool GATHER>
+__global__ void __launch_bounds__(256) move_rows_ilp(float4* host, const int32_t* ids, int64_t nids, float4* dev) {
+  const int64_t total = nids * kRowF4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < total; base += 8 * stride) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = base + u * stride;
+      if (i < total) {
+        const int64_t k = i / kRowF4;
+        const int c = (int)(i - k * kRowF4);
+        v[u] = GATHER ? host[(int64_t)ids[k] * kRowF4 + c] : dev[i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = base + u * stride;
+      if (i < total) {
+        const int64_t k = i / kRowF4;
+        const int c = (int)(i - k * kRowF4);
+        if (GATHER) dev[i] = v[u]; else host[(int64_t)ids[k] * kRowF4 + c] = v[u];
+      }
+    }
   }
 }
 
@@ -124,6 +154,55 @@ int main(int argc, char** argv) {
       CK(cudaStreamSynchronize(s2));
     }, 3);
     printf("{\"probe\":\"zc_gather_scatter_concurrent\",\"gbs_total\":%.2f}\n", bytes / ms / 1e6);
+  }
+  for (int blocks : {8, 16, 32, 64, 128}) {
+    float ms = timeit([&] { move_rows_ilp<true><<<blocks, 256>>>(darena_view, dids, nids, dout); }, 3);
+    printf("{\"probe\":\"zc_gather_ilp\",\"blocks\":%d,\"gbs\":%.2f}\n", blocks, bytes / ms / 1e6);
+    ms = timeit([&] { move_rows_ilp<false><<<blocks, 256>>>(darena_view, dids, nids, dout); }, 3);
+    printf("{\"probe\":\"zc_scatter_ilp\",\"blocks\":%d,\"gbs\":%.2f}\n", blocks, bytes / ms / 1e6);
+  }
+  {  // ILP gather (32 CTAs) + scatter (32 CTAs) concurrently, and gather (SM) + a contiguous CE D2H
+    float ms = timeit([&] {
+      move_rows_ilp<true><<<32, 256, 0, s1>>>(darena_view, dids, nids / 2, dout);
+      move_rows_ilp<false><<<32, 256, 0, s2>>>(darena_view, dids + nids / 2, nids - nids / 2, dout);
+      CK(cudaStreamSynchronize(s1));
+      CK(cudaStreamSynchronize(s2));
+    }, 3);
+    printf("{\"probe\":\"zc_ilp_gather_scatter_concurrent\",\"gbs_total\":%.2f}\n", bytes / ms / 1e6);
+    const size_t half = (size_t)(nids / 2) * 640;
+    ms = timeit([&] {
+      move_rows_ilp<true><<<32, 256, 0, s1>>>(darena_view, dids, nids / 2, dout);
+      CK(cudaMemcpyAsync(h2, d2, half, cudaMemcpyDeviceToHost, s2));
+      CK(cudaStreamSynchronize(s1));
+      CK(cudaStreamSynchronize(s2));
+    }, 3);
+    printf("{\"probe\":\"zc_gather_plus_ce_d2h\",\"gbs_total\":%.2f}\n", 2 * half / ms / 1e6);
+  }
+  {  // copy-engine row gather / scatter: one cudaMemcpyBatchAsync entry per 640-byte row
+    const size_t nb = std::min<size_t>((size_t)nids, 1u << 20);
+    std::vector<void*> dsts(nb), srcs(nb);
+    std::vector<size_t> sizes(nb, 640);
+    char* db = (char*)dout;
+    for (size_t k = 0; k < nb; ++k) {
+      srcs[k] = (char*)harena + (size_t)ids[k] * 640;
+      dsts[k] = db + k * 640;
+    }
+    cudaMemcpyAttributes at{};
+    at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    size_t idx0 = 0, fail = 0;
+    cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), nb, &at, &idx0, 1, &fail, s1);
+    CK(cudaStreamSynchronize(s1));
+    if (e != cudaSuccess) {
+      printf("{\"probe\":\"ce_batch\",\"error\":\"%s\"}\n", cudaGetErrorString(e));
+    } else {
+      auto t0 = std::chrono::steady_clock::now();
+      float ms = timeit([&] { CK(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), nb, &at, &idx0, 1, &fail, s1)); CK(cudaStreamSynchronize(s1)); }, 3);
+      double api = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count() / 4;
+      printf("{\"probe\":\"ce_batch_gather\",\"rows\":%zu,\"gbs\":%.2f,\"ms\":%.2f,\"host_ms\":%.2f}\n", nb, nb * 640.0 / ms / 1e6, ms, api);
+      float ms2 = timeit([&] { CK(cudaMemcpyBatchAsync(srcs.data(), dsts.data(), sizes.data(), nb, &at, &idx0, 1, &fail, s1)); CK(cudaStreamSynchronize(s1)); }, 3);
+      printf("{\"probe\":\"ce_batch_scatter\",\"rows\":%zu,\"gbs\":%.2f}\n", nb, nb * 640.0 / ms2 / 1e6);
+    }
   }
   return 0;
 }
