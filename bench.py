@@ -900,11 +900,11 @@ def main():
 # the fraction of the lane-pixel slots it issues that are useful contributions (a library built
 # with GSS_RASTER_STATS=1, tools/raster_work.py).
 RASTER_PROFILE = {
-    "sweep": {"kernel": "backward_kernel", "issue_busy": 0.834, "useful_of_offered": 0.534,
-              "source": "profiles/r02_ncu_raster_c4_baseline.txt (Issue Slots Busy), "
+    "sweep": {"kernel": "backward_kernel", "issue_busy": 0.847, "useful_of_offered": 0.534,
+              "source": "profiles/r02_ncu_raster_c4.txt (Issue Slots Busy), "
                         "profiles/r02_raster_work_c4.json (bwd_useful_of_offered)"},
-    "composite": {"kernel": "forward_kernel", "issue_busy": 0.898, "useful_of_offered": 0.655,
-                  "source": "profiles/r02_ncu_raster_c4_baseline.txt (Issue Slots Busy), "
+    "composite": {"kernel": "forward_kernel", "issue_busy": 0.856, "useful_of_offered": 0.655,
+                  "source": "profiles/r02_ncu_raster_c4.txt (Issue Slots Busy), "
                             "profiles/r02_raster_work_c4.json (fwd_useful_of_offered)"},
 }
 

@@ -136,6 +136,10 @@ int gss_arena_check(const gss_arena* arena, gss_stream_t stream);
  * first gss_deferred_update / gss_restore_view / gss_arena_check on the arena and live until this
  * call (synchronises the device). */
 int gss_arena_release(const gss_arena* arena);
+/* AccessReport (adam.hpp:36-50) of the arena since its first use (keyed like the scratch):
+ * out6 = update_passes, touched_rows, param_bytes (7*dim*4 per touched row), counter_bytes (n per
+ * deferred pass), restore_rows, restore_read_bytes (4*dim*4 per restored row). Synchronises. */
+int gss_arena_access(const gss_arena* arena, uint64_t* out6);
 
 /* ---- rasterizer (render.hpp:361-640) ---------------------------------------------------- */
 /* A render context is the device-side RenderResult (render.hpp:284-289): it owns the splat

@@ -19,7 +19,8 @@
 //
 // Errors map to the reference's exception types: status 2 -> gss::ConfigError (or
 // std::invalid_argument where the reference throws it), 3 -> gss::InvariantViolation,
-// 1 (CUDA) -> std::runtime_error. The arena's AccessReport tally is not maintained.
+// 4 -> gss::ParseError, 1 (CUDA) -> std::runtime_error. The arena's AccessReport tally
+// (adam.hpp:36-50) is maintained on the device and added to the reference arena's.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -43,6 +44,7 @@ inline void check(int st, bool invalid_argument = false) {
     throw gss::ConfigError(msg);
   }
   if (st == GSS_ERR_INVARIANT) throw gss::InvariantViolation(msg);
+  if (st == GSS_ERR_PARSE) throw gss::ParseError(msg);
   throw std::runtime_error(msg);
 }
 
@@ -129,6 +131,9 @@ class DevArena {
       s_.groups[i] = gss_group{g.col0, g.dim, g.hp.lr, g.hp.beta1, g.hp.beta2, g.hp.eps};
     }
   }
+  ~DevArena() { gss_arena_release(&s_); }
+  DevArena(const DevArena&) = delete;
+  DevArena& operator=(const DevArena&) = delete;
   gss_arena* get() { return &s_; }
   const gss_arena* get() const { return &s_; }
   void sync(gss::Arena<float>& a) const {
@@ -137,6 +142,19 @@ class DevArena {
     v_.download(a.v.data(), a.v.size());
     c_.download(a.counter.data(), a.counter.size());
     a.step = s_.step;
+    add_access(a.access);
+  }
+  // The device AccessReport tally of this transient mirror, added to the reference arena's
+  // (adam.hpp:36-50; restore_view mutates it through a const arena, as adam.hpp:254 does).
+  void add_access(gss::AccessReport& r) const {
+    uint64_t t[6] = {0, 0, 0, 0, 0, 0};
+    check(gss_arena_access(&s_, t));
+    r.update_passes += t[0];
+    r.touched_rows += t[1];
+    r.param_bytes += t[2];
+    r.counter_bytes += t[3];
+    r.restore_rows += t[4];
+    r.restore_read_bytes += t[5];
   }
 
  private:
@@ -196,6 +214,7 @@ inline void restore_view(const gss::Arena<float>& a, std::span<const int> ids, c
     check(gss_restore_view(d.get(), di.get(), int64_t(ids.size()), nullptr, nullptr, o.get(), nullptr));
   }
   o.download(out, ids.size() * size_t(a.dim));
+  d.add_access(const_cast<gss::Arena<float>&>(a).access);
 }
 
 inline void flush_deferred(gss::Arena<float>& a) {

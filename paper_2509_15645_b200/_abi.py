@@ -173,6 +173,7 @@ SIGNATURES = {
     "gss_init_gaussians": (C.c_int, [P, P, I32, I32, F64, F64, P]),
     "gss_look_at_camera": (C.c_int, [P, P, F32, F32, I32, I32, F32, F32, C.POINTER(GssCamera)]),
     "gss_raster_stats": (C.c_int, [P, I32]),
+    "gss_arena_access": (C.c_int, [C.POINTER(GssArena), P]),
     "gss_engine_kernel_timing": (C.c_int, [P, I32]),
     "gss_engine_timeline_enable": (C.c_int, [P, I32]),
     "gss_engine_timeline": (I64, [P, P, I64]),

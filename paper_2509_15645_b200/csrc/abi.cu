@@ -24,6 +24,7 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
                   const gss_sparse_grads* pending, float* out, cudaStream_t st);
 int arena_check(const gss_arena* ap, cudaStream_t st);
 void arena_release(const gss_arena* ap);
+void arena_access(const gss_arena* ap, uint64_t* out6);
 void cull_workspace_release(const void* ws);
 // raster.cu
 gss_render_ctx* render_ctx_create();
@@ -360,6 +361,12 @@ GSS_API int gss_init_gaussians(const float* positions, const float* colors, int3
   });
 }
 
+GSS_API int gss_arena_access(const gss_arena* arena, uint64_t* out6) {
+  return guarded([&] {
+    require_device();
+    arena_access(arena, out6);
+  });
+}
 GSS_API int gss_raster_stats(uint64_t* out8, int32_t reset) {
   return guarded([&] {
     require_device();

@@ -164,6 +164,7 @@ template <int K> __device__ void load_luts(SmemLuts<K>& s, const LutArgs<K>& L, 
 }
 
 enum Mode : int { kDeferred = 0, kFlush = 1 };
+constexpr int kDenseTally = 2, kRestoreTally = 3;  // tally_host kinds besides kDeferred
 
 // Block index of a sorted id list: bstart[b] = lower_bound(ids, b * kRowsPerBlock) for
 // b = 0 .. nblocks (so a 1024-row block finds its gradient ids with two loads instead of a
@@ -906,6 +907,14 @@ bool host_resident(const gss_arena& a) {
 }
 constexpr int kHostTierBlocks = 64;
 
+unsigned long long* tally_dev(const gss_arena& a);
+__global__ void tally_add_kernel(unsigned long long* dst, const unsigned long long* src_u64, const int64_t* src_i64) {
+  *dst += src_u64 ? *src_u64 : (unsigned long long)*src_i64;
+}
+// Host-known AccessReport parts: a deferred / dense pass (touched rows host-known, or 0 when the
+// device adds them), or a restore of `rows` rows.
+void tally_host(const gss_arena& a, int kind, int64_t rows);
+
 // Block index of a sorted id list (nblocks + 1 entries) into `bstart`.
 int32_t* build_index(const gss_arena& a, const GradsDev& g, int* err, int32_t* bstart, cudaStream_t st) {
   const int nblk = (int)ceil_div(a.n, kRowsPerBlock);
@@ -932,6 +941,7 @@ void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* 
   if (MODE == kDeferred && a.defer_max == 0 && (a.row_stride == 0 || a.row_stride == a.dim)) {
     dense_update_kernel<K><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, bstart, *L, tcount, tmask);
     GSS_LAUNCHED();
+    tally_host(a, kDeferred, a.n);  // defer_max 0: counter == MAX for every row, all touched
   } else {
     // Pass 1: counters + touch list; pass 2: stream the list.
     TouchList tl;
@@ -944,6 +954,11 @@ void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* 
     update_kernel<K, MODE><<<blocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, bstart, *L, tmask, tcount, err,
                                                                    tl);
     GSS_LAUNCHED();
+    if (MODE == kDeferred) {  // adam.hpp:233-236; the touched count is known on the device only
+      tally_host(a, kDeferred, 0);
+      tally_add_kernel<<<1, 1, 0, st>>>(tally_dev(a), tl.count, nullptr);
+      GSS_LAUNCHED();
+    }
     int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, kUpdThreads), (int64_t)sm_count() * GSS_WALK_GRID));
     if (host_resident(a)) wblocks = std::min(wblocks, 4 * kHostTierBlocks);  // reads + writes in flight
     if (vector_rows(a))
@@ -969,12 +984,25 @@ int* err_flag_for(const gss_arena& a) {
   std::lock_guard<std::mutex> lk(g_flag_mu);
   auto it = g_flags.find(a.counter);
   if (it != g_flags.end()) return it->second;
+  // [0] sticky error flag; [2..3] / [4..5]: device tallies (touched rows / restored rows, u64)
   int* f = nullptr;
-  GSS_CUDA(cudaMalloc(&f, sizeof(int)));
-  GSS_CUDA(cudaMemset(f, 0, sizeof(int)));
+  GSS_CUDA(cudaMalloc(&f, 32));
+  GSS_CUDA(cudaMemset(f, 0, 32));
   g_flags[a.counter] = f;
   return f;
 }
+unsigned long long* tally_dev(const gss_arena& a) {
+  return reinterpret_cast<unsigned long long*>(err_flag_for(a) + 2);
+}
+
+// AccessReport (adam.hpp:36-50): host-known parts per arena (keyed like the flag); the device parts
+// (touched rows of a deferred pass, restored rows of a device-counted view) accumulate in the meta
+// block and are folded in by arena_access.
+struct HostTally {
+  uint64_t passes = 0, touched = 0, param_bytes = 0, counter_bytes = 0, restore_rows = 0, restore_bytes = 0;
+};
+std::unordered_map<const void*, HostTally> g_tally;  // guarded by g_flag_mu
+
 }  // namespace
 
 void adam_update(gss_arena* ap, const gss_sparse_grads* grads, int32_t* touched_ids, int64_t* touched_count,
@@ -1063,6 +1091,7 @@ void adam_dense(gss_arena* ap, const float* grads, cudaStream_t st) {
   const int64_t blocks = std::min<int64_t>(ceil_div(a.n * a.dim, kUpdThreads), (int64_t)sms * 8);
   dense_kernel<16><<<(int)blocks, kUpdThreads, 0, st>>>(arena_dev(a), grads, *L);
   GSS_LAUNCHED();
+  tally_host(a, kDenseTally, a.n);
 }
 
 void adam_flush(gss_arena* ap, cudaStream_t st) {
@@ -1192,6 +1221,12 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
   if (count == 0 && !count_dev) return;
   const int64_t t = a.step + 1;
   GradsDev pd = grads_dev(pending);
+  if (count_dev) {  // adam.hpp:287-288 with a device-side row count
+    tally_add_kernel<<<1, 1, 0, st>>>(tally_dev(a) + 1, nullptr, count_dev);
+    GSS_LAUNCHED();
+  } else {
+    tally_host(a, kRestoreTally, count);
+  }
   int dev = 0, sms = 148;
   GSS_CUDA(cudaGetDevice(&dev));
   GSS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1252,6 +1287,44 @@ void arena_release(const gss_arena* ap) {
     GSS_CUDA(cudaFree(it->second));
     g_flags.erase(it);
   }
+  g_tally.erase(ap->counter);
+}
+
+namespace {
+void tally_host(const gss_arena& a, int kind, int64_t rows) {
+  std::lock_guard<std::mutex> lk(g_flag_mu);
+  HostTally& t = g_tally[a.counter];
+  const uint64_t r = (uint64_t)std::max<int64_t>(rows, 0), dim = (uint64_t)a.dim;
+  if (kind == kRestoreTally) {
+    t.restore_rows += r;
+    t.restore_bytes += r * 4u * dim * 4u;  // adam.hpp:287-288
+    return;
+  }
+  t.passes += 1;
+  t.touched += r;
+  t.param_bytes += r * 7u * dim * 4u;  // adam.hpp:204-206, 233-235
+  if (kind == kDeferred) t.counter_bytes += (uint64_t)a.n;
+}
+}  // namespace
+
+// AccessReport of the arena (adam.hpp:36-50): update_passes, touched_rows, param_bytes,
+// counter_bytes, restore_rows, restore_read_bytes (synchronises the device).
+void arena_access(const gss_arena* ap, uint64_t* out6) {
+  require(ap != nullptr && out6 != nullptr, "arena_access: null argument");
+  const gss_arena& a = *ap;
+  unsigned long long dv[2] = {0, 0};
+  unsigned long long* td = tally_dev(a);
+  GSS_CUDA(cudaDeviceSynchronize());
+  GSS_CUDA(cudaMemcpy(dv, td, sizeof dv, cudaMemcpyDeviceToHost));
+  std::lock_guard<std::mutex> lk(g_flag_mu);
+  const HostTally t = g_tally[a.counter];
+  const uint64_t dim = (uint64_t)a.dim;
+  out6[0] = t.passes;
+  out6[1] = t.touched + dv[0];
+  out6[2] = t.param_bytes + dv[0] * 7u * dim * 4u;
+  out6[3] = t.counter_bytes;
+  out6[4] = t.restore_rows + dv[1];
+  out6[5] = t.restore_bytes + dv[1] * 4u * dim * 4u;
 }
 
 int arena_check(const gss_arena* ap, cudaStream_t st) {

@@ -220,6 +220,14 @@ class Arena:
     def _sync_step(self, a: GssArena) -> None:
         self.step = int(a.step)
 
+    def access(self) -> dict:
+        """AccessReport (adam.hpp:36-50) tallied on the device since the arena's first use."""
+        out = np.zeros(6, np.uint64)
+        a = self.c_struct()
+        check(lib().gss_arena_access(C.byref(a), out.ctypes.data))
+        return dict(zip(("update_passes", "touched_rows", "param_bytes", "counter_bytes", "restore_rows",
+                         "restore_read_bytes"), (int(x) for x in out)))
+
     def check_counters(self, stream=None) -> None:
         """check_counters (adam.hpp:154-158) + the sortedness flag of the last deferred pass."""
         a = self.c_struct()

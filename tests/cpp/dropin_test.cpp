@@ -106,6 +106,12 @@ void test_adam() {
   gss_b200::adam_step_dense(dev, dense.data());
   expect(same_bits(ref.w, dev.w) && same_bits(ref.m, dev.m) && same_bits(ref.v, dev.v),
          "adam_step_dense bit-exact");
+  const auto& ra = ref.access;
+  const auto& da = dev.access;
+  expect(ra.update_passes == da.update_passes && ra.touched_rows == da.touched_rows &&
+             ra.param_bytes == da.param_bytes && ra.counter_bytes == da.counter_bytes &&
+             ra.restore_rows == da.restore_rows && ra.restore_read_bytes == da.restore_read_bytes,
+         "AccessReport tally (adam.hpp:36-50) equal to the reference's");
   // InvariantViolation on unsorted ids (adam.hpp:231)
   std::vector<int> bad{5, 3};
   std::vector<float> bg(2 * dim, 0.1f);
