@@ -108,6 +108,11 @@ int gss_cull(const float* geo, int64_t n, int64_t stride, const gss_camera* cam,
              size_t workspace_bytes, gss_stream_t stream);
 
 /* ---- optimizer (adam.hpp:67-313) -------------------------------------------------------- */
+/* Arenas whose w/m/v live in pinned host memory (the offload tier, store.hpp:149-192; row-
+ * interleaved, counters on the device) are updated / restored through HBM staging: listed rows
+ * are gathered over the host link, processed on the device, and written rows scattered back, in
+ * chunks of this many bytes (ForwardStage chunks, store.hpp:204-213; default 32 MB). */
+int gss_set_host_chunk_bytes(int64_t bytes);
 /* build_group_luts (adam.hpp:67-97), fp64 on the host, cast to float. Arrays have max_delay+1
  * entries; scalars[5] = one_minus_b1, one_minus_b2, bias_correction, step_size, eps. */
 int gss_build_group_luts(double lr, double beta1, double beta2, double eps, int64_t t, int32_t max_delay,
@@ -281,6 +286,12 @@ int gss_engine_step_async(gss_engine* e, const gss_camera* cam, const float* gt_
                           int32_t* valid_count_host);
 /* Applies the lazy update still owed by an open step() segment (run() always drains itself). */
 int gss_engine_drain(gss_engine* e);
+/* SplitTable (splitter.hpp:12-23) as the OffloadEngine constructor takes it (engine.hpp:62-68):
+ * per stored camera (ncams = the engine's camera count, or 0 to clear) a split flag and the
+ * column s in (0, W). run() then culls a split camera's left [0, s] and right [s, W] viewports,
+ * renders the two sub-passes over their std::set_union and aggregates the gradients
+ * (engine.hpp:266-273, 355-371; splitter.hpp:85-123). Not inside an open step() segment. */
+int gss_engine_set_splits(gss_engine* e, int32_t ncams, const int32_t* split, const int32_t* column);
 /* snapshot (engine.hpp:91-111): restored parameters, host n x 59. */
 int gss_engine_snapshot(gss_engine* e, float* rows_out);
 /* Raw tier state (stored, not restored) for parity checks; any pointer may be NULL. */

@@ -383,9 +383,11 @@ GaussianSet<F> set_from_rows(int n, const float* rows) {
 
 // optim_d[] = lr_mean, lr_scale, lr_quat, lr_opacity, lr_sh, sh_rest_divisor, beta1, beta2, eps, scene_extent
 // flags: bit0 pipelined, bit1 dense-oracle trainer
-REF_API void* ref_engine_new(int n, const float* rows, int ncams, const void* cams, const float* gts, int defer_max,
-                             int geo_defer_max, int flags, int workers, int sh_degree, const float* bg,
-                             const double* optim_d) {
+// split / cols (optional, ncams entries): the SplitTable given to the OffloadEngine constructor
+// (engine.hpp:62-68; splitter.hpp:12-23).
+REF_API void* ref_engine_new_split(int n, const float* rows, int ncams, const void* cams, const float* gts,
+                                   int defer_max, int geo_defer_max, int flags, int workers, int sh_degree,
+                                   const float* bg, const double* optim_d, const int* split, const int* cols) {
   auto* e = new RefEngine();
   const GaussianSet<F> gs = set_from_rows(n, rows);
   std::vector<Camera<F>> cv(static_cast<const Camera<F>*>(cams), static_cast<const Camera<F>*>(cams) + ncams);
@@ -411,9 +413,23 @@ REF_API void* ref_engine_new(int n, const float* rows, int ncams, const void* ca
     ec.pipelined = (flags & 1) != 0;
     ec.sh_degree = sh_degree;
     ec.background = bgv;
-    e->eng = std::make_unique<OffloadEngine<F>>(gs, cv, gv, ec);
+    SplitTable st;
+    if (split) {
+      st.cameras.resize(ncams);
+      for (int k = 0; k < ncams; ++k) {
+        st.cameras[k].split = split[k] != 0;
+        st.cameras[k].column = cols[k];
+      }
+    }
+    e->eng = std::make_unique<OffloadEngine<F>>(gs, cv, gv, ec, st);
   }
   return e;
+}
+REF_API void* ref_engine_new(int n, const float* rows, int ncams, const void* cams, const float* gts, int defer_max,
+                             int geo_defer_max, int flags, int workers, int sh_degree, const float* bg,
+                             const double* optim_d) {
+  return ref_engine_new_split(n, rows, ncams, cams, gts, defer_max, geo_defer_max, flags, workers, sh_degree, bg,
+                              optim_d, nullptr, nullptr);
 }
 REF_API void ref_engine_free(void* h) { delete static_cast<RefEngine*>(h); }
 REF_API int ref_engine_run(void* h, int iters, float* losses, int* valid_counts) {

@@ -163,6 +163,8 @@ SIGNATURES = {
     "gss_engine_step": (C.c_int, [P, C.POINTER(GssCamera), P, P, P]),
     "gss_engine_step_async": (C.c_int, [P, C.POINTER(GssCamera), P, P, P]),
     "gss_engine_drain": (C.c_int, [P]),
+    "gss_engine_set_splits": (C.c_int, [P, C.c_int32, P, P]),
+    "gss_set_host_chunk_bytes": (C.c_int, [C.c_int64]),
     "gss_engine_snapshot": (C.c_int, [P, P]),
     "gss_engine_state": (C.c_int, [P, P, P, P, P, P, P]),
     "gss_engine_accum": (C.c_int, [P, P, P]),

@@ -72,6 +72,8 @@ void engine_run(gss_engine* e, int iters, float* losses, int32_t* valid);
 void engine_step(gss_engine* e, const gss_camera* cam, const float* gt_host, float* loss_host, int32_t* valid_host,
                  bool wait);
 void engine_drain(gss_engine* e);
+void engine_set_splits(gss_engine* e, int32_t ncams, const int32_t* split, const int32_t* column);
+void set_host_chunk_bytes(int64_t bytes);
 void engine_snapshot(gss_engine* e, float* rows_out);
 void engine_state(gss_engine* e, float* geo_w, float* ng_w, float* ng_m, float* ng_v, uint8_t* ng_counter,
                   int64_t* steps2);
@@ -420,6 +422,15 @@ GSS_API int gss_engine_step_async(gss_engine* e, const gss_camera* cam, const fl
     require_device();
     engine_step(e, cam, gt_host, loss_host, valid_count_host, false);
   });
+}
+GSS_API int gss_set_host_chunk_bytes(int64_t bytes) {
+  return guarded([&] {
+    require(bytes > 0, "chunk bytes must be > 0");
+    set_host_chunk_bytes(bytes);
+  });
+}
+GSS_API int gss_engine_set_splits(gss_engine* e, int32_t ncams, const int32_t* split, const int32_t* column) {
+  return guarded([&] { engine_set_splits(e, ncams, split, column); });
 }
 GSS_API int gss_engine_drain(gss_engine* e) {
   return guarded([&] { engine_drain(e); });

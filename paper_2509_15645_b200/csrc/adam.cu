@@ -13,7 +13,10 @@
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
+#include <atomic>
+#include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -95,6 +98,7 @@ struct ArenaDev {
   int defer_max;
   uint32_t div_magic;  // ceil(2^32 / dim)
   int64_t stride;      // floats between rows of w, m, v (>= dim)
+  int positional;      // 1: a staging copy — row of list entry k is at k * stride (host-tier passes)
 };
 
 struct GradsDev {
@@ -198,6 +202,7 @@ struct TouchList {  // rows a deferred pass touches (unordered; each row at most
   int32_t* slot;
   uint8_t* del;
   unsigned long long* count;
+  int64_t t0 = 0, t1 = INT64_MAX;  // the walk's range of list entries (a staged chunk)
 };
 
 template <int K, int MODE>
@@ -558,15 +563,17 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_WALK4_MINB) walk4_kernel(Aren
   load_packed_luts<K>(lut, L, a.dim);
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t T = (int64_t)*tl.count;
+  const int64_t T = min((int64_t)*tl.count, tl.t1);
   const int dim = a.dim;
   const int nq = (dim + 3) >> 2;  // float4 units per row
   const int dq = 32 / nq, dr = 32 - dq * nq;
   constexpr int kU = GSS_WALK4_KU;
   const int64_t wstride = (int64_t)gridDim.x * (kUpdThreads / 32) * 32;
-  for (int64_t t0 = ((int64_t)blockIdx.x * (kUpdThreads / 32) + (threadIdx.x >> 5)) * 32; t0 < T; t0 += wstride) {
+  for (int64_t t0 = tl.t0 + ((int64_t)blockIdx.x * (kUpdThreads / 32) + (threadIdx.x >> 5)) * 32; t0 < T;
+       t0 += wstride) {
     const bool mine = t0 + lane < T;
-    const int64_t my_base = mine ? (int64_t)tl.row[t0 + lane] * a.stride : -1;
+    const int64_t my_base =
+        mine ? (a.positional ? (t0 + lane - tl.t0) : (int64_t)tl.row[t0 + lane]) * a.stride : -1;
     const int32_t my_del = mine ? tl.del[t0 + lane] : 0;
     const int32_t my_slot = (mine && MODE == kDeferred) ? tl.slot[t0 + lane] : -1;
     int r = lane / nq, q = lane - (lane / nq) * nq;
@@ -841,7 +848,109 @@ ArenaDev arena_dev(const gss_arena& a) {
   d.n = a.n; d.dim = a.dim; d.defer_max = a.defer_max;
   d.div_magic = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)a.dim - 1) / (uint64_t)a.dim);
   d.stride = a.row_stride > 0 ? a.row_stride : a.dim;
+  d.positional = 0;
   return d;
+}
+
+// ---- host-tier passes through HBM staging (selective offloading, store.hpp:149-222) -----------
+// A pinned host arena is read and written over the host link. Kernels that read-modify-write host
+// rows in place interleave read requests behind posted writes on the link (measured: 6 GB/s each
+// way, profiles/r02_linkprobe.txt); pure gathers and pure scatters run at the link's rate (51 / 47
+// GB/s). So a host-tier pass moves whole rows: gather the listed rows into a positional HBM
+// staging copy, run the pass there at HBM speed, scatter the written rows back — in chunks of
+// chunk_bytes (the reference's ForwardStage chunks, store.hpp:204-222), alternating two streams so
+// one chunk's host->device gather overlaps the previous chunk's device->host scatter.
+// Staging row layout: the three float4-padded segments w | m | v back to back (3 * nq float4).
+__host__ __device__ inline int stage_stride(int dim) { return 3 * ((dim + 3) / 4) * 4; }
+
+ArenaDev staged_arena(const gss_arena& a, float* stage) {
+  ArenaDev d = arena_dev(a);
+  const int seg = (a.dim + 3) / 4 * 4;
+  d.w = stage;
+  d.m = stage + seg;
+  d.v = stage + 2 * seg;
+  d.stride = stage_stride(a.dim);
+  d.positional = 1;
+  return d;
+}
+
+#ifndef GSS_MOVE_ILP
+#define GSS_MOVE_ILP 8
+#endif
+// GATHER: stage[k] = host rows[list[t0 + k]]; else host rows[list[t0 + k]] = stage[k], for
+// k < t1 - t0. Consecutive threads take consecutive 16-byte units of a row (a row's three segments
+// are 39 contiguous units of the 640-byte interleaved row), GSS_MOVE_ILP loads in flight each.
+template <bool GATHER>
+__global__ void __launch_bounds__(256) move_rows_kernel(ArenaDev a, const int32_t* list, int64_t t0, int64_t t1,
+                                                        float* stage) {
+  const int nq = (a.dim + 3) >> 2;
+  const uint32_t upr = 3u * (uint32_t)nq;
+  // unit index math in 32 bits: callers pass at most 2^31 / upr rows per launch
+  const uint32_t total = (uint32_t)((t1 - t0) * (int64_t)upr);
+  const uint32_t step = gridDim.x * blockDim.x;
+  const int sstride = stage_stride(a.dim);
+  for (uint32_t u0 = blockIdx.x * blockDim.x + threadIdx.x; u0 < total; u0 += step * GSS_MOVE_ILP) {
+    float4 val[GSS_MOVE_ILP];
+    float* dst[GSS_MOVE_ILP];
+#pragma unroll
+    for (int i = 0; i < GSS_MOVE_ILP; ++i) {
+      const uint32_t u = u0 + i * step;
+      dst[i] = nullptr;
+      if (u < total) {
+        const uint32_t k = u / upr;
+        const int j = (int)(u - k * upr);
+        const int seg = j / nq, q = j - seg * nq;
+        const int64_t id = list[t0 + k];
+        float* hp = (seg == 0 ? a.w : (seg == 1 ? a.m : a.v)) + id * a.stride + 4 * q;
+        float* sp = stage + k * sstride + seg * nq * 4 + 4 * q;
+        if (GATHER) {
+          val[i] = ld4(hp);
+          dst[i] = sp;
+        } else {
+          val[i] = ld4(sp);
+          dst[i] = hp;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < GSS_MOVE_ILP; ++i)
+      if (dst[i]) st4(dst[i], val[i]);
+  }
+}
+constexpr int kMoveBlocks = 64;  // 64 x 256 threads x 8 units in flight: ~2 MB outstanding per direction
+
+// chunk size of the staged host-tier passes (the engine sets it from EngineConfig::chunk_bytes)
+std::atomic<int64_t> g_host_chunk_bytes{int64_t(32) << 20};
+// GSS_HOST_STAGING=0 selects the in-place zero-copy passes instead (A/B measurement only).
+bool host_staging() {
+  static const bool on = [] {
+    const char* e = std::getenv("GSS_HOST_STAGING");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// A second stream per device for the alternating chunks, plus fork / join events.
+struct AuxStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+std::mutex g_aux_mu;
+std::unordered_map<int, AuxStream> g_aux;
+AuxStream& aux_stream() {
+  int dev = 0;
+  GSS_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_aux_mu);
+  AuxStream& x = g_aux[dev];
+  if (!x.s) {
+    // highest priority: the link-bound chunks' few CTAs are scheduled ahead of a concurrent render
+    int lo = 0, hi = 0;
+    GSS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    GSS_CUDA(cudaStreamCreateWithPriority(&x.s, cudaStreamNonBlocking, hi));
+    GSS_CUDA(cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming));
+    GSS_CUDA(cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming));
+  }
+  return x;
 }
 
 void validate_arena(const gss_arena& a) {
@@ -879,10 +988,11 @@ int* err_flag_for(const gss_arena& a);
 
 // Per-arena scratch (keyed by the counter buffer, like the error flag), grown on demand from the
 // stream-ordered pool and kept: a pass allocates and frees nothing. Slot 0 serves the update passes
-// (block index + touch list), slot 1 the forwarding gather (pending block index); one writer per
+// (block index + touch list), slot 1 the forwarding gather (pending block index), slots 2 / 3 the
+// HBM staging of a host-tier update / gather (staged_walk, adam_restore); one writer per
 // arena at a time (the reference engine's DAG) keeps each slot single-stream.
 std::mutex g_scr_mu;
-std::unordered_map<const void*, std::pair<void*, size_t>> g_scr[2];
+std::unordered_map<const void*, std::pair<void*, size_t>> g_scr[4];
 char* arena_scratch(const gss_arena& a, int slot, size_t bytes, cudaStream_t st) {
   std::lock_guard<std::mutex> lk(g_scr_mu);
   auto& e = g_scr[slot][a.counter];
@@ -925,6 +1035,55 @@ int32_t* build_index(const gss_arena& a, const GradsDev& g, int* err, int32_t* b
   return bstart;
 }
 
+// Pass 2 of a deferred / flush pass over a pinned host arena: the touch list's rows in chunks,
+// each gathered into HBM staging, walked there (walk4_kernel on the positional copy) and scattered
+// back; chunk c runs on stream (c & 1) so gathers and scatters of neighbouring chunks overlap on
+// the link. The touched count is read back once (the host sizes the chunk loop).
+int64_t* pinned_count() {
+  thread_local int64_t* p = nullptr;
+  if (!p) GSS_CUDA(cudaHostAlloc((void**)&p, sizeof(int64_t), cudaHostAllocDefault));
+  return p;
+}
+char* arena_scratch(const gss_arena& a, int slot, size_t bytes, cudaStream_t st);
+template <int K, int MODE>
+void staged_walk(const gss_arena& a, const GradsDev& gd, const LutArgs<K>& L, const TouchList& tl, cudaStream_t st) {
+  int64_t* hc = pinned_count();
+  GSS_CUDA(cudaMemcpyAsync(hc, tl.count, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GSS_CUDA(cudaStreamSynchronize(st));
+  const int64_t T = *hc;
+  if (T <= 0) return;
+  const int ss = stage_stride(a.dim);
+  const int64_t C = std::max<int64_t>(1024, g_host_chunk_bytes.load() / ((int64_t)ss * 4));
+  const int64_t nch = ceil_div(T, C);
+  const int64_t crow = std::min<int64_t>(C, T);
+  float* stage = reinterpret_cast<float*>(arena_scratch(a, 2, (size_t)(nch > 1 ? 2 : 1) * crow * ss * 4, st));
+  AuxStream& ax = aux_stream();
+  if (nch > 1) {
+    GSS_CUDA(cudaEventRecord(ax.fork, st));
+    GSS_CUDA(cudaStreamWaitEvent(ax.s, ax.fork, 0));
+  }
+  const int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(crow, 32 * (kUpdThreads / 32)) * 4,
+                                                                   (int64_t)sm_count() * GSS_WALK_GRID));
+  for (int64_t c = 0; c < nch; ++c) {
+    cudaStream_t sx = (c & 1) ? ax.s : st;
+    float* buf = stage + (c & 1) * crow * ss;
+    const int64_t t0 = c * C, t1 = std::min<int64_t>(T, t0 + C);
+    move_rows_kernel<true><<<kMoveBlocks, 256, 0, sx>>>(arena_dev(a), tl.row, t0, t1, buf);
+    GSS_LAUNCHED();
+    TouchList tc = tl;
+    tc.t0 = t0;
+    tc.t1 = t1;
+    walk4_kernel<K, MODE><<<wblocks, kUpdThreads, 0, sx>>>(staged_arena(a, buf), gd, L, tc);
+    GSS_LAUNCHED();
+    move_rows_kernel<false><<<kMoveBlocks, 256, 0, sx>>>(arena_dev(a), tl.row, t0, t1, buf);
+    GSS_LAUNCHED();
+  }
+  if (nch > 1) {
+    GSS_CUDA(cudaEventRecord(ax.join, ax.s));
+    GSS_CUDA(cudaStreamWaitEvent(st, ax.join, 0));
+  }
+}
+
 template <int K, int MODE>
 void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* tmask, int64_t* tcount,
                    cudaStream_t st) {
@@ -960,6 +1119,10 @@ void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* 
       GSS_LAUNCHED();
     }
     int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, kUpdThreads), (int64_t)sm_count() * GSS_WALK_GRID));
+    if (host_resident(a) && vector_rows(a) && host_staging()) {
+      staged_walk<K, MODE>(a, gd, *L, tl, st);
+      return;
+    }
     if (host_resident(a)) wblocks = std::min(wblocks, 4 * kHostTierBlocks);  // reads + writes in flight
     if (vector_rows(a))
       walk4_kernel<K, MODE><<<wblocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, *L, tl);
@@ -1153,7 +1316,7 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_RESTORE_MINB) restore_walk_ke
     int64_t my_base = -1;
     int2 my_res = make_int2(-1, 0);
     if (j < cnt) {
-      my_base = (int64_t)ids[j] * a.stride;
+      my_base = (a.positional ? j : (int64_t)ids[j]) * a.stride;
       my_res = res[j];
     }
     int r = lane / nq, q = lane - (lane / nq) * nq;
@@ -1234,11 +1397,34 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
   int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kRestoreChunk), (int64_t)sms * 64));
   if (host_resident(a)) blocks = std::min(blocks, kHostTierBlocks);
   const size_t pb_bytes = ((size_t)(ceil_div(a.n, kRowsPerBlock) + 1) * 4 + 255) / 256 * 256;
-  const bool split = GSS_RESTORE_SPLIT && vector_rows(a) && a.defer_max < 16 && !host_resident(a);
+  const bool host = host_resident(a);
+  // Host tier with a host-known row count: gather the rows into HBM staging over the link first,
+  // then restore from the staged copy (see move_rows_kernel).
+  const bool staged = host && vector_rows(a) && a.defer_max < 16 && !count_dev && host_staging();
+  const bool split = GSS_RESTORE_SPLIT && vector_rows(a) && a.defer_max < 16 && (!host || staged);
   char* scr = arena_scratch(a, 1, pb_bytes + (split ? (size_t)std::max<int64_t>(cap, 1) * sizeof(int2) : 0), st);
   int32_t* pbstart = nullptr;
   if (pending && pd.ids) pbstart = build_index(a, pd, err_flag_for(a), reinterpret_cast<int32_t*>(scr), st);
-  if (split) {
+  if (staged) {
+    float* stage =
+        reinterpret_cast<float*>(arena_scratch(a, 3, (size_t)std::max<int64_t>(count, 1) * stage_stride(a.dim) * 4, st));
+    for (int64_t c0 = 0; c0 < count; c0 += int64_t(1) << 25) {  // 32-bit unit indices per launch
+      const int64_t c1 = std::min<int64_t>(count, c0 + (int64_t(1) << 25));
+      move_rows_kernel<true><<<kMoveBlocks, 256, 0, st>>>(arena_dev(a), ids, c0, c1,
+                                                          stage + c0 * stage_stride(a.dim));
+      GSS_LAUNCHED();
+    }
+    int2* res = reinterpret_cast<int2*>(scr + pb_bytes);
+    auto L = std::make_unique<LutArgs<16>>();
+    std::memset(L.get(), 0, sizeof(LutArgs<16>));
+    fill_luts<16>(a, t, false, *L);
+    const int rb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, 256), (int64_t)sms * 16));
+    restore_resolve_kernel<<<rb, 256, 0, st>>>(arena_dev(a), ids, count, nullptr, pd, pbstart, res);
+    GSS_LAUNCHED();
+    const int wb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kUpdThreads), (int64_t)sms * GSS_RESTORE_MINB));
+    restore_walk_kernel<16><<<wb, kUpdThreads, 0, st>>>(staged_arena(a, stage), ids, count, nullptr, pd, res,
+                                                         pending ? 1 : 0, *L, out);
+  } else if (split) {
     int2* res = reinterpret_cast<int2*>(scr + pb_bytes);
     auto L = std::make_unique<LutArgs<16>>();
     std::memset(L.get(), 0, sizeof(LutArgs<16>));
@@ -1337,6 +1523,10 @@ int arena_check(const gss_arena* ap, cudaStream_t st) {
   if (h & 1) throw Error(GSS_ERR_INVARIANT, "deferred_update: gradient ids not sorted or out of range");
   if (h & 2) throw Error(GSS_ERR_INVARIANT, "arena: defer counter out of range");
   return 0;
+}
+
+void set_host_chunk_bytes(int64_t bytes) {
+  if (bytes > 0) g_host_chunk_bytes.store(bytes);
 }
 
 }  // namespace gssd

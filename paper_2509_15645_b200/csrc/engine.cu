@@ -15,6 +15,7 @@
 // w/m/v + uint8 counters, defer_max) lives in HBM (scene fits: 180 GB) or, with
 // nongeo_on_host, in pinned host memory read by the forwarding gather through the PCIe/C2C
 // mapping and updated lazily in place (zero-copy), see DESIGN.md §offload.
+#include <cub/cub.cuh>
 #include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
@@ -50,6 +51,7 @@ gss_render_ctx* render_ctx_create();
 void arena_release(const gss_arena* ap);
 void render_ctx_timing(gss_render_ctx* ctx, bool on);
 void render_ctx_times(gss_render_ctx* ctx, double* ms2, int64_t* n2, uint64_t* contribs);
+void set_host_chunk_bytes(int64_t bytes);
 }  // namespace gssd
 
 struct gss_render_ctx;
@@ -98,6 +100,54 @@ __global__ void iota_kernel(int32_t* ids, int64_t n) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) ids[i] = (int32_t)i;
 }
+
+// ---- split cameras: std::set_union of the two sorted cull lists (engine.hpp:270-272) and the
+// slot maps of each side into the union (engine.hpp:324-332), from the two cull bit masks.
+// popc(left | right) per 32-row word; word nwords holds 0 so the scan's last entry is the count.
+__global__ void union_popc_kernel(const uint32_t* L, const uint32_t* R, int64_t nwords, int32_t* wc) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w < nwords) wc[w] = __popc(L[w] | R[w]);
+  else if (w == nwords) wc[w] = 0;
+}
+// Union ids ascending: word w's set bits at wpre[w] + rank within the word; count = wpre[nwords].
+__global__ void union_ids_kernel(const uint32_t* L, const uint32_t* R, const int32_t* wpre, int64_t nwords,
+                                 int32_t* ids, int64_t* count) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w == nwords) *count = wpre[nwords];
+  if (w >= nwords) return;
+  uint32_t u = L[w] | R[w];
+  int32_t o = wpre[w];
+  while (u) {
+    const int b = __ffs(u) - 1;
+    u &= u - 1;
+    ids[o++] = (int32_t)(w * 32 + b);
+  }
+}
+// slot of sub-list entry k in the union = number of union ids below it.
+__global__ void union_slot_kernel(const int32_t* sub, const int64_t* sub_count, const uint32_t* L, const uint32_t* R,
+                                  const int32_t* wpre, int32_t* map) {
+  const int64_t V = *sub_count;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < V; k += (int64_t)gridDim.x * blockDim.x) {
+    const int id = sub[k];
+    const int w = id >> 5;
+    const uint32_t below = (L[w] | R[w]) & ((1u << (id & 31)) - 1u);
+    map[k] = wpre[w] + __popc(below);
+  }
+}
+// aggregate_grads (splitter.hpp:85-123): out[map[k]] += in[k] over `width` columns; the left side
+// is added before the right (two launches in order) onto zeroed rows, the reference's
+// `row = 0; row += left; row += right` arithmetic.
+__global__ void add_rows_kernel(const float* in, int64_t stride, const int32_t* map, const int64_t* count, int width,
+                                float* out) {
+  const int64_t n = *count * width;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / width;
+    const int c = (int)(e - k * width);
+    out[(int64_t)map[k] * stride + c] += in[k * stride + c];
+  }
+}
+// loss = ll + rl (engine.hpp:362).
+__global__ void split_loss_kernel(const float* sl, float* loss) { *loss = sl[0] + sl[1]; }
 
 template <class T> T* dmalloc(size_t count) {
   T* p = nullptr;
@@ -195,6 +245,24 @@ struct gss_engine {
   std::vector<uint32_t> delays_ns;  // stage-delay injection (test instrumentation)
   size_t delay_next = 0;
   // iteration bookkeeping
+  // split cameras (engine.hpp:62-68, 266-273, 356-371): per stored camera the split column
+  // (-1 = rendered whole). Left / right culls, their union and the slot maps live per plan.
+  std::vector<int32_t> split_col;
+  int plan_col[3] = {-1, -1, -1};
+  int64_t split_cap = 0;                 // capacity (rows) of the split buffers
+  uint32_t* smask[2] = {nullptr, nullptr};  // left / right cull masks (stream D scratch)
+  int32_t* wpre = nullptr;               // exclusive prefix of popc(left | right) per mask word
+  void* scan_tmp = nullptr;
+  size_t scan_tmp_bytes = 0;
+  int32_t* sids[3][2] = {};              // per plan: left / right ids
+  int32_t* smap[3][2] = {};              // per plan: left / right slot -> union slot
+  int64_t* scount[3][2] = {};            // per plan: left / right counts (device)
+  int64_t* scount_host = nullptr;        // pinned [3][2]
+  int64_t scap_rows = 0;                 // capacity of the per-side gradient buffers
+  float* sg_geo[2] = {nullptr, nullptr};
+  float* sg_ng[2] = {nullptr, nullptr};
+  float* sg_m2d[2] = {nullptr, nullptr};
+  float* sloss = nullptr;                // [2] per-side losses of the iteration being rendered
   int next_iter = 0;
   int seg_begin = 0;
   int open_pending = -1;  // iteration whose lazy update is still owed
@@ -311,14 +379,97 @@ void collect_completed(gss_engine* e) {
   e->pending_times.swap(keep);
 }
 
-// engine.hpp:255-278 (no split cameras: the split machinery is §8f "next").
-void stage_cull(gss_engine* e, int g, const gss_camera& cam) {
+// Split-camera buffers sized for the current n (allocated on the first split camera; regrown
+// after densification grows n — both streams are drained first, the plans in flight use them).
+void ensure_split_buffers(gss_engine* e) {
+  if (e->split_cap >= e->n && e->smask[0]) return;
+  GSS_CUDA(cudaStreamSynchronize(e->sD));
+  GSS_CUDA(cudaStreamSynchronize(e->sH));
+  auto f = [](auto*& p) { if (p) cudaFree(p); p = nullptr; };
+  const int64_t n = std::max<int64_t>(e->n, 1);
+  const int64_t nwords = (n + 31) / 32;
+  for (int k = 0; k < 2; ++k) {
+    f(e->smask[k]);
+    e->smask[k] = dmalloc<uint32_t>((size_t)nwords);
+  }
+  f(e->wpre);
+  e->wpre = dmalloc<int32_t>((size_t)nwords + 1);
+  for (int p = 0; p < 3; ++p)
+    for (int k = 0; k < 2; ++k) {
+      f(e->sids[p][k]);
+      f(e->smap[p][k]);
+      e->sids[p][k] = dmalloc<int32_t>((size_t)n);
+      e->smap[p][k] = dmalloc<int32_t>((size_t)n);
+      if (!e->scount[p][k]) e->scount[p][k] = dmalloc<int64_t>(1);
+    }
+  if (!e->scount_host) GSS_CUDA(cudaHostAlloc((void**)&e->scount_host, 6 * sizeof(int64_t), cudaHostAllocDefault));
+  if (!e->sloss) e->sloss = dmalloc<float>(2);
+  size_t tb = 0;
+  GSS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, e->wpre, e->wpre, (int)(nwords + 1)));
+  if (tb > e->scan_tmp_bytes) {
+    f(e->scan_tmp);
+    e->scan_tmp = dmalloc<char>(tb);
+    e->scan_tmp_bytes = tb;
+  }
+  e->split_cap = n;
+}
+
+// Per-side gradient buffers of a split render (rows of the left / right sub-lists).
+void ensure_split_rows(gss_engine* e, int64_t V) {
+  if (V <= e->scap_rows) return;
+  GSS_CUDA(cudaStreamSynchronize(e->sD));
+  const int64_t cap = std::min<int64_t>(std::max<int64_t>(e->n, 1), std::max<int64_t>(V + V / 4, 1024));
+  for (int k = 0; k < 2; ++k) {
+    if (e->sg_geo[k]) cudaFree(e->sg_geo[k]);
+    if (e->sg_ng[k]) cudaFree(e->sg_ng[k]);
+    if (e->sg_m2d[k]) cudaFree(e->sg_m2d[k]);
+    e->sg_geo[k] = dmalloc<float>((size_t)cap * kGeoDim);
+    e->sg_ng[k] = dmalloc<float>((size_t)cap * kNgGradStride);
+    e->sg_m2d[k] = dmalloc<float>((size_t)cap * 2);
+  }
+  e->scap_rows = cap;
+}
+
+int split_column_of(const gss_engine* e, int g, bool stored_camera) {
+  if (!stored_camera || e->split_col.empty()) return -1;
+  return e->split_col[(size_t)g % e->split_col.size()];
+}
+
+// engine.hpp:255-278. A split camera culls the left [0, column] and right [column, W] viewports
+// (closed, as the reference's Viewport) and takes their sorted union; each side's slot map into
+// the union feeds its render pass (engine.hpp:324-332).
+void stage_cull(gss_engine* e, int g, const gss_camera& cam, int col) {
   const int p = g % 3;
   cudaStream_t s = e->sD;
-  stage_begin(e, kCull, s, g, (uint64_t)e->n * 40u);  // + 4 V for the ids (V not host-known yet)
-  const gss_viewport vp{0.0f, (float)cam.width, 0.0f, (float)cam.height};
-  cull(e->gw, e->n, kGeoDim, &cam, &vp, e->cfg.low_pass, nullptr, e->ids[p], e->count[p], e->cull_ws,
-       e->cull_ws_bytes, s);
+  e->plan_col[p] = col;
+  stage_begin(e, kCull, s, g, (uint64_t)e->n * 40u * (col >= 0 ? 2u : 1u));  // + 4 V for the ids (V not host-known yet)
+  if (col < 0) {
+    const gss_viewport vp{0.0f, (float)cam.width, 0.0f, (float)cam.height};
+    cull(e->gw, e->n, kGeoDim, &cam, &vp, e->cfg.low_pass, nullptr, e->ids[p], e->count[p], e->cull_ws,
+         e->cull_ws_bytes, s);
+  } else {
+    ensure_split_buffers(e);
+    const gss_viewport lvp{0.0f, (float)col, 0.0f, (float)cam.height};
+    const gss_viewport rvp{(float)col, (float)cam.width, 0.0f, (float)cam.height};
+    cull(e->gw, e->n, kGeoDim, &cam, &lvp, e->cfg.low_pass, e->smask[0], e->sids[p][0], e->scount[p][0], e->cull_ws,
+         e->cull_ws_bytes, s);
+    cull(e->gw, e->n, kGeoDim, &cam, &rvp, e->cfg.low_pass, e->smask[1], e->sids[p][1], e->scount[p][1], e->cull_ws,
+         e->cull_ws_bytes, s);
+    const int64_t nwords = (e->n + 31) / 32;
+    union_popc_kernel<<<(unsigned)ceil_div(nwords + 1, 256), 256, 0, s>>>(e->smask[0], e->smask[1], nwords, e->wpre);
+    GSS_LAUNCHED();
+    size_t tb = e->scan_tmp_bytes;
+    GSS_CUDA(cub::DeviceScan::ExclusiveSum(e->scan_tmp, tb, e->wpre, e->wpre, (int)(nwords + 1), s));
+    union_ids_kernel<<<(unsigned)ceil_div(nwords + 1, 256), 256, 0, s>>>(e->smask[0], e->smask[1], e->wpre, nwords,
+                                                                         e->ids[p], e->count[p]);
+    GSS_LAUNCHED();
+    for (int k = 0; k < 2; ++k) {
+      union_slot_kernel<<<148 * 8, 256, 0, s>>>(e->sids[p][k], e->scount[p][k], e->smask[0], e->smask[1], e->wpre,
+                                                e->smap[p][k]);
+      GSS_LAUNCHED();
+      GSS_CUDA(cudaMemcpyAsync(e->scount_host + 2 * p + k, e->scount[p][k], sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    }
+  }
   GSS_CUDA(cudaMemcpyAsync(e->count_host + p, e->count[p], sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   stage_end(e, kCull, s, g & 1);
   GSS_CUDA(cudaEventRecord(e->ev_cull[p].e, s));
@@ -354,7 +505,8 @@ void stage_forward_params(gss_engine* e, int g) {
     pg.stride = kNgGradStride;
     pg.col0 = 0;
   }
-  adam_restore(&e->ng, e->ids[p], V, e->count[p], pending ? &pg : nullptr, e->fwd[b], s);
+  // (the host tier takes the host-known count: its gather is staged through HBM in one pass)
+  adam_restore(&e->ng, e->ids[p], V, e->ng_host ? nullptr : e->count[p], pending ? &pg : nullptr, e->fwd[b], s);
   e->fwd_iter[b] = g;
   stage_end(e, kFwd, s, b);
   GSS_CUDA(cudaEventRecord(e->ev_fp[b].e, s));
@@ -380,24 +532,65 @@ void stage_render(gss_engine* e, int g, const gss_camera& cam, const float* gt_d
   sc.sh_degree = deg;
   for (int c = 0; c < 3; ++c) sc.background[c] = e->cfg.background[c];
   sc.low_pass = e->cfg.low_pass;
-  const gss_viewport vp{0.0f, (float)cam.width, 0.0f, (float)cam.height};
   const int64_t full = (int64_t)cam.width * cam.height * 3;
-  // Geometry half first: it reads only the geometric tier, so in pipelined mode it overlaps the
-  // forwarding gather of this iteration on stream H; colour + composite wait for fp(g).
-  rasterize_forward_geometry(e->rctx, &sc, &cam, &vp, s);
-  if (e->cfg.pipelined) {
-    GSS_CUDA(cudaStreamWaitEvent(s, e->ev_fp[b].e, 0));
-    // grads[b] is free once lazy(g-2) consumed it
-    GSS_CUDA(cudaStreamWaitEvent(s, e->ev_lazy[b].e, 0));
-  }
+  const int col = e->plan_col[p];
+  // The waits of the composite: fp(g) (pipelined), the gradient stage's previous reader, and the
+  // step's ground-truth copy.
+  // step(): the ground truth was copied in on sC, overlapping cull/geometry/gather
   const bool step_gt = e->gt_pending;
-  if (step_gt) {  // step(): the ground truth was copied in on sC, overlapping cull/geometry/gather
-    GSS_CUDA(cudaStreamWaitEvent(s, e->ev_gt.e, 0));
-    e->gt_pending = false;
+  e->gt_pending = false;
+  bool waited = false;
+  auto wait_inputs = [&] {
+    if (waited) return;
+    waited = true;
+    if (e->cfg.pipelined) {
+      GSS_CUDA(cudaStreamWaitEvent(s, e->ev_fp[b].e, 0));
+      // grads[b] is free once lazy(g-2) consumed it
+      GSS_CUDA(cudaStreamWaitEvent(s, e->ev_lazy[b].e, 0));
+    }
+    if (step_gt) GSS_CUDA(cudaStreamWaitEvent(s, e->ev_gt.e, 0));
+  };
+  if (col < 0) {
+    const gss_viewport vp{0.0f, (float)cam.width, 0.0f, (float)cam.height};
+    // Geometry half first: it reads only the geometric tier, so in pipelined mode it overlaps the
+    // forwarding gather of this iteration on stream H; colour + composite wait for fp(g).
+    rasterize_forward_geometry(e->rctx, &sc, &cam, &vp, s);
+    wait_inputs();
+    rasterize_forward_finish(e->rctx, e->image, gt_dev, full, e->d_img, loss_out, s);
+    rasterize_backward(e->rctx, e->d_img, e->g_geo[b], kGeoDim, e->g_ng[b], kNgGradStride, e->g_m2d[b], s);
+  } else {
+    // engine.hpp:355-371: two sub-passes (left, right viewport), each normalised by the full image,
+    // loss = ll + rl, gradients aggregated over the union (left added first).
+    ensure_split_rows(e, std::max(e->scount_host[2 * p], e->scount_host[2 * p + 1]));
+    for (int k = 0; k < 2; ++k) {
+      gss_render_scene ss = sc;
+      ss.ids = e->sids[p][k];
+      ss.count = e->scount_host[2 * p + k];
+      ss.slot_map = e->smap[p][k];
+      const gss_viewport vp = k == 0 ? gss_viewport{0.0f, (float)col, 0.0f, (float)cam.height}
+                                     : gss_viewport{(float)col, (float)cam.width, 0.0f, (float)cam.height};
+      rasterize_forward_geometry(e->rctx, &ss, &cam, &vp, s);
+      wait_inputs();
+      rasterize_forward_finish(e->rctx, e->image, gt_dev, full, e->d_img, e->sloss + k, s);
+      rasterize_backward(e->rctx, e->d_img, e->sg_geo[k], kGeoDim, e->sg_ng[k], kNgGradStride, e->sg_m2d[k], s);
+    }
+    GSS_CUDA(cudaMemsetAsync(e->g_geo[b], 0, (size_t)V * kGeoDim * 4, s));
+    GSS_CUDA(cudaMemsetAsync(e->g_ng[b], 0, (size_t)V * kNgGradStride * 4, s));
+    GSS_CUDA(cudaMemsetAsync(e->g_m2d[b], 0, (size_t)V * 2 * 4, s));
+    for (int k = 0; k < 2; ++k) {
+      const int64_t* cnt = e->scount[p][k];
+      const int32_t* map = e->smap[p][k];
+      add_rows_kernel<<<148 * 8, 256, 0, s>>>(e->sg_geo[k], kGeoDim, map, cnt, kGeoDim, e->g_geo[b]);
+      GSS_LAUNCHED();
+      add_rows_kernel<<<148 * 8, 256, 0, s>>>(e->sg_ng[k], kNgGradStride, map, cnt, kNgDim, e->g_ng[b]);
+      GSS_LAUNCHED();
+      add_rows_kernel<<<148 * 8, 256, 0, s>>>(e->sg_m2d[k], 2, map, cnt, 2, e->g_m2d[b]);
+      GSS_LAUNCHED();
+    }
+    split_loss_kernel<<<1, 1, 0, s>>>(e->sloss, loss_out);
+    GSS_LAUNCHED();
   }
-  rasterize_forward_finish(e->rctx, e->image, gt_dev, full, e->d_img, loss_out, s);
   if (step_gt) GSS_CUDA(cudaEventRecord(e->ev_gt_done[e->gt_cur].e, s));  // its buffer is free again
-  rasterize_backward(e->rctx, e->d_img, e->g_geo[b], kGeoDim, e->g_ng[b], kNgGradStride, e->g_m2d[b], s);
   e->g_plan[b] = p;
   stage_end(e, kRender, s, b);
   GSS_CUDA(cudaEventRecord(e->ev_render[b].e, s));
@@ -452,6 +645,7 @@ void stage_lazy(gss_engine* e, int g) {
   gr.rows = e->g_ng[b];
   gr.stride = kNgGradStride;
   gr.col0 = 0;
+  if (e->ng_host) set_host_chunk_bytes(e->cfg.chunk_bytes);  // staged host-tier chunks (store.hpp:204-213)
   adam_update(&e->ng, &gr, nullptr, slot >= 0 ? e->touched_ring + slot : nullptr, s);
   stage_end(e, kLazy, s, b);
   GSS_CUDA(cudaEventRecord(e->ev_lazy[b].e, s));
@@ -461,14 +655,16 @@ void stage_lazy(gss_engine* e, int g) {
 // (engine.hpp:434-445); pipelined mode enqueues lazy(g-1) on the host-tier stream right after
 // fp(g) so it overlaps render(g) (engine.hpp:498-508). The data each stage reads is the same in
 // both orders, so the trajectories are bitwise identical.
-void iteration(gss_engine* e, int g, const gss_camera& cam, const float* gt_dev, float* loss_out) {
+void iteration(gss_engine* e, int g, const gss_camera& cam, const float* gt_dev, float* loss_out, int col = -1) {
   nvtxRangePushA("iteration");
-  stage_cull(e, g, cam);
+  stage_cull(e, g, cam, col);
   stage_forward_params(e, g);
   const int owed = e->open_pending;
-  if (e->cfg.pipelined && owed >= 0) stage_lazy(e, owed);
+  // lazy(g-1) runs on stream H after fp(g) in both modes (pipelined: overlapping render(g) on D).
+  // It is enqueued after render(g): a host-tier lazy pass reads its touched count back before
+  // chunking (staged_walk), and render(g) must already be queued on D by then.
   stage_render(e, g, cam, gt_dev, loss_out);
-  if (!e->cfg.pipelined && owed >= 0) stage_lazy(e, owed);
+  if (owed >= 0) stage_lazy(e, owed);
   stage_geo_update(e, g);
   stage_handoff(e, g);
   e->open_pending = g;
@@ -545,20 +741,26 @@ gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss
   e->cams.assign(cams, cams + ncams);
   e->ng_host = cfg->nongeo_on_host != 0;
   GSS_CUDA(cudaStreamCreateWithFlags(&e->sD, cudaStreamNonBlocking));
-  GSS_CUDA(cudaStreamCreateWithFlags(&e->sH, cudaStreamNonBlocking));
+  {
+    // stream H (the host-tier stage, link-bound with small grids) at the highest priority, so its
+    // CTAs are scheduled ahead of the render's on stream D
+    int lo = 0, hi = 0;
+    GSS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    GSS_CUDA(cudaStreamCreateWithPriority(&e->sH, cudaStreamNonBlocking, hi));
+  }
   GSS_CUDA(cudaStreamCreateWithFlags(&e->sC, cudaStreamNonBlocking));
   const size_t nn = (size_t)std::max<int64_t>(n, 1);
   e->gw = dmalloc<float>(nn * kGeoDim);
   e->gm = dmalloc<float>(nn * kGeoDim);
   e->gv = dmalloc<float>(nn * kGeoDim);
   e->gcnt = dmalloc<uint8_t>(nn);
-  if (e->ng_host) {
+  // The host tier's w/m/v live in pinned host memory; its counters (1 byte per row, read and
+  // written by the device passes only) stay in HBM.
+  if (e->ng_host)
     GSS_CUDA(cudaHostAlloc((void**)&e->nw, nn * kNgStride * 4, cudaHostAllocMapped));
-    GSS_CUDA(cudaHostAlloc((void**)&e->ncnt, nn, cudaHostAllocMapped));
-  } else {
+  else
     e->nw = dmalloc<float>(nn * kNgStride);
-    e->ncnt = dmalloc<uint8_t>(nn);
-  }
+  e->ncnt = dmalloc<uint8_t>(nn);
   e->nm = e->nw + kNgSeg;
   e->nv = e->nw + 2 * kNgSeg;
   GSS_CUDA(cudaMemsetAsync(e->gm, 0, nn * kGeoDim * 4, e->sD));
@@ -625,11 +827,8 @@ void engine_destroy(gss_engine* e) {
   }
   auto f = [](void* p) { if (p) cudaFree(p); };
   f(e->gts_dev); f(e->gw); f(e->gm); f(e->gv); f(e->gcnt);
-  if (e->ng_host) {
-    cudaFreeHost(e->nw); cudaFreeHost(e->ncnt);
-  } else {
-    f(e->nw); f(e->ncnt);
-  }
+  if (e->ng_host) cudaFreeHost(e->nw); else f(e->nw);
+  f(e->ncnt);
   for (int p = 0; p < 3; ++p) { f(e->ids[p]); f(e->count[p]); }
   if (e->count_host) cudaFreeHost(e->count_host);
   f(e->cull_ws);
@@ -641,6 +840,11 @@ void engine_destroy(gss_engine* e) {
   for (auto ev : e->ev_free) cudaEventDestroy(ev);
   if (e->epoch) cudaEventDestroy(e->epoch);
   f(e->touched_ring);
+  for (int k = 0; k < 2; ++k) { f(e->smask[k]); f(e->sg_geo[k]); f(e->sg_ng[k]); f(e->sg_m2d[k]); }
+  for (int p = 0; p < 3; ++p)
+    for (int k = 0; k < 2; ++k) { f(e->sids[p][k]); f(e->smap[p][k]); f(e->scount[p][k]); }
+  f(e->wpre); f(e->scan_tmp); f(e->sloss);
+  if (e->scount_host) cudaFreeHost(e->scount_host);
   if (e->sD) cudaStreamDestroy(e->sD);
   if (e->sH) cudaStreamDestroy(e->sH);
   if (e->sC) cudaStreamDestroy(e->sC);
@@ -666,7 +870,7 @@ void engine_run(gss_engine* e, int iters, float* losses, int32_t* valid) {
   for (int j = 0; j < iters; ++j) {
     const int g = g0 + j;
     const size_t ci = (size_t)g % e->cams.size();
-    iteration(e, g, e->cams[ci], e->gts_dev + img * ci, e->loss_dev + j);
+    iteration(e, g, e->cams[ci], e->gts_dev + img * ci, e->loss_dev + j, split_column_of(e, g, true));
   }
   drain(e);
   e->next_iter = g0 + iters;
@@ -716,6 +920,27 @@ void engine_step(gss_engine* e, const gss_camera* cam, const float* gt_host, flo
     GSS_CUDA(cudaMemcpyAsync(loss_host, e->loss_dev, 4, cudaMemcpyDeviceToHost, e->sD));
   }
   e->launches_last = launches() - l0;
+}
+
+// SplitTable (splitter.hpp:12-23) given to the OffloadEngine constructor (engine.hpp:62-68): per
+// stored camera a split flag and column s in (0, W). Applies to run(); step() renders whole views.
+void engine_set_splits(gss_engine* e, int32_t ncams, const int32_t* split, const int32_t* column) {
+  require(e != nullptr, "engine: null");
+  require(e->open_pending < 0, "engine: set_splits inside an open step() segment; call drain first",
+          GSS_ERR_INVARIANT);
+  if (ncams == 0) {
+    e->split_col.clear();
+    return;
+  }
+  require(split && column, "engine: null split table");
+  require((size_t)ncams == e->cams.size(), "engine: split table size differs from the camera count");
+  std::vector<int32_t> cols((size_t)ncams, -1);
+  for (int i = 0; i < ncams; ++i) {
+    if (!split[i]) continue;
+    require(column[i] > 0 && column[i] < e->cams[i].width, "engine: split column must lie in (0, W)");
+    cols[i] = column[i];
+  }
+  e->split_col = cols;
 }
 
 void engine_drain(gss_engine* e) {
@@ -808,13 +1033,11 @@ void engine_densify(gss_engine* e, const gss_densify_config* dc, double extent, 
   uint8_t* gc2 = dmalloc<uint8_t>(nn);
   float* nw2 = nullptr;
   uint8_t* nc2 = nullptr;
-  if (e->ng_host) {
+  if (e->ng_host)
     GSS_CUDA(cudaHostAlloc((void**)&nw2, nn * kNgStride * 4, cudaHostAllocMapped));
-    GSS_CUDA(cudaHostAlloc((void**)&nc2, nn, cudaHostAllocMapped));
-  } else {
+  else
     nw2 = dmalloc<float>(nn * kNgStride);
-    nc2 = dmalloc<uint8_t>(nn);
-  }
+  nc2 = dmalloc<uint8_t>(nn);
   if (n2 > 0) {
     densify_apply_kernel<<<(unsigned)ceil_div(n2, 256), 256, 0, s>>>(nsurv, nchild, surv, children, e->gw, e->gm,
                                                                     e->gv, e->gcnt, e->nw, e->ncnt, gw2, gm2, gv2,
@@ -828,11 +1051,8 @@ void engine_densify(gss_engine* e, const gss_densify_config* dc, double extent, 
   arena_release(&e->geo);
   arena_release(&e->ng);
   cudaFree(e->gw); cudaFree(e->gm); cudaFree(e->gv); cudaFree(e->gcnt);
-  if (e->ng_host) {
-    cudaFreeHost(e->nw); cudaFreeHost(e->ncnt);
-  } else {
-    cudaFree(e->nw); cudaFree(e->ncnt);
-  }
+  if (e->ng_host) cudaFreeHost(e->nw); else cudaFree(e->nw);
+  cudaFree(e->ncnt);
   e->gw = gw2; e->gm = gm2; e->gv = gv2; e->gcnt = gc2;
   e->nw = nw2; e->nm = nw2 + kNgSeg; e->nv = nw2 + 2 * kNgSeg; e->ncnt = nc2;
   e->n = n2;

@@ -170,7 +170,11 @@ class Arena:
     """Arena<float> (adam.hpp:119-159) resident in device memory: w, m, v [n, dim] + uint8 counter."""
 
     def __init__(self, n: int, dim: int, groups: Sequence[GroupSpec], defer_max: int, device=None, *,
-                 interleaved: bool = False):
+                 interleaved: bool = False, host: bool = False):
+        """host=True: the row-interleaved w/m/v buffer in pinned host memory (the offload tier,
+        store.hpp:149-192; counters stay on the device) — passes over it are staged through HBM."""
+        if host and not interleaved:
+            raise ConfigError(2, "arena: a host-resident arena uses the row-interleaved layout")
         if defer_max < 0 or defer_max > 254:
             raise ConfigError(2, "arena: defer max must be in [0, 254]")
         covered = 0
@@ -186,7 +190,10 @@ class Arena:
             # float4s (16-byte aligned), the row to whole 128-byte lines (the engine's layout)
             seg = -(-dim // 4) * 4
             self.row_stride = -(-3 * seg // 32) * 32
-            self._buf = torch.zeros((n, self.row_stride), dtype=torch.float32, device=dev)
+            if host:
+                self._buf = torch.zeros((n, self.row_stride), dtype=torch.float32).pin_memory()
+            else:
+                self._buf = torch.zeros((n, self.row_stride), dtype=torch.float32, device=dev)
             self.w, self.m, self.v = (self._buf[:, i * seg:i * seg + dim] for i in range(3))
         else:
             self.row_stride = dim
@@ -195,6 +202,7 @@ class Arena:
             self.v = torch.zeros((n, dim), dtype=torch.float32, device=dev)
         self.counter = torch.zeros(max(n, 1), dtype=torch.uint8, device=dev)[:n]
         self.step = 0
+        self.host = bool(host)
 
     def __del__(self):
         # the library's scratch + sticky error flag for this arena (keyed by the counter buffer)
@@ -265,7 +273,7 @@ def deferred_update(a: Arena, grads: SparseGrads, *, want_touched: bool = True, 
     """deferred_update (adam.hpp:211-238); returns the touched ids (ascending) when asked."""
     s = a.c_struct()
     g = grads.c_struct()
-    dev = a.w.device
+    dev = a.counter.device
     touched = torch.empty(max(a.count, 1), dtype=torch.int32, device=dev) if want_touched else None
     tcount = torch.zeros(1, dtype=torch.int64, device=dev)
     check(lib().gss_deferred_update(C.byref(s), C.byref(g), _ptr(touched), _ptr(tcount), _stream(stream)))
@@ -282,12 +290,17 @@ def restore_view(a: Arena, ids: torch.Tensor, pending: Optional[SparseGrads], ou
     """restore_view (adam.hpp:252-289): pure read; arena untouched."""
     n = int(ids.numel())
     if out is None:
-        out = torch.empty((max(n, 1), a.dim), dtype=torch.float32, device=a.w.device)[:n]
+        out = torch.empty((max(n, 1), a.dim), dtype=torch.float32, device=a.counter.device)[:n]
     s = a.c_struct()
     pg = pending.c_struct() if pending is not None else None
     check(lib().gss_restore_view(C.byref(s), _ptr(ids) if n else None, n, None,
                                  C.byref(pg) if pg is not None else None, _ptr(out) if n else None, _stream(stream)))
     return out
+
+
+def set_host_chunk_bytes(nbytes: int) -> None:
+    """Chunk size of the staged host-tier passes (ForwardStage chunks, store.hpp:204-213)."""
+    check(lib().gss_set_host_chunk_bytes(int(nbytes)))
 
 
 def flush_deferred(a: Arena, stream=None) -> None:
@@ -721,7 +734,7 @@ class OffloadEngine:
     def __init__(self, init_rows: np.ndarray, cams: Sequence[GssCamera], gts: Optional[np.ndarray],
                  optim: OptimConfig = OptimConfig(), *, pipelined: bool = True, sh_degree: int = 3,
                  sh_warmup_step: int = 0, background=(0.0, 0.0, 0.0), low_pass: float = K_LOW_PASS,
-                 nongeo_on_host: bool = False):
+                 nongeo_on_host: bool = False, splits=None):
         cfg = GssEngineConfig()
         lib().gss_engine_config_default(C.byref(cfg))
         for k in ("lr_mean", "lr_scale", "lr_quat", "lr_opacity", "lr_sh", "sh_rest_divisor", "beta1", "beta2", "eps",
@@ -742,6 +755,24 @@ class OffloadEngine:
                                          None if self._gts is None else self._gts.ctypes.data, C.byref(cfg))
         if not self.h:
             check(int(1) if "device" in lib().gss_last_error().decode() else 2)
+        if splits is not None:
+            self.set_splits(splits)
+
+    def set_splits(self, splits):
+        """SplitTable (splitter.hpp:12-23; OffloadEngine constructor, engine.hpp:62-68): one
+        (split, column) pair per stored camera — or SplitEntry-like objects with .split/.column, or
+        the dicts of evalsplit.compute_split_points. run() renders split cameras as two sub-passes."""
+        flags = np.zeros(len(splits), np.int32)
+        cols = np.zeros(len(splits), np.int32)
+        for i, e in enumerate(splits):
+            if isinstance(e, dict):
+                sp, col = e["split"], e["column"]
+            elif hasattr(e, "split"):
+                sp, col = e.split, e.column
+            else:
+                sp, col = e
+            flags[i], cols[i] = int(bool(sp)), int(col)
+        check(lib().gss_engine_set_splits(self.h, len(splits), flags.ctypes.data, cols.ctypes.data))
 
     def close(self):
         if getattr(self, "h", None):

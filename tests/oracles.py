@@ -55,6 +55,8 @@ def ref():
             "ref_synth_scene": (None, [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P, P]),
             "ref_look_at_camera": (None, [P, P, F32, F32, C.c_int, C.c_int, F32, F32, P]),
             "ref_engine_new": (P, [C.c_int, P, C.c_int, P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P]),
+            "ref_engine_new_split": (P, [C.c_int, P, C.c_int, P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P,
+                                         P, P]),
             "ref_engine_free": (None, [P]),
             "ref_engine_run": (C.c_int, [P, C.c_int, P, P]),
             "ref_engine_snapshot": (None, [P, P]),
@@ -316,7 +318,7 @@ OPTIM_DEFAULT = np.array([1.6e-4, 5e-3, 1e-3, 5e-2, 2.5e-3, 20.0, 0.9, 0.999, 1e
 
 class RefEngine:
     def __init__(self, rows, cams, gts, defer_max=15, geo_defer_max=0, pipelined=False, dense=False, workers=1,
-                 sh_degree=3, bg=(0, 0, 0), optim=OPTIM_DEFAULT):
+                 sh_degree=3, bg=(0, 0, 0), optim=OPTIM_DEFAULT, splits=None):
         rows = np.ascontiguousarray(rows, np.float32)
         cams = np.ascontiguousarray(cams, np.float32)
         gts = np.ascontiguousarray(gts, np.float32)
@@ -324,8 +326,15 @@ class RefEngine:
         flags = (1 if pipelined else 0) | (2 if dense else 0)
         bga = np.asarray(bg, np.float32)
         opt = np.ascontiguousarray(optim, np.float64)
-        self.h = ref().ref_engine_new(self.n, _p(rows), cams.shape[0], _p(cams), _p(gts), defer_max, geo_defer_max,
-                                      flags, workers, sh_degree, _p(bga), _p(opt))
+        if splits is None:
+            self.h = ref().ref_engine_new(self.n, _p(rows), cams.shape[0], _p(cams), _p(gts), defer_max,
+                                          geo_defer_max, flags, workers, sh_degree, _p(bga), _p(opt))
+        else:  # (split, column) per camera: the SplitTable of the OffloadEngine constructor
+            sp = np.ascontiguousarray([int(bool(a)) for a, _ in splits], np.int32)
+            co = np.ascontiguousarray([int(b) for _, b in splits], np.int32)
+            self.h = ref().ref_engine_new_split(self.n, _p(rows), cams.shape[0], _p(cams), _p(gts), defer_max,
+                                                geo_defer_max, flags, workers, sh_degree, _p(bga), _p(opt),
+                                                _p(sp), _p(co))
 
     def __del__(self):
         if getattr(self, "h", None):

@@ -214,3 +214,44 @@ def test_engine_layout_interleaved_aligned_grads_bitwise(ref, defer_max):
     ra.flush()
     G.flush_deferred(ga)
     assert_same(ra, ga)
+
+
+@pytest.mark.parametrize("defer_max", [1, 15])
+def test_host_tier_arena_staged_passes_bitwise(ref, defer_max):
+    """The pinned host tier (store.hpp:149-192): deferred passes and the forwarding gather run
+    through HBM staging in chunks (two alternating streams), bit-identical to the reference; a
+    small chunk size forces several chunks per pass."""
+    rng = np.random.default_rng(77 + defer_max)
+    n, dim = 6000, 49
+    ra = O.RefArena(n, dim, GROUPS49, defer_max)
+    ga = G.Arena(n, dim, [G.GroupSpec(f"g{i}", c0, d, G.Hyperparams(lr)) for i, (c0, d, lr) in enumerate(GROUPS49)],
+                 defer_max, interleaved=True, host=True)
+    assert not ga.w.is_cuda and ga.counter.is_cuda
+    w0 = rng.uniform(-1, 1, (n, dim)).astype(np.float32)
+    ra.w[:] = w0
+    ga.w.copy_(torch.from_numpy(w0))
+    G.set_host_chunk_bytes(1024 * 156 * 4)  # 1024 rows per chunk
+    try:
+        for step in range(24):
+            dens = 0.0 if step % 9 == 4 else rng.uniform(0.05, 0.6)
+            ids = np.nonzero(rng.uniform(size=n) < dens)[0].astype(np.int32)
+            rows = rng.normal(size=(ids.size, dim)).astype(np.float32)
+            if step % 5 == 2:  # forwarding gather with this pass's gradients pending
+                q = np.nonzero(rng.uniform(size=n) < 0.5)[0].astype(np.int32)
+                pend = G.SparseGrads(torch.from_numpy(ids).cuda(), torch.from_numpy(rows).cuda(), dim)
+                got = G.restore_view(ga, torch.from_numpy(q).cuda(), pend).cpu().numpy()
+                assert np.array_equal(bits(got), bits(ra.restore(q, (ids, rows, dim, 0))))
+            t_ref = ra.deferred(ids, rows, dim)
+            t_gpu = G.deferred_update(ga, G.SparseGrads(torch.from_numpy(ids).cuda(), torch.from_numpy(rows).cuda(), dim))
+            torch.cuda.synchronize()
+            assert np.array_equal(t_ref, t_gpu.cpu().numpy())
+            assert_same(ra, ga)
+        q = np.arange(n, dtype=np.int32)
+        got0 = G.restore_view(ga, torch.from_numpy(q).cuda(), None).cpu().numpy()
+        assert np.array_equal(bits(got0), bits(ra.restore(q)))
+        G.flush_deferred(ga)
+        ra.flush()
+        torch.cuda.synchronize()
+        assert_same(ra, ga)
+    finally:
+        G.set_host_chunk_bytes(32 << 20)
