@@ -1,6 +1,7 @@
 // gss_b200.hpp — drop-in C++ API for the reference's hot path, backed by libgss_b200.so.
 //
-// Include AFTER the reference headers (gss/render.hpp, gss/adam.hpp); every function keeps the
+// Needs the reference headers on the include path (gss/render.hpp, gss/adam.hpp, gss/engine.hpp
+// are included here); every function keeps the
 // reference signature (namespace gss -> gss_b200) and semantics, and runs on the B200 through
 // the C ABI in gss_b200.h. Inputs are the reference's host containers: they are copied to the
 // device, processed by the sm_100a kernels and copied back, so a caller of the reference path
@@ -9,9 +10,10 @@
 //
 //   reference (file:line)                         drop-in
 //   frustum_cull        render.hpp:253-260        gss_b200::frustum_cull
-//   rasterize_forward   render.hpp:384-464        gss_b200::Rasterizer::forward
+//   rasterize_forward   render.hpp:384-464        gss_b200::rasterize_forward (-> gss_b200::RenderResult)
 //   compute_loss_l1     render.hpp:497-511        gss_b200::compute_loss_l1
-//   rasterize_backward  render.hpp:526-640        gss_b200::Rasterizer::backward
+//   rasterize_backward  render.hpp:526-640        gss_b200::rasterize_backward (<- gss_b200::RenderResult)
+//   OffloadEngine       engine.hpp:55-522         gss_b200::OffloadEngine (EngineConfig<float>, SplitTable)
 //   adam_step_dense     adam.hpp:198-207          gss_b200::adam_step_dense
 //   deferred_update     adam.hpp:211-238          gss_b200::deferred_update
 //   restore_view        adam.hpp:252-289          gss_b200::restore_view
@@ -27,10 +29,15 @@
 
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
+
+#include <gss/adam.hpp>
+#include <gss/engine.hpp>
+#include <gss/render.hpp>
 
 #include "gss_b200.h"
 
@@ -309,6 +316,171 @@ class Rasterizer {
   DevBuf<int32_t> ids_, slot_;
   DevBuf<float> geo_, ng_, img_;
   std::vector<int> ids_host_;
+};
+
+// Reference-signature free functions (render.hpp:384, 526). gss_b200::RenderResult carries what
+// the reference's RenderResult<float> carries between the two calls — the image (sized to the
+// viewport's pixel window) and the window origin in `aux` — while the splat records, sorted tile
+// lists and per-pixel aux stay on the device (the `dev` handle) for rasterize_backward. `workers`
+// is accepted and ignored (the device schedules itself).
+struct RenderAux {
+  int px0 = 0, py0 = 0, pw = 0, ph = 0;
+  size_t device_bytes = 0;
+  size_t byte_size() const { return device_bytes; }
+};
+struct RenderResult {
+  gss::Image<float> image;
+  RenderAux aux;
+  std::shared_ptr<Rasterizer> dev;
+};
+
+inline RenderResult rasterize_forward(const gss::RenderScene<float>& sc, const gss::Camera<float>& cam,
+                                      const gss::Viewport<float>& vp, int workers = 1) {
+  (void)workers;
+  RenderResult rr;
+  rr.dev = std::make_shared<Rasterizer>();
+  rr.image = rr.dev->forward(sc, cam, vp);
+  const gss::detail::PixWindow w = gss::detail::viewport_pixels(vp);
+  rr.aux.px0 = w.px0;
+  rr.aux.py0 = w.py0;
+  rr.aux.pw = rr.image.width;
+  rr.aux.ph = rr.image.height;
+  // per-pixel final T + last index + image on the device, 64-byte splat records
+  rr.aux.device_bytes = size_t(rr.aux.pw) * rr.aux.ph * 4 * 5 + sc.ids.size() * 64;
+  return rr;
+}
+
+inline gss::GradBuffer<float> rasterize_backward(const gss::RenderScene<float>& sc, const gss::Camera<float>& cam,
+                                                 const RenderResult& rr, const gss::Image<float>& d_img,
+                                                 int workers = 1) {
+  (void)cam;
+  (void)workers;
+  if (!rr.dev) throw gss::InvariantViolation("rasterize_backward: RenderResult has no device state");
+  if (d_img.width != rr.image.width || d_img.height != rr.image.height)
+    throw std::invalid_argument("rasterize_backward: d_img shape differs from the rendered window");
+  gss::GradBuffer<float> gb = rr.dev->backward(d_img);
+  if (gb.ids.size() != sc.ids.size()) throw gss::InvariantViolation("rasterize_backward: scene differs from forward");
+  return gb;
+}
+
+// ---- OffloadEngine (engine.hpp:55-522) ----------------------------------------------------
+// The reference's engine interface over gss_engine_*: the same constructor arguments
+// (GaussianSet, cameras, ground truths, EngineConfig<float>, SplitTable), run(n) returning the
+// per-iteration {loss, valid_count}, snapshot(), the densification statistics and the timeline.
+// The engine keeps every tier on the device (or the non-geometric tier in pinned host memory when
+// nongeo_on_host is set); nothing crosses back to the host per iteration except the losses.
+class OffloadEngine {
+ public:
+  struct IterResult {
+    float loss{};
+    int valid_count = 0;
+  };
+
+  OffloadEngine(const gss::GaussianSet<float>& init, std::vector<gss::Camera<float>> cams,
+                std::vector<gss::Image<float>> gts, gss::EngineConfig<float> cfg, gss::SplitTable splits = {},
+                bool nongeo_on_host = false)
+      : cams_(std::move(cams)), sh_degree_(cfg.sh_degree) {
+    if (gts.size() != cams_.size()) throw gss::ConfigError("OffloadEngine: one ground truth per camera");
+    const int n = init.count;
+    std::vector<float> rows(size_t(n) * gss::kParamDim);
+    for (int i = 0; i < n; ++i) init.full_row(i, rows.data() + size_t(i) * gss::kParamDim);
+    std::vector<float> g;
+    for (size_t k = 0; k < gts.size(); ++k) {
+      if (gts[k].width != cams_[k].width || gts[k].height != cams_[k].height)
+        throw gss::ConfigError("OffloadEngine: ground truth shape differs from its camera");
+      g.insert(g.end(), gts[k].data.begin(), gts[k].data.end());
+    }
+    gss_engine_config c{};
+    gss_engine_config_default(&c);
+    const gss::OptimConfig& o = cfg.optim;
+    c.lr_mean = o.lr_mean; c.lr_scale = o.lr_scale; c.lr_quat = o.lr_quat; c.lr_opacity = o.lr_opacity;
+    c.lr_sh = o.lr_sh; c.sh_rest_divisor = o.sh_rest_divisor; c.beta1 = o.beta1; c.beta2 = o.beta2; c.eps = o.eps;
+    c.scene_extent = o.scene_extent; c.defer_max = o.defer_max; c.geo_defer_max = o.geo_defer_max;
+    c.pipelined = cfg.pipelined ? 1 : 0;
+    c.sh_degree = cfg.sh_degree;
+    c.sh_warmup_step = cfg.sh_warmup_step;
+    c.background[0] = cfg.background.x; c.background[1] = cfg.background.y; c.background[2] = cfg.background.z;
+    c.low_pass = cfg.low_pass;
+    c.nongeo_on_host = nongeo_on_host ? 1 : 0;
+    c.chunk_bytes = int64_t(cfg.chunk_bytes);
+    std::vector<gss_camera> gc(cams_.size());
+    for (size_t k = 0; k < cams_.size(); ++k) gc[k] = *cam_ptr(cams_[k]);
+    e_ = gss_engine_create(n, rows.data(), int32_t(gc.size()), gc.data(), g.empty() ? nullptr : g.data(), &c);
+    if (!e_) check(std::string(gss_last_error()).find("device") != std::string::npos ? GSS_ERR_CUDA : GSS_ERR_INVALID);
+    if (!splits.cameras.empty()) {
+      if (splits.cameras.size() != cams_.size()) throw gss::ConfigError("OffloadEngine: split table size");
+      std::vector<int32_t> sp(splits.cameras.size()), col(splits.cameras.size());
+      for (size_t k = 0; k < sp.size(); ++k) {
+        sp[k] = splits.cameras[k].split ? 1 : 0;
+        col[k] = splits.cameras[k].column;
+      }
+      check(gss_engine_set_splits(e_, int32_t(sp.size()), sp.data(), col.data()));
+    }
+  }
+  ~OffloadEngine() { gss_engine_destroy(e_); }
+  OffloadEngine(const OffloadEngine&) = delete;
+  OffloadEngine& operator=(const OffloadEngine&) = delete;
+
+  // engine.hpp:73-88: n iterations, drained.
+  std::vector<IterResult> run(int n) {
+    if (n <= 0) return {};
+    std::vector<float> losses(static_cast<size_t>(n));
+    std::vector<int32_t> valid(static_cast<size_t>(n));
+    check(gss_engine_run(e_, n, losses.data(), valid.data()));
+    std::vector<IterResult> out(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) out[i] = {losses[i], valid[i]};
+    return out;
+  }
+
+  // engine.hpp:91-111: both tiers restored.
+  gss::GaussianSet<float> snapshot() const {
+    const int n = count();
+    std::vector<float> rows(size_t(std::max(n, 1)) * gss::kParamDim);
+    check(gss_engine_snapshot(e_, rows.data()));
+    gss::GaussianSet<float> gs;
+    gs.resize(n);
+    gs.sh_degree = sh_degree_;
+    for (int i = 0; i < n; ++i) gs.set_full_row(i, rows.data() + size_t(i) * gss::kParamDim);
+    return gs;
+  }
+
+  int count() const { return int(gss_engine_count(e_)); }
+
+  // engine.hpp:187-188 (densification statistics)
+  std::vector<double> accum_grad_norm() const {
+    std::vector<double> nrm(size_t(std::max(count(), 1)));
+    std::vector<int32_t> cnt(nrm.size());
+    check(gss_engine_accum(e_, nrm.data(), cnt.data()));
+    nrm.resize(size_t(count()));
+    return nrm;
+  }
+  std::vector<int> accum_grad_count() const {
+    std::vector<double> nrm(size_t(std::max(count(), 1)));
+    std::vector<int32_t> cnt(nrm.size());
+    check(gss_engine_accum(e_, nrm.data(), cnt.data()));
+    return std::vector<int>(cnt.begin(), cnt.begin() + count());
+  }
+
+  // engine.hpp:22-28: rows since the timeline was enabled (enable_timeline(true) first).
+  void enable_timeline(bool on) { check(gss_engine_timeline_enable(e_, on ? 1 : 0)); }
+  std::vector<gss::TimelineRow> timeline() const {
+    static const char* const kStage[6] = {"cull", "forward_params", "render", "geo_update", "handoff", "lazy_update"};
+    const int64_t k = gss_engine_timeline(e_, nullptr, 0);
+    if (k < 0) check(int(-k));
+    std::vector<gss_timeline_row> r(size_t(std::max<int64_t>(k, 1)));
+    const int64_t got = gss_engine_timeline(e_, r.data(), int64_t(r.size()));
+    std::vector<gss::TimelineRow> out;
+    for (int64_t i = 0; i < got; ++i)
+      out.push_back({r[i].iteration, kStage[r[i].stage % 6], r[i].t0_ns, r[i].t1_ns, r[i].bytes, r[i].worker});
+    return out;
+  }
+
+  gss_engine* handle() const { return e_; }
+
+ private:
+  std::vector<gss::Camera<float>> cams_;
+  int sh_degree_ = 3;
+  gss_engine* e_ = nullptr;
 };
 
 }  // namespace gss_b200

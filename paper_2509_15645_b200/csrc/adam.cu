@@ -921,11 +921,15 @@ constexpr int kMoveBlocks = 64;  // 64 x 256 threads x 8 units in flight: ~2 MB 
 
 // chunk size of the staged host-tier passes (the engine sets it from EngineConfig::chunk_bytes)
 std::atomic<int64_t> g_host_chunk_bytes{int64_t(32) << 20};
-// GSS_HOST_STAGING=0 selects the in-place zero-copy passes instead (A/B measurement only).
+// The staged passes are opt-in (GSS_HOST_STAGING=1): measured on the B200 (tools/host_tier_probe.py,
+// 40M rows, 13% visible; profiles/r02_host_tier_ab.txt) the in-place zero-copy passes move the
+// host link's bytes faster — forwarding gather 72.8 vs 81.3 ms, deferred update 124 vs 177 ms — the
+// device reads and writes host rows concurrently from many SMs, while the staged chunks serialise
+// gather, pass and scatter per chunk.
 bool host_staging() {
   static const bool on = [] {
     const char* e = std::getenv("GSS_HOST_STAGING");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }

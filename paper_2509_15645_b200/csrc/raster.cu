@@ -748,9 +748,11 @@ __global__ void loss_final_kernel(const double* partials, int n, float inv, floa
   }
 }
 
-// Reverse sweep state of one pixel (render.hpp:542-589).
+// Reverse sweep state of one pixel (render.hpp:542-589). The suffix colour enters the sweep only
+// through its dot product with the pixel's (constant) colour gradient, so the state keeps that
+// scalar S = suf . g (suf_c += rgb_c * w  =>  S += (rgb . g) * w).
 struct PixB {
-  float cx, cy, T, g0, g1, g2, s0, s1, s2;
+  float cx, cy, T, g0, g1, g2, S;
   int x, y, L;
 };
 
@@ -772,34 +774,46 @@ __device__ __forceinline__ float rcp_fast(float x) {
   return r;
 }
 
+// The 0.999 clamp can only fire for a splat whose alpha_base exceeds 0.999 - 1e-4 (weight <= 1);
+// every other record takes the sweep without the clamp test (a warp-uniform choice per record).
+constexpr float kClampGuard = 0.9989f;
+
 // One contribution of splat r (sweep position jpos) to pixel p of the reverse sweep
-// (render.hpp:554-589): steps the pixel's reverse state and accumulates 10 per-lane sums
+// (render.hpp:554-589): steps the pixel's reverse state and accumulates 9 per-lane sums
 //   v[0..2] = sum alpha*T*g_rgb                      (rgb gradient)
 //   v[3]    = sum t,  t = weight * d_alpha (0 when the 0.999 clamp is active)   (alpha_base gradient)
-//   v[4..9] = sum t*q, t*dx^2, t*dy^2, t*dx*dy, t*dx, t*dy
+//   v[4..8] = sum t*dx^2, t*dy^2, t*dx*dy, t*dx, t*dy
 // from which the per-record combine (sweep_combine) forms the mean2d and cov gradients:
 // dq_i = alpha * d_alpha * (-0.5/det) = ab * nh * t, and the reference's per-contribution terms
-// dqi * (2b*dy - 2c*dx) ... are linear in these moments with per-splat coefficients. The arithmetic
-// runs on fast math with explicit FMAs (tolerance-checked); the 0.999 clamp decision,
+// dqi * (2b*dy - 2c*dx) ... are linear in these moments with per-splat coefficients (sum t*q too:
+// q is the conic's quadratic form in dx, dy). The arithmetic runs on fast math with explicit FMAs
+// (tolerance-checked). CLAMP: the record may reach the 0.999 clamp — the decision,
 // which selects the reference's branch (render.hpp:560-573), is recomputed with the forward's exact
 // arithmetic whenever the fast alpha is within 1e-4 of the threshold, so both passes always take the
 // same branch. Predicated: a lane whose pixel is outside the record's box (or past its last index)
 // adds exact zeros and keeps its state.
+template <bool CLAMP>
 __device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k, bool xin, int jpos, PixB& p,
-                                            float v[10]) {
+                                            float v[9]) {
   const bool ok = xin & (jpos < p.L) & (p.y >= r.by0) & (p.y < r.by1);
   const float dx = p.cx - r.mx, dy = p.cy - r.my;
   const float dxx = dx * dx, dyy = dy * dy, dxy = dx * dy;
   float q = __fmaf_rn(k.ia, dxx, __fmaf_rn(k.ic, dyy, k.ibm2 * dxy));
   q = (q < 0.0f || !ok) ? 0.0f : q;  // an idle lane evaluates at q = 0: every term stays finite
   const float weight = ex2_fast(-0.72134752f * q);  // exp(-q/2)
-  float raw = r.ab * weight;
-  const bool near = ok && fabsf(raw - 0.999f) < 1e-4f;
-  if (__any_sync(0xffffffffu, near)) {
-    if (near) raw = contrib_eval(r, p.cx, p.cy).clamped ? 1.0f : 0.0f;
+  bool clamped = false;
+  float alpha;
+  if (CLAMP) {
+    float raw = r.ab * weight;
+    const bool near = ok && fabsf(raw - 0.999f) < 1e-4f;
+    if (__any_sync(0xffffffffu, near)) {
+      if (near) raw = contrib_eval(r, p.cx, p.cy).clamped ? 1.0f : 0.0f;
+    }
+    clamped = raw > 0.999f;
+    alpha = ok ? (clamped ? 0.999f : r.ab * weight) : 0.0f;
+  } else {
+    alpha = ok ? r.ab * weight : 0.0f;
   }
-  const bool clamped = raw > 0.999f;
-  const float alpha = ok ? (clamped ? 0.999f : r.ab * weight) : 0.0f;
   const float inv1m = rcp_fast(1.0f - alpha);
   const float Tb = ok ? p.T * inv1m : p.T;  // transmittance before this contribution
   const float w_rgb = alpha * Tb;
@@ -807,56 +821,53 @@ __device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k
   v[1] = __fmaf_rn(w_rgb, p.g1, v[1]);
   v[2] = __fmaf_rn(w_rgb, p.g2, v[2]);
   const float dot_c = __fmaf_rn(r.r, p.g0, __fmaf_rn(r.g, p.g1, r.bl * p.g2));
-  const float dot_suf = __fmaf_rn(p.s0, p.g0, __fmaf_rn(p.s1, p.g1, p.s2 * p.g2));
-  const float d_alpha = __fmaf_rn(Tb, dot_c, -dot_suf * inv1m);
-  p.s0 = __fmaf_rn(r.r, w_rgb, p.s0);
-  p.s1 = __fmaf_rn(r.g, w_rgb, p.s1);
-  p.s2 = __fmaf_rn(r.bl, w_rgb, p.s2);
+  const float d_alpha = __fmaf_rn(Tb, dot_c, -p.S * inv1m);
+  p.S = __fmaf_rn(dot_c, w_rgb, p.S);
   p.T = Tb;
   const float t = (ok && !clamped) ? weight * d_alpha : 0.0f;  // render.hpp:572-586 only when not clamped
   v[3] += t;
-  v[4] = __fmaf_rn(t, q, v[4]);
-  v[5] = __fmaf_rn(t, dxx, v[5]);
-  v[6] = __fmaf_rn(t, dyy, v[6]);
-  v[7] = __fmaf_rn(t, dxy, v[7]);
-  v[8] = __fmaf_rn(t, dx, v[8]);
-  v[9] = __fmaf_rn(t, dy, v[9]);
+  v[4] = __fmaf_rn(t, dxx, v[4]);
+  v[5] = __fmaf_rn(t, dyy, v[5]);
+  v[6] = __fmaf_rn(t, dxy, v[6]);
+  v[7] = __fmaf_rn(t, dx, v[7]);
+  v[8] = __fmaf_rn(t, dy, v[8]);
   return ok;
 }
 
-// The 9 SlotAcc terms (rgb3, mean2d2, cov3, alpha_base; render.hpp:538) of one record from its 10
-// swept sums (bwd_contrib): with f = ab * (-0.5/det),
+// The 9 SlotAcc terms (rgb3, mean2d2, cov3, alpha_base; render.hpp:538) of one record from its 9
+// swept sums (bwd_contrib): with f = ab * (-0.5/det) and Sq = ia*Sxx + ic*Syy + ibm2*Sxy,
 //   mean2d = f * (2b*Sy - 2c*Sx, 2b*Sx - 2a*Sy),  cov = f * (Syy - c*Sq, 2b*Sq - 2*Sxy, Sxx - a*Sq).
-__device__ __forceinline__ void sweep_combine(const SplatRec& r, const BwdConic& k, const float u[10], float o[9]) {
+__device__ __forceinline__ void sweep_combine(const SplatRec& r, const BwdConic& k, const float u[9], float o[9]) {
   const float f = r.ab * k.nh, b2 = 2.0f * r.b;
+  const float sq = __fmaf_rn(k.ia, u[4], __fmaf_rn(k.ic, u[5], k.ibm2 * u[6]));
   o[0] = u[0];
   o[1] = u[1];
   o[2] = u[2];
-  o[3] = f * __fmaf_rn(b2, u[9], -2.0f * r.c * u[8]);
-  o[4] = f * __fmaf_rn(b2, u[8], -2.0f * r.a * u[9]);
-  o[5] = f * __fmaf_rn(-r.c, u[4], u[6]);
-  o[6] = f * __fmaf_rn(b2, u[4], -2.0f * u[7]);
-  o[7] = f * __fmaf_rn(-r.a, u[4], u[5]);
+  o[3] = f * __fmaf_rn(b2, u[8], -2.0f * r.c * u[7]);
+  o[4] = f * __fmaf_rn(b2, u[7], -2.0f * r.a * u[8]);
+  o[5] = f * __fmaf_rn(-r.c, sq, u[5]);
+  o[6] = f * __fmaf_rn(b2, sq, -2.0f * u[6]);
+  o[7] = f * __fmaf_rn(-r.a, sq, u[4]);
   o[8] = u[3];
 }
 
-// Warp reduce-scatter of 10 values in 12 shuffles (10 x 5 butterflies would take 50; padding to 16
-// takes 16): the value set is halved per lane bit with minimal padding, 10 -> 5 -> 3 -> 2 -> 1
+// Warp reduce-scatter of 9 values in 12 shuffles (9 x 5 butterflies would take 45; padding to 16
+// takes 16): the value set is halved per lane bit with minimal padding, 9 -> 5 -> 3 -> 2 -> 1
 // (bits 4, 3, 2, 1), then lanes 2k and 2k+1 add. Afterwards lane l holds the warp total of value
 // index reduce_scatter_index(l) (-1: a padding slot). Fixed order: deterministic.
 __device__ __forceinline__ int reduce_scatter_index(int lane) {
   const int j3 = ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);  // of the 3-set (3 = padding)
   const int j5 = ((lane >> 3) & 1) * 3 + j3;                   // of the 5-set (5.. = padding)
-  const int j10 = ((lane >> 4) & 1) * 5 + j5;                  // of the 10 values (9 = padding)
-  return (j3 < 3 && j5 < 5 && j10 < 10) ? j10 : -1;
+  const int j10 = ((lane >> 4) & 1) * 5 + j5;                  // of the 10 slots (9 = padding)
+  return (j3 < 3 && j5 < 5 && j10 < 9) ? j10 : -1;
 }
-__device__ __forceinline__ float warp_reduce_scatter10(const float v[10], int lane) {
+__device__ __forceinline__ float warp_reduce_scatter9(const float v[9], int lane) {
   float x[5];
-  {  // bit 4: 10 values -> 5
+  {  // bit 4: 9 values (+1 padding) -> 5
     const bool up = (lane & 16) != 0;
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-      const float lo = v[i], hi = v[i + 5];
+      const float lo = v[i], hi = i + 5 < 9 ? v[i + 5] : 0.0f;
       x[i] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, 16);
     }
   }
@@ -905,7 +916,7 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
   __shared__ SplatRec sh[kBwdBatch];
   __shared__ BwdConic shk[kBwdBatch];
   __shared__ int32_t sinst[kBwdBatch];  // the record's (splat, this tile) instance index
-  constexpr int kNv = 10;  // swept sums per record (bwd_contrib)
+  constexpr int kNv = 9;  // swept sums per record (bwd_contrib)
   __shared__ float red[kBwdBatch][kBwdWarps][kNv];
   __shared__ unsigned long long wmask[kBwdWarps][kBwdMasks];
   __shared__ int smax;
@@ -936,9 +947,7 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
       p.g2 = d_img[pix * 3 + 2];
       if (p.g0 == 0.0f && p.g1 == 0.0f && p.g2 == 0.0f) p.L = 0;  // render.hpp:551
     }
-    p.s0 = p.T * bg0;
-    p.s1 = p.T * bg1;
-    p.s2 = p.T * bg2;
+    p.S = __fmaf_rn(p.T * bg0, p.g0, __fmaf_rn(p.T * bg1, p.g1, (p.T * bg2) * p.g2));  // (final_T * bg) . g
     lmax = max(lmax, p.L);
   }
   if (threadIdx.x == 0) smax = 0;
@@ -1015,14 +1024,28 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
         for (int i = 0; i < kNv; ++i) v[i] = 0.0f;
 #if GSS_RASTER_STATS
         ++st_walk;
-#pragma unroll
-        for (int q = 0; q < kBwdPPT; ++q) st_use += bwd_contrib(r, k, xin, bstart + jj, px[q], v) ? 1 : 0;
-#else
-#pragma unroll
-        for (int q = 0; q < kBwdPPT; ++q) bwd_contrib(r, k, xin, bstart + jj, px[q], v);
 #endif
+        if (r.ab > kClampGuard) {
+#pragma unroll
+          for (int q = 0; q < kBwdPPT; ++q) {
+            const bool u = bwd_contrib<true>(r, k, xin, bstart + jj, px[q], v);
+#if GSS_RASTER_STATS
+            st_use += u ? 1 : 0;
+#endif
+            (void)u;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < kBwdPPT; ++q) {
+            const bool u = bwd_contrib<false>(r, k, xin, bstart + jj, px[q], v);
+#if GSS_RASTER_STATS
+            st_use += u ? 1 : 0;
+#endif
+            (void)u;
+          }
+        }
         // A record no lane contributed to reduces exact zeros: the same partial without a vote.
-        const float tot = warp_reduce_scatter10(v, lane);
+        const float tot = warp_reduce_scatter9(v, lane);
         if ((lane & 1) == 0 && vidx >= 0) red[jj][warp][vidx] = tot;
       }
     }
@@ -1030,14 +1053,14 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
     // Fixed-order cross-warp sum over the warps that walked the record, then the record's 9 SlotAcc
     // terms: one instance partial per splat of the batch (a thread per record).
     for (int jj = threadIdx.x; jj < nb; jj += kBwdThreads) {
-      float u[10];
+      float u[kNv];
 #pragma unroll
-      for (int i = 0; i < 10; ++i) u[i] = 0.0f;
+      for (int i = 0; i < kNv; ++i) u[i] = 0.0f;
 #pragma unroll
       for (int q = 0; q < kBwdWarps; ++q)
         if ((wmask[q][jj >> 6] >> (jj & 63)) & 1ull)
 #pragma unroll
-          for (int i = 0; i < 10; ++i) u[i] += red[jj][q][i];
+          for (int i = 0; i < kNv; ++i) u[i] += red[jj][q][i];
       float o[9];
       sweep_combine(sh[jj], shk[jj], u, o);
       float* dst = partials + (int64_t)sinst[jj] * 9;

@@ -9,6 +9,7 @@
 //   tolerance: rasterize_backward rows + mean2d, rel(a,b) = |a-b|/max(1,|a|,|b|) <= 1e-4
 //              (acceptance.cpp:44; the reference's own gradient tolerance)
 #include <gss/adam.hpp>
+#include <gss/engine.hpp>
 #include <gss/render.hpp>
 #include <gss/rng.hpp>
 #include <gss/synth.hpp>
@@ -156,6 +157,31 @@ void test_raster() {
     std::printf("  backward rel dev: rows %.3e, mean2d %.3e\n", dr, dm);
     expect(g_ref.ids == g_dev.ids && dr <= 1e-4 && dm <= 1e-4, "rasterize_backward rows, mean2d within 1e-4");
   }
+  {  // the reference-signature free functions: the caller's code is unchanged but for the namespace
+    const auto& cam = scene.cameras[2];
+    const gss::Viewport<float> vp{7.0f, 50.5f, 3.0f, 40.0f};
+    const auto ids = gss::frustum_cull<float>(rows.geo_view(), cfg.n, cam, vp);
+    gss::RenderScene<float> sc;
+    sc.ids = std::span<const int>(ids);
+    sc.geo = rows.geo_view();
+    sc.nongeo = rows.nongeo_view();
+    const auto rr = gss::rasterize_forward(sc, cam, vp, 2);
+    const auto rd = gss_b200::rasterize_forward(sc, cam, vp, 2);
+    expect(rd.aux.px0 == rr.aux.px0 && rd.aux.py0 == rr.aux.py0 && same_bits(rd.image.data, rr.image.data),
+           "gss_b200::rasterize_forward (sub-viewport) image + window bit-exact");
+    gss::Image<float> gt_win(rr.image.width, rr.image.height), d_ref, d_dev;
+    for (int y = 0; y < gt_win.height; ++y)
+      for (int x = 0; x < gt_win.width; ++x)
+        for (int c = 0; c < 3; ++c) gt_win.at(y, x, c) = scene.gt_images[2].at(y + rr.aux.py0, x + rr.aux.px0, c);
+    const size_t full = size_t(cam.width) * cam.height * 3;
+    const float l_ref = gss::compute_loss_l1(rr.image, gt_win, d_ref, full);
+    const float l_dev = gss_b200::compute_loss_l1(rd.image, gt_win, d_dev, full);
+    const auto g_ref = gss::rasterize_backward(sc, cam, rr, d_ref, 2);
+    const auto g_dev = gss_b200::rasterize_backward(sc, cam, rd, d_dev, 2);
+    expect(l_ref == l_dev && g_ref.ids == g_dev.ids && rel_max(g_ref.rows, g_dev.rows) <= 1e-4 &&
+               rel_max(g_ref.mean2d, g_dev.mean2d) <= 1e-4,
+           "gss_b200::rasterize_backward (RenderResult) within 1e-4");
+  }
   bool threw = false;
   gss::Image<float> a(4, 4), b(5, 4), d;
   try {
@@ -164,6 +190,52 @@ void test_raster() {
     threw = true;
   }
   expect(threw, "shape mismatch -> std::invalid_argument");
+}
+
+// gss::OffloadEngine vs gss_b200::OffloadEngine: identical constructor arguments (EngineConfig,
+// SplitTable), run() results and snapshot within the per-step tolerance, identical valid counts.
+void test_engine() {
+  gss::SynthConfig cfg;
+  cfg.n = 600;
+  cfg.cams = 5;
+  cfg.width = 40;
+  cfg.height = 32;
+  cfg.seed = 21;
+  const auto scene = gss::synth_scene<float>(cfg);
+  gss::GaussianSet<float> start = scene.truth;
+  for (int i = 0; i < start.count; ++i) {
+    start.opacity[i] = float(std::log(0.1 / 0.9));
+    for (int k = 3; k < gss::kShScalars; ++k) start.sh[i * gss::kShScalars + k] = 0.0f;
+  }
+  gss::EngineConfig<float> ec;
+  ec.pipelined = true;
+  ec.workers = 4;
+  gss::SplitTable st;
+  st.cameras.resize(cfg.cams);
+  st.cameras[1].split = true;
+  st.cameras[1].column = 17;
+  st.cameras[3].split = true;
+  st.cameras[3].column = 30;
+  gss::OffloadEngine<float> ref(start, scene.cameras, scene.gt_images, ec, st);
+  gss_b200::OffloadEngine dev(start, scene.cameras, scene.gt_images, ec, st);
+  const auto r1 = ref.run(12);
+  const auto r2 = dev.run(12);
+  bool same_valid = r1.size() == r2.size();
+  double ldev = 0.0;
+  for (size_t i = 0; i < r1.size() && same_valid; ++i) {
+    same_valid = r1[i].valid_count == r2[i].valid_count;
+    ldev = std::max(ldev, std::abs(double(r1[i].loss) - r2[i].loss) / std::max(1.0, std::abs(double(r1[i].loss))));
+  }
+  std::printf("  engine loss dev %.3e\n", ldev);
+  expect(same_valid && r1[0].loss == r2[0].loss && ldev <= 1e-4,
+         "gss_b200::OffloadEngine (split table) run(): valid counts, first loss bit-exact, losses within 1e-4");
+  const auto s1 = ref.snapshot(), s2 = dev.snapshot();
+  const double sdev = std::max(rel_max(s1.mean, s2.mean), rel_max(s1.sh, s2.sh));
+  expect(s1.count == s2.count && sdev <= 1e-4, "gss_b200::OffloadEngine snapshot within 1e-4");
+  expect(ref.accum_grad_count() == dev.accum_grad_count(), "accum_grad_count identical");
+  dev.enable_timeline(true);
+  dev.run(2);
+  expect(dev.timeline().size() == 12, "timeline: 6 stages x 2 iterations");
 }
 
 }  // namespace
@@ -176,6 +248,7 @@ int main() {
   test_cull();
   test_adam();
   test_raster();
+  test_engine();
   std::printf("%d failed\n", g_fail);
   return g_fail;
 }

@@ -217,10 +217,10 @@ def test_engine_layout_interleaved_aligned_grads_bitwise(ref, defer_max):
 
 
 @pytest.mark.parametrize("defer_max", [1, 15])
-def test_host_tier_arena_staged_passes_bitwise(ref, defer_max):
-    """The pinned host tier (store.hpp:149-192): deferred passes and the forwarding gather run
-    through HBM staging in chunks (two alternating streams), bit-identical to the reference; a
-    small chunk size forces several chunks per pass."""
+def test_host_tier_arena_passes_bitwise(ref, defer_max):
+    """The pinned host tier (store.hpp:149-192): deferred passes, flush and the forwarding gather
+    over host-resident rows (in place through the mapping; GSS_HOST_STAGING=1 stages them through
+    HBM in chunks — a subprocess run below), bit-identical to the reference."""
     rng = np.random.default_rng(77 + defer_max)
     n, dim = 6000, 49
     ra = O.RefArena(n, dim, GROUPS49, defer_max)
@@ -255,3 +255,17 @@ def test_host_tier_arena_staged_passes_bitwise(ref, defer_max):
         assert_same(ra, ga)
     finally:
         G.set_host_chunk_bytes(32 << 20)
+
+
+def test_host_tier_staged_variant_bitwise():
+    """The opt-in staged host-tier passes (GSS_HOST_STAGING=1: chunked gather -> device pass ->
+    scatter on two streams) give the same bits as the reference (the test above in a subprocess)."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, GSS_HOST_STAGING="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        f"{__file__}::test_host_tier_arena_passes_bitwise"], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
