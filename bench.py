@@ -348,7 +348,7 @@ def run_ours(a, rank, world):
         torch.cuda.empty_cache()
         vis = float(np.mean(hvalid))
         touched = vis + (a.n - vis) / 16.0  # deferred update: grads + saturated counters (defer_max 15)
-        link_bytes = vis * (3 * 196 + 1) + touched * 2 * 3 * 196
+        link_bytes = vis * 3 * 196 + touched * 2 * 3 * 196  # counters stay in HBM
         host = {"value": h_steps / (hms / 1e3), "unit": "iters/s", "steps": h_steps, "warmup": h_warm,
                 "ms_per_step": hms / h_steps, "stage_ms_per_step": {k: v / h_steps for k, v in hstage.items()},
                 "clocks": hclocks, "link_bytes_per_step_est": link_bytes,
@@ -357,6 +357,14 @@ def run_ours(a, rank, world):
     # --- isolated HBM-bound kernels on the trained state (culled/s; Adam GB/s) ---
     kern = [] if a.no_probe else kernel_probe(G, truth, cams, dev, a)
     link = link_probe(dev) if world == 1 else None
+    if host is not None and link is not None:
+        # link roofline of the host tier: the link bytes a step moves (forwarding gather reads the
+        # visible rows' w/m/v + counters, the lazy pass reads and writes every touched row) over the
+        # step time, against the measured copy peak of both directions (full duplex)
+        ach = host["link_bytes_per_step_est"] / (host["ms_per_step"] / 1e3) / 1e9
+        peak = link["h2d_gbs"] + link["d2h_gbs"]
+        host["link_roofline"] = {"bound": "host link", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                                 "peak_source": "bench link probe: pinned cudaMemcpyAsync h2d + d2h (1 GiB, best of 3)"}
 
     vis = np.asarray(valid, np.float64)
     hbm, src = peaks()

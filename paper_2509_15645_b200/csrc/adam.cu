@@ -732,7 +732,7 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_RESTORE_MINB) restore_kernel(
     const int j = warp * 32 + lane;
     const int32_t my_id = j < nk ? cid[j] : -1;
     const int32_t my_del = j < nk ? cdel[j] : 0;
-    const int32_t my_slot = (j < nk && has_pending) ? cslot[j] : -1;
+    const int32_t my_slot = (j < nk && has_pending && pend.ids) ? cslot[j] : -1;  // empty pending set: no slots
     if (vec && warp * 32 < nk) {
       // 16-byte units of 4 columns (see walk4_kernel): row-interleaved arenas
       const int nq = (dim + 3) >> 2;

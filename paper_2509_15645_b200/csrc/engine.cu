@@ -283,6 +283,7 @@ void ensure_rows(gss_engine* e, int64_t V) {
   // forward_params(g) and lazy(g-1)): grow them preserving their contents.
   auto grow = [&](float*& buf, int width) {
     float* nb = dmalloc<float>((size_t)cap * width);
+    GSS_CUDA(cudaMemset(nb, 0, (size_t)cap * width * sizeof(float)));  // the copied tail is defined too
     if (buf) {
       GSS_CUDA(cudaMemcpy(nb, buf, (size_t)e->cap_rows * width * sizeof(float), cudaMemcpyDeviceToDevice));
       cudaFree(buf);

@@ -63,6 +63,16 @@ def window_of(vp: GssViewport) -> Tuple[int, int, int, int]:
     return px0, py0, pw, ph
 
 
+def loss_from_sums_dev(parts: torch.Tensor, normalizer: int) -> torch.Tensor:
+    """loss_from_sums on the device (no host round trip): the fp64 strip sums added in strip order,
+    cast once, times (float)(1 / normalizer) — the same arithmetic, a float32 scalar tensor."""
+    tot = parts[0]
+    for k in range(1, int(parts.shape[0])):
+        tot = tot + parts[k]
+    inv = torch.tensor(float(np.float32(1.0) / np.float32(float(normalizer))), dtype=torch.float32, device=parts.device)
+    return tot.to(torch.float32) * inv
+
+
 def loss_from_sums(sums_f64: Sequence[float], normalizer: int) -> float:
     """(float)(sum of the strips' fp64 sums, in strip order) * (1 / (float)normalizer), the device
     loss_final arithmetic (render.hpp:510)."""
@@ -162,26 +172,38 @@ class TorchExchange:
         return out.to(send.device), recv_counts
 
     def allgather_f64(self, x: torch.Tensor) -> List[float]:
+        return [float(v) for v in self.allgather_f64_dev(x).cpu().tolist()]
+
+    def allgather_f64_dev(self, x: torch.Tensor) -> torch.Tensor:
+        """[world] fp64 tensor on x's device (rank order); no host round trip with NCCL."""
         t = x.reshape(1).to(torch.float64)
         t = t if self.device_native else t.cpu()
         parts = [torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(parts, t, group=self.group)
-        return [float(p.item()) for p in parts]
+        return torch.cat(parts).to(x.device)
 
 
 def render_step(ex: TorchExchange, scene: G.RenderScene, cam, vp: GssViewport, gt: Optional[torch.Tensor],
-                background=(0.0, 0.0, 0.0), normalizer: int = 0):
+                background=(0.0, 0.0, 0.0), normalizer: int = 0, bounds: Optional[Sequence[int]] = None,
+                device_loss: bool = False):
     """One view, image-parallel over the exchange group: returns (loss, GradBuffer of this shard,
-    strip image, info). Rank k owns strip k of `vp`."""
+    strip image, info). Rank k owns strip k of `vp` (column bounds: `bounds`, e.g. the balanced
+    ones of balanced_bounds, else equal whole-tile strips). device_loss: the loss stays a device
+    float32 scalar (no host round trip)."""
     px0, py0, pw, ph = window_of(vp)
-    bounds = strip_bounds(px0, pw, ex.world)
+    bounds = list(bounds) if bounds is not None else strip_bounds(px0, pw, ex.world)
+    if len(bounds) != ex.world + 1 or bounds[0] != px0 or bounds[-1] != px0 + pw:
+        raise ValueError("render_step: bounds must be world + 1 column cuts spanning the window")
     norm = normalizer if normalizer > 0 else pw * ph * 3
     st, send, scounts = owner_project(scene, cam, vp, bounds)
     recv, rcounts = ex.alltoallv(send, scounts)
     fw = strip_forward(recv, cam, strip_viewport(vp, bounds, ex.rank), background, gt, norm)
     loss = None
     if gt is not None:
-        loss = loss_from_sums(ex.allgather_f64(fw.loss_sum), norm)
+        if device_loss:
+            loss = loss_from_sums_dev(ex.allgather_f64_dev(fw.loss_sum), norm)
+        else:
+            loss = loss_from_sums(ex.allgather_f64(fw.loss_sum), norm)
     part = strip_backward(fw, fw.d_img) if gt is not None else None
     gb = None
     if part is not None:
@@ -234,6 +256,26 @@ class SelfExchange:
     def allgather_f64(self, x):
         return [float(x.reshape(-1)[0].item())]
 
+    def allgather_f64_dev(self, x):
+        return x.reshape(1).to(torch.float64)
+
+
+def balanced_bounds(ex, geo: torch.Tensor, n: int, cam, vp: GssViewport, align: int = 16) -> List[int]:
+    """Column strips balanced by visible Gaussians over all shards (evalsplit.balanced_strip_bounds,
+    the reference's split search generalised to N strips, splitter.hpp:31-81): each evaluation is
+    an exact device cull of this shard for viewport [px0, c), summed over the exchange group."""
+    from . import evalsplit as ES
+
+    px0, py0, pw, ph = window_of(vp)
+
+    def count_upto(c):
+        sub = GssViewport(vp.x0, float(c), vp.y0, vp.y1)
+        local = torch.tensor([float(G.frustum_cull(geo, n, cam, sub).numel())], dtype=torch.float64,
+                             device=geo.device)
+        return int(round(sum(ex.allgather_f64(local))))
+
+    return ES.balanced_strip_bounds(count_upto, px0, pw, ex.world, align)
+
 
 class ShardTrainer:
     """One rank of sharded training: this rank's contiguous id shard of the scene
@@ -250,8 +292,14 @@ class ShardTrainer:
 
     def __init__(self, init_rows: np.ndarray, cams, gts, ex=None, optim: Optional[G.OptimConfig] = None, *,
                  sh_degree: int = 3, sh_warmup_step: int = 0, background=(0.0, 0.0, 0.0), device=None,
-                 pipelined: bool = False):
+                 pipelined: bool = False, balance: bool = False, device_loss: bool = False):
+        """balance: per-camera strips balanced by visible Gaussians (balanced_bounds, computed on
+        the camera's first use) instead of equal column strips. device_loss: step() returns the
+        loss as a device float32 scalar (no per-step host round trip for it)."""
         self.ex = ex or SelfExchange()
+        self.balance = bool(balance)
+        self.device_loss = bool(device_loss)
+        self.bounds = {}
         self.pipelined = bool(pipelined)
         self.sH = torch.cuda.Stream() if self.pipelined else None
         self.opt = optim or G.OptimConfig()
@@ -271,6 +319,10 @@ class ShardTrainer:
         self.g = 0
         self.pending: Optional[G.SparseGrads] = None
         self.last_info = {}
+        # densification statistics of this shard (engine.hpp:404-408: accum_norm += |dL/dmean2d|,
+        # accum_cnt += 1 per visible Gaussian per iteration), as the engine's handoff stage keeps them
+        self.accum_norm = torch.zeros(max(self.n, 1), dtype=torch.float64, device=dev)[: self.n]
+        self.accum_cnt = torch.zeros(max(self.n, 1), dtype=torch.int32, device=dev)[: self.n]
 
     def step(self, cam=None, gt: Optional[torch.Tensor] = None) -> float:
         g = self.g
@@ -299,10 +351,23 @@ class ShardTrainer:
         deg = min(self.sh_degree, g // self.sh_warmup_step) if self.sh_warmup_step > 0 else self.sh_degree
         sc = G.RenderScene(ids=ids, geo=self.geo.w, nongeo=fwd, nongeo_compact=True, sh_degree=deg,
                            background=self.background)
-        loss, gb, _, info = render_step(self.ex, sc, cam, vp, gt, self.background)  # render(g)
+        bounds = None
+        if self.balance:
+            ci = g % len(self.cams) if cam is self.cams[g % len(self.cams)] else None
+            key = ci if ci is not None else id(cam)
+            if key not in self.bounds:
+                self.bounds[key] = balanced_bounds(self.ex, self.geo.w, self.n, cam, vp)
+            bounds = self.bounds[key]
+        loss, gb, _, info = render_step(self.ex, sc, cam, vp, gt, self.background, bounds=bounds,
+                                        device_loss=self.device_loss)  # render(g)
         G.deferred_update(self.geo, G.SparseGrads(ids, gb.rows, G.K_PARAM_DIM, 0), want_touched=False,
                           check_invariants=False)                              # geo_update(g)
         self.pending = G.SparseGrads(ids, gb.rows, G.K_PARAM_DIM, G.K_GEO_DIM)  # handoff(g)
+        if ids.numel():  # densification statistics (engine.hpp:404-408), fp64, ids unique
+            m = gb.mean2d.reshape(-1, 2).double()
+            idl = ids.long()
+            self.accum_norm.index_add_(0, idl, torch.sqrt(m[:, 0] * m[:, 0] + m[:, 1] * m[:, 1]))
+            self.accum_cnt.index_add_(0, idl, torch.ones_like(ids))
         self.last_info = dict(info, visible=int(ids.numel()))
         self.g += 1
         return loss

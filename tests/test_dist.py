@@ -158,3 +158,8 @@ def test_strip_bounds_and_loss_arithmetic():
     s = [1234.5678901234, 0.0009876, 77.125]
     want = np.float32(sum(s)) * (np.float32(1.0) / np.float32(6220800.0))
     assert IP.loss_from_sums(s, 6220800) == float(want)
+    # the same arithmetic on tensors (device path, no host round trip): identical float32
+    import torch
+    for parts in (s, [3.0], [1e-3, 2e-3, 5.5, 1e9, 7.0, 0.25, 0.5, 0.125]):
+        got = IP.loss_from_sums_dev(torch.tensor(parts, dtype=torch.float64), 6220800)
+        assert got.dtype == torch.float32 and float(got) == IP.loss_from_sums(parts, 6220800)

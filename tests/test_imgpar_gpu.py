@@ -208,7 +208,25 @@ def test_shard_trainer_world1_equals_engine(pipelined):
     assert np.array_equal(tr.state()["ng_counter"].cpu().numpy(), st["ng_counter"])
 
 
-def _train_worker(rank, world, port, q):
+def test_shard_trainer_densify_stats_and_device_loss_equal_engine():
+    """The shard keeps the engine's densification statistics (engine.hpp:404-408) bit for bit, and
+    device_loss=True returns the same loss as a device scalar (no per-step host round trip)."""
+    rows, cams, gts = scene(13, 4000, 80, 64)
+    tr = IP.ShardTrainer(rows, cams, gts, device_loss=True, balance=True)
+    losses = [tr.step() for _ in range(6)]
+    assert all(isinstance(x, torch.Tensor) and x.is_cuda for x in losses)
+    tr.drain()
+    torch.cuda.synchronize()
+    eng = G.OffloadEngine(rows, cams, np.stack([g.cpu().numpy() for g in gts]), pipelined=False)
+    el, _ = eng.run(6)
+    norm, cnt = eng.accum()
+    eng.close()
+    assert np.array_equal(np.float32([float(x) for x in losses]), el)
+    assert np.array_equal(tr.accum_cnt.cpu().numpy(), cnt)
+    assert np.array_equal(tr.accum_norm.cpu().numpy().view(np.uint64), np.asarray(norm).view(np.uint64))
+
+
+def _train_worker(rank, world, port, q, balance=False):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
@@ -217,7 +235,7 @@ def _train_worker(rank, world, port, q):
         torch.cuda.set_device(0)
         rows, cams, gts = scene(13, 4000, 80, 64)
         lo, hi = D.id_range(rows.shape[0], rank, world)
-        tr = IP.ShardTrainer(rows[lo:hi], cams, gts, IP.TorchExchange())
+        tr = IP.ShardTrainer(rows[lo:hi], cams, gts, IP.TorchExchange(), balance=balance)
         losses = [tr.step() for _ in range(5)]
         tr.drain()
         torch.cuda.synchronize()
@@ -226,14 +244,16 @@ def _train_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_process_training_matches_single_shard():
+@pytest.mark.parametrize("balance", [False, True])
+def test_two_process_training_matches_single_shard(balance):
+    """Two shards over gloo (equal strips, or strips balanced by visible Gaussians) train like one."""
     import torch.multiprocessing as mp
 
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_train_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_train_worker, args=(r, world, port, q, balance)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
