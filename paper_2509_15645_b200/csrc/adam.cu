@@ -357,7 +357,10 @@ __global__ void __launch_bounds__(kUpdThreads) dense_update_kernel(ArenaDev a, G
   float4* M = reinterpret_cast<float4*>(a.m + e0);
   float4* V = reinterpret_cast<float4*>(a.v + e0);
   const int nq = ne >> 2;
-  constexpr int kU = 2;
+#ifndef GSS_DENSE_KU
+#define GSS_DENSE_KU 1  // 0.77 vs 0.74 of HBM for 2 (tools/adam_probe.py)
+#endif
+  constexpr int kU = GSS_DENSE_KU;
   auto elem = [&](float& w, float& m, float& v, float gv, int col) {
     const float4 A = cA[col], B = cB[col];
     const float m_new = A.x * m + A.z * gv;
@@ -541,13 +544,13 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_WALK_MINB) walk_kernel(ArenaD
 // arithmetic and shuffles of the scalar walk are amortised over 4 columns. Columns dim..4*nq-1 of
 // the last unit are row padding (never read back as data).
 #ifndef GSS_WALK4_KU
-#define GSS_WALK4_KU 2
+#define GSS_WALK4_KU 1  // 1 unit per lane + 4 blocks/SM: 0.64 vs 0.56 of HBM for 2 + 3 (tools/adam_probe.py)
 #endif
 #ifndef GSS_WALK_GRID
 #define GSS_WALK_GRID 8  // walk blocks per SM (grid-stride over the touch list)
 #endif
 #ifndef GSS_WALK4_MINB
-#define GSS_WALK4_MINB 3
+#define GSS_WALK4_MINB 4
 #endif
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
@@ -658,10 +661,10 @@ bool vector_rows(const gss_arena& a) {
 // flattened (id, column) walk reads the arena rows with consecutive lanes on consecutive columns.
 constexpr int kRestoreChunk = kUpdThreads;
 #ifndef GSS_RESTORE_MINB
-#define GSS_RESTORE_MINB 3
+#define GSS_RESTORE_MINB 4
 #endif
 #ifndef GSS_RESTORE_KV
-#define GSS_RESTORE_KV 2
+#define GSS_RESTORE_KV 1  // with 4 blocks/SM: 0.57 vs 0.53 of HBM (tools/adam_probe.py)
 #endif
 constexpr int kSeg = 2048;
 template <int K>

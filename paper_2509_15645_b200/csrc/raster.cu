@@ -50,6 +50,9 @@ constexpr int kFwdBlockRows = 4 * kFwdPPT;
 #ifndef GSS_FWD_MINB
 #define GSS_FWD_MINB 0
 #endif
+#ifndef GSS_BWD_ROWSKIP
+#define GSS_BWD_ROWSKIP 0
+#endif
 #ifndef GSS_BWD_MINB
 #define GSS_BWD_MINB 10  // 10 sweep CTAs per SM (96 registers, no spill): measured best
 #endif
@@ -136,6 +139,7 @@ struct gss_render_ctx {
   gssd::SceneDev sc{};
   gssd::Cam cam{};
   int64_t V = 0, I = 0;
+  const uint64_t* pay_sorted = nullptr;  // depth-ordered sort payloads of the last binning (slot + box)
   int have_forward = 0;
   int64_t* pinned = nullptr;  // host-visible counts
   cudaStream_t last_stream = nullptr;
@@ -163,9 +167,10 @@ __device__ __forceinline__ const float* ng_row(const SceneDev& s, int k, int id)
 
 // project_all (render.hpp:361-380) + CSR box (render.hpp:297-314, 418-419) + tile count.
 // Opacity and view-dependent colour of slot k (render.hpp:372-378, sh.hpp:77-86).
-__device__ __forceinline__ void splat_colour(const SceneDev& s, const Cam& cam, int k, int id, const float* g,
-                                             SplatRec& r) {
-  const float* ng = ng_row(s, k, id);
+// DEG >= 0: the SH degree known at compile time (the basis stays in registers); -1: s.sh_degree.
+template <int DEG = -1>
+__device__ __forceinline__ void splat_colour_row(const SceneDev& s, const Cam& cam, const float* ng, const float* g,
+                                                 SplatRec& r) {
   r.ab = 1.0f / (1.0f + gss_expf(-ng[0]));
   const f3 cp = cam_position(cam);
   f3 dir{g[0] - cp.x, g[1] - cp.y, g[2] - cp.z};
@@ -177,8 +182,9 @@ __device__ __forceinline__ void splat_colour(const SceneDev& s, const Cam& cam, 
     dir = f3{0.0f, 0.0f, 1.0f};
   }
   float basis[16];
-  sh_basis(dir.x, dir.y, dir.z, s.sh_degree, basis);
-  const int nb = (s.sh_degree + 1) * (s.sh_degree + 1);
+  const int deg = DEG >= 0 ? DEG : s.sh_degree;
+  sh_basis(dir.x, dir.y, dir.z, deg, basis);
+  const int nb = (deg + 1) * (deg + 1);
   float rgb0 = 0.5f, rgb1 = 0.5f, rgb2 = 0.5f;
   for (int b = 0; b < nb; ++b) {
     rgb0 += basis[b] * ng[1 + 3 * b];
@@ -189,13 +195,47 @@ __device__ __forceinline__ void splat_colour(const SceneDev& s, const Cam& cam, 
   r.g = clamp01(rgb1);
   r.bl = clamp01(rgb2);
 }
+__device__ __forceinline__ void splat_colour(const SceneDev& s, const Cam& cam, int k, int id, const float* g,
+                                             SplatRec& r) {
+  splat_colour_row(s, cam, ng_row(s, k, id), g, r);
+}
+
+// Stages the non-geometric rows of a warp's 32 consecutive slots (nf floats each) into SMEM rows of
+// pitch `pitch` (odd: lane-strided row access is conflict-free): consecutive lanes copy consecutive
+// floats of a row (coalesced), every element in flight at once through LDGSTS (no register
+// round trip), then the warp waits for its copies.
+template <int PITCH>
+__device__ __forceinline__ void stage_rows(const SceneDev& s, int64_t k0, int nk, int nf, int lane,
+                                           float (*rows)[PITCH]) {
+  const float* my_row = lane < nk ? ng_row(s, (int)(k0 + lane), s.ids[k0 + lane]) : s.nongeo;
+  for (int e = lane; e < 32 * nf; e += 32) {
+    const int kk = e / nf, c = e - kk * nf;
+    const float* rp = (const float*)__shfl_sync(0xffffffffu, (unsigned long long)my_row, kk);
+    if (kk < nk) cp_async4(&rows[kk][c], rp + c);
+  }
+  cp_async_wait_all();
+  __syncwarp();
+}
+
+// Depth-sort payload: slot k in the low 32 bits, the splat's tile box (tx0, ty0, ntx, nty, a byte
+// each) in the high 32 bits when it fits (windows up to 255 x 255 tiles: 4080 px), else the
+// kNoBox sentinel. Binning then reads the depth-ordered payload sequentially instead of gathering
+// each slot's record and tile count at random.
+constexpr uint32_t kNoBox = 0xffffffffu;
+__device__ __forceinline__ uint64_t pack_payload(int64_t k, int nt, int tx0, int ty0, int ntx, int nty) {
+  uint32_t hi = 0;  // nt == 0: an empty box
+  if (nt > 0) hi = (tx0 < 256 && ty0 < 256 && ntx < 256 && nty < 256)
+                       ? (uint32_t)tx0 | ((uint32_t)ty0 << 8) | ((uint32_t)ntx << 16) | ((uint32_t)nty << 24)
+                       : kNoBox;
+  return ((uint64_t)hi << 32) | (uint32_t)k;
+}
 
 // project_all (render.hpp:361-380) + CSR box (render.hpp:297-314, 418-419) + tile count. With
 // COLOUR = false only the geometry is produced (opacity/colour zero) — colour_kernel fills it in
 // once the non-geometric rows are available, so binning can run while they are gathered.
 template <bool COLOUR>
 __global__ void preprocess_kernel(SceneDev s, Cam cam, Win w, int64_t V, SplatRec* recs, int32_t* ntiles,
-                                  uint32_t* dkey, int32_t* dslot) {
+                                  uint32_t* dkey, uint64_t* dpay) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= V) return;
   const int id = s.ids[k];
@@ -204,7 +244,7 @@ __global__ void preprocess_kernel(SceneDev s, Cam cam, Win w, int64_t V, SplatRe
   f3 t;
   SplatRec r;
   memset(&r, 0, sizeof(r));
-  int nt = 0;
+  int nt = 0, ptx0 = 0, pty0 = 0, pntx = 0, pnty = 0;
   if (project_geo(cam, g, s.lp, p, t)) {
     if (COLOUR) splat_colour(s, cam, (int)k, id, g, r);
     r.mx = p.mx; r.my = p.my; r.a = p.a; r.b = p.b; r.c = p.c;
@@ -223,6 +263,7 @@ __global__ void preprocess_kernel(SceneDev s, Cam cam, Win w, int64_t V, SplatRe
         const int tx0 = (bx0 - w.px0) / kTileSize, tx1 = (bx1 - 1 - w.px0) / kTileSize;
         const int ty0 = (by0 - w.py0) / kTileSize, ty1 = (by1 - 1 - w.py0) / kTileSize;
         nt = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+        ptx0 = tx0; pty0 = ty0; pntx = tx1 - tx0 + 1; pnty = ty1 - ty0 + 1;
       }
     }
   }
@@ -232,17 +273,32 @@ __global__ void preprocess_kernel(SceneDev s, Cam cam, Win w, int64_t V, SplatRe
   ntiles[k] = nt;
   // Depth sort key: binned splats have depth >= near > 0, whose IEEE bits order like the values.
   dkey[k] = nt > 0 ? __float_as_uint(r.depth) : 0xffffffffu;
-  dslot[k] = (int32_t)k;
+  dpay[k] = pack_payload(k, nt, ptx0, pty0, pntx, pnty);
 }
 
 // The colour half of preprocess for the binned splats (ntiles > 0: the only records compositing
 // and the sweep read; a valid unbinned slot's opacity only meets zero gradient sums in the chain).
-__global__ void colour_kernel(SceneDev s, Cam cam, int64_t V, const int32_t* ntiles, SplatRec* recs) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= V || ntiles[k] == 0) return;
+// Warp-cooperative: a warp owns 32 consecutive slots, stages the row floats the SH degree reads
+// (1 + 3 (deg+1)^2) into SMEM (stage_rows) and each lane evaluates its slot from SMEM — instead of
+// every lane streaming its own 196-byte row.
+constexpr int kColThreads = 128;
+constexpr int kColRow = 49;  // odd pitch
+template <int DEG>
+__global__ void __launch_bounds__(kColThreads) colour_kernel(SceneDev s, Cam cam, int64_t V, const int32_t* ntiles,
+                                                              SplatRec* recs) {
+  __shared__ float row_s[kColThreads / 32][32][kColRow];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t k0 = (int64_t)blockIdx.x * kColThreads + warp * 32;
+  if (k0 >= V) return;
+  const int nk = (V - k0) < 32 ? (int)(V - k0) : 32;
+  const int64_t k = k0 + lane;
+  const bool mine = lane < nk && ntiles[k] > 0;
+  if (!__any_sync(0xffffffffu, mine)) return;
+  stage_rows<kColRow>(s, k0, nk, 1 + 3 * (DEG + 1) * (DEG + 1), lane, row_s[warp]);
+  if (!mine) return;
   const int id = s.ids[k];
   SplatRec r;
-  splat_colour(s, cam, (int)k, id, s.geo + (int64_t)id * s.geo_stride, r);
+  splat_colour_row<DEG>(s, cam, row_s[warp][lane], s.geo + (int64_t)id * s.geo_stride, r);
   recs[k].ab = r.ab;
   recs[k].r = r.r;
   recs[k].g = r.g;
@@ -253,11 +309,11 @@ __global__ void colour_kernel(SceneDev s, Cam cam, int64_t V, const int32_t* nti
 // re-clipped to this window w (an image strip): the reference box of a splat is the same for
 // every window, only its clip differs, so per-pixel contribution lists are unchanged.
 __global__ void clip_kernel(const SplatRec* in, int64_t V, Win w, SplatRec* recs, int32_t* ntiles, uint32_t* dkey,
-                            int32_t* dslot) {
+                            uint64_t* dpay) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= V) return;
   SplatRec r = in[k];
-  int nt = 0;
+  int nt = 0, ptx0 = 0, pty0 = 0, pntx = 0, pnty = 0;
   if (r.bx1 > r.bx0 && r.by1 > r.by0) {
     const int wx1 = w.px0 + w.pw, wy1 = w.py0 + w.ph;
     r.bx0 = max(w.px0, r.bx0); r.bx1 = min(wx1, r.bx1);
@@ -266,13 +322,14 @@ __global__ void clip_kernel(const SplatRec* in, int64_t V, Win w, SplatRec* recs
       const int tx0 = (r.bx0 - w.px0) / kTileSize, tx1 = (r.bx1 - 1 - w.px0) / kTileSize;
       const int ty0 = (r.by0 - w.py0) / kTileSize, ty1 = (r.by1 - 1 - w.py0) / kTileSize;
       nt = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+      ptx0 = tx0; pty0 = ty0; pntx = tx1 - tx0 + 1; pnty = ty1 - ty0 + 1;
     }
   }
   if (nt == 0) r.bx0 = r.bx1 = r.by0 = r.by1 = 0;
   recs[k] = r;
   ntiles[k] = nt;
   dkey[k] = nt > 0 ? __float_as_uint(r.depth) : 0xffffffffu;
-  dslot[k] = (int32_t)k;
+  dpay[k] = pack_payload(k, nt, ptx0, pty0, pntx, pnty);
 }
 
 // Image-strip routing: does record k's pixel box touch columns [x0, x1)?
@@ -312,7 +369,7 @@ __device__ __forceinline__ void tile_box(const SplatRec& r, const Win& w, int& t
 // (ties in slot = ascending id order) inside each tile, the reference's std::stable_sort order
 // (render.hpp:406-416). Instance numbering follows this order; slot_off[k] / ntiles[k] give slot
 // k's instance range for the backward's per-slot sums.
-__global__ void duplicate_kernel(const SplatRec* recs, const int32_t* order, const int32_t* ntiles,
+__global__ void duplicate_kernel(const SplatRec* recs, const uint64_t* pay, const int32_t* ntiles,
                                  const int32_t* offsets, Win w, int64_t V, uint32_t* keys, int32_t* vals,
                                  SplatRec* recs_rw, int32_t* slot_off) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -322,12 +379,23 @@ __global__ void duplicate_kernel(const SplatRec* recs, const int32_t* order, con
   int32_t k = 0, off = 0, nt = 0;
   int tx0 = 0, ty0 = 0, ntx = 1, nty = 0;
   if (valid) {
-    k = order[i];
+    const uint64_t p = pay[i];
+    const uint32_t hi = (uint32_t)(p >> 32);
+    k = (int32_t)(uint32_t)p;
     off = offsets[i];
     recs_rw[k].off = off;
     slot_off[k] = off;
-    nt = ntiles[k];
-    if (nt > 0) tile_box(recs[k], w, tx0, ty0, ntx, nty);
+    if (hi != kNoBox) {  // the tile box travelled with the sort
+      tx0 = (int)(hi & 0xffu);
+      ty0 = (int)((hi >> 8) & 0xffu);
+      ntx = (int)((hi >> 16) & 0xffu);
+      nty = (int)(hi >> 24);
+      nt = ntx * nty;
+      if (nt == 0) ntx = 1;
+    } else {
+      nt = ntiles[k];
+      if (nt > 0) tile_box(recs[k], w, tx0, ty0, ntx, nty);
+    }
   }
   if (nt > 0 && nt <= 4) {  // small splats: this lane writes its own keys (row-major tile order)
     int j = 0;
@@ -356,9 +424,14 @@ __global__ void duplicate_kernel(const SplatRec* recs, const int32_t* order, con
 // ntiles in sorted order (0 at position V), for the instance-offset scan: offsets[V] = I.
 struct SortedCount {
   const int32_t* nt;
-  const int32_t* order;
+  const uint64_t* pay;
   int32_t V;
-  __host__ __device__ int32_t operator()(int32_t i) const { return i < V ? nt[order[i]] : 0; }
+  __host__ __device__ int32_t operator()(int32_t i) const {
+    if (i >= V) return 0;
+    const uint64_t p = pay[i];
+    const uint32_t hi = (uint32_t)(p >> 32);
+    return hi != kNoBox ? (int32_t)(((hi >> 16) & 0xffu) * (hi >> 24)) : nt[(uint32_t)p];
+  }
 };
 
 // Tile ranges of the sorted instance keys: thread t owns keys [4t, 4t + 4) (one 16-byte load; the
@@ -1035,8 +1108,16 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
             (void)u;
           }
         } else {
+#if GSS_BWD_ROWSKIP
+          // pixel step q covers band rows 2q, 2q+1: skip the steps whose rows the box misses
+          // (warp-uniform; an idle step adds exact zeros and keeps the state, so skipping is exact)
+          const int rlo = r.by0 - by0w, rhi = r.by1 - by0w;  // box rows relative to the band
+#endif
 #pragma unroll
           for (int q = 0; q < kBwdPPT; ++q) {
+#if GSS_BWD_ROWSKIP
+            if (2 * q + 1 < rlo || 2 * q >= rhi) continue;
+#endif
             const bool u = bwd_contrib<false>(r, k, xin, bstart + jj, px[q], v);
 #if GSS_RASTER_STATS
             st_use += u ? 1 : 0;
@@ -1068,6 +1149,16 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
       for (int i = 0; i < 9; ++i) dst[i] = o[i];
     }
   }
+  // Records behind every pixel's last contribution (sweep position >= Lmax: the T-stop tail) get
+  // exact-zero partials here, so the partials buffer needs no clearing pass before the sweep.
+  for (int j = Lmax + threadIdx.x; j < rg.y - rg.x; j += kBwdThreads) {
+    const SplatRec& r = recs[vals[rg.x + j]];
+    int tx0, ty0, ntx, nty;
+    tile_box(r, w, tx0, ty0, ntx, nty);
+    float* dst = partials + (int64_t)(r.off + (ty - ty0) * ntx + (tx - tx0)) * 9;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) dst[i] = 0.0f;
+  }
 #if GSS_RASTER_STATS
   if (lane == 0) {
     atomicAdd(&g_rstats[5], st_walk);
@@ -1075,6 +1166,52 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
   }
   atomicAdd(&g_rstats[7], st_use);
 #endif
+}
+
+// Per-slot sums of the instance partials in depth order: a warp owns 32 consecutive depth
+// positions, whose instance ranges [offsets[i], offsets[i+1]) are adjacent — one contiguous span.
+// The span is staged into SMEM in chunks of kSumChunk instances with every 4-byte piece in flight
+// (LDGSTS, coalesced), and each lane adds its own slot's instances from SMEM in instance order
+// (fixed order: deterministic). The sum lands at the slot the sort payload names.
+constexpr int kSumWarps = 8;
+constexpr int kSumChunk = 128;  // instances per staged chunk (4.5 KB per warp)
+__global__ void __launch_bounds__(kSumWarps * 32) slot_sum_depth_kernel(int64_t V, const int32_t* __restrict__ offsets,
+                                                                      const uint64_t* __restrict__ pay,
+                                                                      const float* __restrict__ partials, float* sums) {
+  __shared__ float stage[kSumWarps][kSumChunk * 9];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t i0 = ((int64_t)blockIdx.x * kSumWarps + warp) * 32;
+  if (i0 >= V) return;
+  const int64_t i = i0 + lane;
+  const bool valid = i < V;
+  const int64_t iend = i0 + 32 < V ? i0 + 32 : V;
+  const int32_t o0 = valid ? offsets[i] : offsets[iend];
+  const int32_t o1 = valid ? offsets[i + 1] : o0;
+  const int32_t s0 = __shfl_sync(0xffffffffu, o0, 0);
+  const int32_t s1 = offsets[iend];
+  float acc[9];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) acc[c] = 0.0f;
+  float* st = stage[warp];
+  for (int32_t c0 = s0; c0 < s1; c0 += kSumChunk) {
+    const int n = (s1 - c0 < kSumChunk ? s1 - c0 : kSumChunk) * 9;
+    const float* src = partials + (int64_t)c0 * 9;
+    __syncwarp();
+    for (int e = lane; e < n; e += 32) cp_async4(st + e, src + e);
+    cp_async_wait_all();
+    __syncwarp();
+    const int32_t a = o0 > c0 ? o0 : c0, b = o1 < c0 + kSumChunk ? o1 : c0 + kSumChunk;
+    for (int32_t j = a; j < b; ++j) {
+      const float* q = st + (j - c0) * 9;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) acc[c] += q[c];
+    }
+  }
+  if (valid) {
+    const int64_t k = (int64_t)(uint32_t)pay[i];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) sums[k * 9 + c] = acc[c];
+  }
 }
 
 // render.hpp:600-638 + project_geo_backward (render.hpp:152-237), per slot.
@@ -1102,17 +1239,16 @@ __global__ void __launch_bounds__(kSumThreads) slot_sum_kernel(int64_t V, const 
   for (int c = 0; c < 9; ++c) acc[c] = 0.0f;
   const int32_t hend = min(o1, o0 + kHead);
   int32_t i = o0;
-  for (; i + 1 < hend; i += 2) {
-    float a0[9], a1[9];
+  for (; i + 3 < hend; i += 4) {  // 36 loads in flight, summed in instance order
+    float a[4][9];
 #pragma unroll
-    for (int c = 0; c < 9; ++c) {
-      a0[c] = partials[(int64_t)i * 9 + c];
-      a1[c] = partials[(int64_t)(i + 1) * 9 + c];
-    }
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
-    for (int c = 0; c < 9; ++c) acc[c] = (acc[c] + a0[c]) + a1[c];
+      for (int c = 0; c < 9; ++c) a[u][c] = partials[(int64_t)(i + u) * 9 + c];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) acc[c] = (((acc[c] + a[0][c]) + a[1][c]) + a[2][c]) + a[3][c];
   }
-  if (i < hend)
+  for (; i < hend; ++i)
 #pragma unroll
     for (int c = 0; c < 9; ++c) acc[c] += partials[(int64_t)i * 9 + c];
   unsigned big = __ballot_sync(0xffffffffu, o1 - o0 > kHead);
@@ -1154,7 +1290,7 @@ constexpr int kChainThreads = 128;
 #ifndef GSS_CHAIN_MINB
 #define GSS_CHAIN_MINB 6  // 6 blocks of 128 threads per SM (80 registers): the chain is latency bound
 #endif
-constexpr int kChainRow = 61;     // odd row pitch: conflict-free per-lane row access
+constexpr int kChainRow = 49;     // odd row pitch: conflict-free per-lane row access
 // Warp-cooperative: a warp owns 32 consecutive slots. It sums each slot's instance partials with
 // all lanes, stages the slots' 49-float non-geometric rows in SMEM with coalesced loads; each lane
 // then runs the reference chain for its slot, and the 59 outputs are written back through SMEM
@@ -1171,17 +1307,7 @@ __global__ void __launch_bounds__(kChainThreads, GSS_CHAIN_MINB) chain_kernel(Sc
   if (k0 >= V) return;
   const int nk = (V - k0) < 32 ? (int)(V - k0) : 32;
   float(*rows)[kChainRow] = row_s[warp];
-  {
-    // Row base pointers resolved once per lane, then 49 independent coalesced loads per lane.
-    const float* my_row = lane < nk ? ng_row(s, (int)(k0 + lane), s.ids[k0 + lane]) : s.nongeo;
-#pragma unroll 7
-    for (int e = lane; e < 32 * 49; e += 32) {
-      const int kk = e / 49, c = e - kk * 49;
-      const float* rp = (const float*)__shfl_sync(0xffffffffu, (unsigned long long)my_row, kk);
-      if (kk < nk) rows[kk][c] = rp[c];
-    }
-  }
-  __syncwarp();
+  stage_rows<kChainRow>(s, k0, nk, 49, lane, rows);
   const int64_t k = k0 + lane;
   // Geometric gradients (row columns 0..9) live in registers; the 49 non-geometric ones overwrite
   // this lane's staged non-geometric row in place (column 10 + i -> slot i, each slot read before
@@ -1451,11 +1577,12 @@ void bin_phase(gss_render_ctx* ctx, const Win& w, int64_t V, cudaStream_t st) {
   if (V > 0) {
     auto* dka = static_cast<uint32_t*>(ctx->dkeys_a.p);
     auto* dkb = static_cast<uint32_t*>(ctx->dkeys_b.get((size_t)V * 4, st));
-    auto* oa = static_cast<int32_t*>(ctx->order_a.p);
-    auto* ob = static_cast<int32_t*>(ctx->order_b.get((size_t)V * 4, st));
-    // 1. stable sort of the V splats by depth (record order breaks ties: ascending id).
+    auto* oa = static_cast<uint64_t*>(ctx->order_a.p);
+    auto* ob = static_cast<uint64_t*>(ctx->order_b.get((size_t)V * 8, st));
+    // 1. stable sort of the V splats by depth (record order breaks ties: ascending id); the payload
+    //    carries the slot and its packed tile box.
     cub::DoubleBuffer<uint32_t> ddk(dka, dkb);
-    cub::DoubleBuffer<int32_t> ddv(oa, ob);
+    cub::DoubleBuffer<uint64_t> ddv(oa, ob);
     size_t db = 0;
     GSS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, db, ddk, ddv, (int)V, 0, 32, st));
     // 2. instance offsets in depth order; offs[V] = I.
@@ -1467,7 +1594,8 @@ void bin_phase(gss_render_ctx* ctx, const Win& w, int64_t V, cudaStream_t st) {
     void* tmp = ctx->cub_tmp.get(std::max(db, tb), st);
     GSS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, db, ddk, ddv, (int)V, 0, 32, st));
     count_launch();
-    const int32_t* order = ddv.Current();
+    const uint64_t* order = ddv.Current();
+    ctx->pay_sorted = order;
     GSS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, CountIt(thrust::counting_iterator<int32_t>(0),
                                                                 SortedCount{nt, order, (int32_t)V}),
                                            offs, (int)(V + 1), st));
@@ -1570,6 +1698,7 @@ void begin_forward(gss_render_ctx* ctx, const gss_camera* cam, const Win& w, int
   ctx->win = w;
   ctx->V = V;
   ctx->I = 0;
+  ctx->pay_sorted = nullptr;
   ctx->have_forward = 1;
 }
 
@@ -1578,7 +1707,7 @@ void alloc_records(gss_render_ctx* ctx, int64_t V, cudaStream_t st) {
   ctx->recs.get(n * sizeof(SplatRec), st);
   ctx->ntiles.get((n + 1) * 4, st);
   ctx->dkeys_a.get(n * 4, st);
-  ctx->order_a.get(n * 4, st);
+  ctx->order_a.get(n * 8, st);  // depth-sort payloads (slot + packed tile box)
 }
 
 void per_slot_sums(gss_render_ctx* ctx, const float* d_img, float* sums, cudaStream_t st) {
@@ -1593,8 +1722,8 @@ void per_slot_sums(gss_render_ctx* ctx, const float* d_img, float* sums, cudaStr
   const SplatRec* recs = static_cast<const SplatRec*>(ctx->recs.p);
   const int32_t* soff = static_cast<const int32_t*>(ctx->slot_off.p);
   const int32_t* nts = static_cast<const int32_t*>(ctx->ntiles.p);
+  // every instance partial is written by the sweep (walked records, or zeros for a tile's T-stop tail)
   float* partials = static_cast<float*>(ctx->partials.get((size_t)std::max<int64_t>(I, 1) * 9 * 4, st));
-  GSS_CUDA(cudaMemsetAsync(partials, 0, (size_t)I * 9 * 4, st));
   {
     const int ntile = w.tw * w.th;
     ktime_begin(ctx, 1, st);
@@ -1606,7 +1735,17 @@ void per_slot_sums(gss_render_ctx* ctx, const float* d_img, float* sums, cudaStr
     GSS_LAUNCHED();
     ktime_end(ctx, st);
   }
-  slot_sum_kernel<<<(unsigned)ceil_div(V, kSumThreads), kSumThreads, 0, st>>>(V, soff, nts, partials, sums);
+#ifndef GSS_SUM_DEPTH
+#define GSS_SUM_DEPTH 1
+#endif
+  if (GSS_SUM_DEPTH && ctx->pay_sorted) {
+    // slots never binned (V_bin .. V in depth order: depth key 0xffffffff) have no instances: their
+    // ranges are empty and their sums are written as zeros like every other slot's
+    slot_sum_depth_kernel<<<(unsigned)ceil_div(V, kSumWarps * 32), kSumWarps * 32, 0, st>>>(
+        V, static_cast<const int32_t*>(ctx->offsets.p), ctx->pay_sorted, partials, sums);
+  } else {
+    slot_sum_kernel<<<(unsigned)ceil_div(V, kSumThreads), kSumThreads, 0, st>>>(V, soff, nts, partials, sums);
+  }
   GSS_LAUNCHED();
 }
 
@@ -1642,7 +1781,7 @@ void rasterize_forward(gss_render_ctx* ctx, const gss_render_scene* scene, const
   if (V > 0 && npix > 0) {
     preprocess_kernel<true><<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(
         ctx->sc, ctx->cam, w, V, static_cast<SplatRec*>(ctx->recs.p), static_cast<int32_t*>(ctx->ntiles.p),
-        static_cast<uint32_t*>(ctx->dkeys_a.p), static_cast<int32_t*>(ctx->order_a.p));
+        static_cast<uint32_t*>(ctx->dkeys_a.p), static_cast<uint64_t*>(ctx->order_a.p));
     GSS_LAUNCHED();
   }
   bin_and_composite(ctx, w, V, FwdOut{image, gt, cam->width, inv, d_img, loss_dev, nullptr, final_T_opt, ncontrib_opt,
@@ -1712,7 +1851,7 @@ void rasterize_forward_geometry(gss_render_ctx* ctx, const gss_render_scene* sce
   if (V > 0 && (int64_t)w.pw * w.ph > 0) {
     preprocess_kernel<false><<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(
         ctx->sc, ctx->cam, w, V, static_cast<SplatRec*>(ctx->recs.p), static_cast<int32_t*>(ctx->ntiles.p),
-        static_cast<uint32_t*>(ctx->dkeys_a.p), static_cast<int32_t*>(ctx->order_a.p));
+        static_cast<uint32_t*>(ctx->dkeys_a.p), static_cast<uint64_t*>(ctx->order_a.p));
     GSS_LAUNCHED();
   }
   bin_phase(ctx, w, V, st);
@@ -1729,7 +1868,10 @@ void rasterize_forward_finish(gss_render_ctx* ctx, float* image, const float* gt
           "compute_loss_l1: image and ground-truth shapes differ");
   const float inv = gt ? 1.0f / (float)(double)(normalizer > 0 ? normalizer : npix * 3) : 0.0f;
   if (V > 0 && npix > 0) {
-    colour_kernel<<<(unsigned)ceil_div(V, 128), 128, 0, st>>>(ctx->sc, ctx->cam, V,
+    auto ck = ctx->sc.sh_degree == 0 ? colour_kernel<0>
+              : ctx->sc.sh_degree == 1 ? colour_kernel<1>
+              : ctx->sc.sh_degree == 2 ? colour_kernel<2> : colour_kernel<3>;
+    ck<<<(unsigned)ceil_div(V, kColThreads), kColThreads, 0, st>>>(ctx->sc, ctx->cam, V,
                                                               static_cast<const int32_t*>(ctx->ntiles.p),
                                                               static_cast<SplatRec*>(ctx->recs.p));
     GSS_LAUNCHED();
@@ -1819,7 +1961,7 @@ void rasterize_records_forward(gss_render_ctx* ctx, const void* records, int64_t
     clip_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, st>>>(
         static_cast<const SplatRec*>(records), count, w, static_cast<SplatRec*>(ctx->recs.p),
         static_cast<int32_t*>(ctx->ntiles.p), static_cast<uint32_t*>(ctx->dkeys_a.p),
-        static_cast<int32_t*>(ctx->order_a.p));
+        static_cast<uint64_t*>(ctx->order_a.p));
     GSS_LAUNCHED();
   }
   bin_and_composite(ctx, w, count, FwdOut{image, gt, cam->width, inv, d_img, loss_dev, loss_sum_dev, final_T_opt,
