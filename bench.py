@@ -395,6 +395,7 @@ def run_ours(a, rank, world):
         "link": link,
         "clocks": clocks,
         "losses": [float(losses[0]), float(losses[-1])],
+        "strips": "balanced by visible Gaussians per camera (imgpar.balanced_bounds)",
     }
     return out, (hbm, src), (cams, gts, start, truth)
 
@@ -438,7 +439,9 @@ def run_imgpar(a, rank, world):
     del td, geo_t, ng_t
     torch.cuda.empty_cache()
     start = training_start(truth)
-    tr = IP.ShardTrainer(start, cams, gts, ex, pipelined=True)
+    # strips balanced by visible Gaussians over all shards; the loss stays on the device in the
+    # timed loop (the e2e loop below reads it on the host every step)
+    tr = IP.ShardTrainer(start, cams, gts, ex, pipelined=True, balance=True, device_loss=True)
     for _ in range(a.warmup):
         tr.step()
     if world > 1:
@@ -478,7 +481,7 @@ def run_imgpar(a, rank, world):
             torch.cuda.current_stream().wait_event(ready[j % 2])
             if j + 1 < n:
                 prefetch(j + 1, off + j + 1)
-            tr.step(cams[(off + j) % len(cams)], gbufs[j % 2])
+            float(tr.step(cams[(off + j) % len(cams)], gbufs[j % 2]))  # loss read on the host
 
     e2e_loop(a.warmup, 0)
     if world > 1:
@@ -498,13 +501,13 @@ def run_imgpar(a, rank, world):
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference synth_scene generator per shard, GT rendered on device)",
-        "config": {"workload": f"C2 per GPU, sharded: {world} x {a.n // 1_000_000}M Gaussians in one scene, "
+        "config": {"workload": f"sharded: {world} x {a.n / 1e6:g}M Gaussians in one scene, "
                                f"{a.width}x{a.height} views rendered image-parallel ({world} column strips), "
                                "all state in HBM, deferred Adam defer_max=15",
                    "n_gaussians_per_gpu": a.n, "n_gaussians": a.n * world, "width": a.width, "height": a.height,
                    "cams": a.cams, "parallelism": f"id-range shards x{world} + image strips, NCCL all-to-allv"
                    if world > 1 else "1 GPU (split-phase path, no exchange)",
-                   "l2": "inputs > L2 (2.8 GB optimizer state per rank), no flush",
+                   "l2": f"inputs > L2 ({a.n * 760 / 1e9:.1f} GB optimizer state per rank), no flush",
                    "mean_visible_per_gpu": vbar, "used_ratio": vbar / a.n,
                    "records_sent_per_gpu_per_step": float(np.mean(sent)),
                    "value_definition": "shard-iterations/s = N x (iterations/s of the N-shard job)"},
@@ -908,11 +911,13 @@ def main():
 # the fraction of the lane-pixel slots it issues that are useful contributions (a library built
 # with GSS_RASTER_STATS=1, tools/raster_work.py).
 RASTER_PROFILE = {
-    "sweep": {"kernel": "backward_kernel", "issue_busy": 0.847, "useful_of_offered": 0.534,
-              "source": "profiles/r02_ncu_raster_c4.txt (Issue Slots Busy), "
+    "sweep": {"kernel": "backward_kernel", "issue_busy": 0.855, "useful_of_offered": 0.534,
+              "dram_bytes_per_launch": 1.968153e9 + 1.387961e9,
+              "source": "profiles/r02_ncu_raster_c4_round2.txt (Issue Slots Busy, dram__bytes of camera 0), "
                         "profiles/r02_raster_work_c4.json (bwd_useful_of_offered)"},
     "composite": {"kernel": "forward_kernel", "issue_busy": 0.856, "useful_of_offered": 0.655,
-                  "source": "profiles/r02_ncu_raster_c4.txt (Issue Slots Busy), "
+                  "dram_bytes_per_launch": 415.150848e6 + 265.354240e6,
+                  "source": "profiles/r02_ncu_raster_c4_round2.txt (Issue Slots Busy, dram__bytes of camera 0), "
                             "profiles/r02_raster_work_c4.json (fwd_useful_of_offered)"},
 }
 
@@ -929,7 +934,10 @@ def render_roofline(out):
     ach = rk[f"{which}_contribs_per_s"]
     frac = prof["issue_busy"] * prof["useful_of_offered"]
     return {"bound": "issue", "kernel": prof["kernel"], "achieved": ach, "unit": "contribs/s",
-            "peak": ach / frac, "frac": frac, "traffic": None, "share_of_step": rk[f"{which}_share_of_step"],
+            "peak": ach / frac, "frac": frac, "traffic": prof["dram_bytes_per_launch"],
+            "traffic_note": "ncu dram__bytes_read + write of one launch (camera 0): < 5% of HBM bandwidth over "
+                            "the launch, so neither kernel is memory-bound",
+            "share_of_step": rk[f"{which}_share_of_step"],
             "bytes_or_units_per_launch": rk["contribs_per_step"],
             "frac_source": prof["source"],
             "note": "units = (pixel, splat) contributions composited per view (SURVEY.md §8a rows a8/a10); "

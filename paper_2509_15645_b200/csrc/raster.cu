@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -49,6 +50,9 @@ constexpr int kFwdBlockRows = 4 * kFwdPPT;
 // chooses the registers; the backward sweep then takes 78).
 #ifndef GSS_FWD_MINB
 #define GSS_FWD_MINB 0
+#endif
+#ifndef GSS_FWD_SAFE
+#define GSS_FWD_SAFE 0
 #endif
 #ifndef GSS_BWD_ROWSKIP
 #define GSS_BWD_ROWSKIP 0
@@ -550,6 +554,26 @@ __device__ __forceinline__ float div_rcp_rn(float n, float d, float rd) {
   return __fdiv_rn(n, d);
 }
 
+// A record whose every covered pixel meets the Markstein quotient's range (div_rcp_rn) without a
+// per-pixel test: RN(1/det) usable, and the computed numerator of any pixel in its box either
+// exactly zero (pixel centre on the mean) or in [2^-60, 2^60). The exact numerator is a quadratic
+// form with eigenvalues >= det / (a + c) (those of the covariance) and |d|^2 >= 2^-50 when d != 0
+// (pixel centres are >= 0.5, so a nonzero float difference is >= 2^-25); its float evaluation
+// errs by < 2^-21 (a + c + |b|) |d|^2. The conditions below bound both ends with a 2x margin
+// (NaN or inf fields fail every comparison).
+#if GSS_FWD_SAFE
+__device__ __forceinline__ bool fwd_quotient_safe(const SplatRec& r, float rd) {
+  if (rd == 0.0f) return false;
+  const float a = r.a, c = r.c, ab = fabsf(r.b), det = r.det, tr = a + c;
+  if (!(a > 0.0f && c > 0.0f)) return false;
+  if (!(det >= 0x1p-19f * tr * (tr + ab))) return false;  // cancellation < half the exact value
+  if (!(det >= 0x1p-8f * tr)) return false;                // (det / tr) 2^-50 / 2 >= 2^-59
+  const float wx = fmaxf(fabsf((float)r.bx0 - r.mx), fabsf((float)r.bx1 - r.mx)) + 1.0f;
+  const float wy = fmaxf(fabsf((float)r.by0 - r.my), fabsf((float)r.by1 - r.my)) + 1.0f;
+  return (tr + ab) * (wx * wx + wy * wy) < 0x1p58f;         // < 2^60 with margin
+}
+#endif
+
 // contrib_eval (render.hpp:342-358); det > 0 holds for every binned splat (render.hpp:418).
 // The exponent is -q/2 <= 0 (or NaN), so only the underflow / NaN guards of expf apply.
 // rd: det_rcp(r.det) (the forward stages it per record), or 0 for the plain IEEE division.
@@ -633,7 +657,11 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
     const int nb = min(kFwdBatch, rg.y - b);
     for (int t = threadIdx.x; t < nb; t += kFwdThreads) {
       load_rec(&sh[t], recs, vals[b + t]);
-      sh[t].depth = det_rcp(sh[t].det);  // the SMEM copy's depth slot holds RN(1/det)
+      const float rd = det_rcp(sh[t].det);
+      sh[t].depth = rd;  // the SMEM copy's depth slot holds RN(1/det)
+#if GSS_FWD_SAFE
+      sh[t].off = fwd_quotient_safe(sh[t], rd) ? 1 : 0;  // and its off slot the range certificate
+#endif
     }
     __syncthreads();
     for (int c0j = 0; c0j < nb && __any_sync(0xffffffffu, !all_done); c0j += 32) {
@@ -665,6 +693,8 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
         // Markstein quotient range (div_rcp_rn): |num| in [2^-60, 2^60) and a usable RN(1/det);
         // a record without one (rd == 0) sends every quotient to the IEEE division.
         const float lo = q2.y != 0.0f ? 0x1p-60f : __int_as_float(0x7f800000);
+        auto pixels = [&](auto checked_c) {
+          constexpr bool kChecked = decltype(checked_c)::value;
 #pragma unroll
         for (int h = 0; h < kFwdPPT; ++h) {
           const bool inb = xin & (yb[h] >= bx.z) & (yb[h] < bx.w);
@@ -679,10 +709,12 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
           const float num = (cdxdx - b2dx * dy) + (q0.z * dy) * dy;
           const float qf = __fmul_rn(num, q2.y);
           float quo = __fmaf_rn(__fmaf_rn(-q2.w, qf, num), q2.y, qf);
-          const float an = fabsf(num);
-          const bool slow = !((an >= lo) & (an < 0x1p60f));
-          if (__any_sync(0xffffffffu, slow)) {  // rare: zero / extreme numerators, extreme det
-            if (slow) quo = __fdiv_rn(num, q2.w);
+          if (kChecked) {
+            const float an = fabsf(num);
+            const bool slow = !((an >= lo) & (an < 0x1p60f));
+            if (__any_sync(0xffffffffu, slow)) {  // rare: zero / extreme numerators, extreme det
+              if (slow) quo = __fdiv_rn(num, q2.w);
+            }
           }
           const float xe = -0.5f * max0(quo);
           const float wgt = gss_expf_nonpos_sel(xe, ek);
@@ -697,6 +729,13 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
             last[h] = lastv;
           }
         }
+        };
+#if GSS_FWD_SAFE
+        if (__float_as_int(q2.z) != 0)
+          pixels(std::false_type{});  // certified record: no per-pixel range test
+        else
+#endif
+          pixels(std::true_type{});
       }
       all_done = true;
 #pragma unroll
