@@ -190,6 +190,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) cull_kernel(const __grid
     const long long tile = t_begin + j;
     const int s = j % kStages;
     if ((tile + 1) * kTile <= a.n) {
+      // the stage's previous contents were read through the generic proxy; order those reads
+      // before the async-proxy (TMA) write that refills it
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&full_bar[s], kTileBytes);
       bulk_g2s(buf + (size_t)s * kTile * kGeo, a.geo + (size_t)tile * kTile * kGeo, kTileBytes, &full_bar[s]);
     } else {
@@ -260,6 +263,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) cull_kernel(const __grid
       if (lane == 0) {
         __threadfence_block();
         if (atomicAdd(&consumed[s], 1u) == kThreads / 32 - 1) {
+          __threadfence_block();  // acquire: every warp's reads of stage s precede the refill
           consumed[s] = 0;
           issue(j + kStages);
         }

@@ -188,3 +188,48 @@ def test_c1_scene_256(ref):
     g = gpu_render(ids, geo, ng, cam, [0, 256, 0, 256], gt=gt)
     print("visible", ids.size, "contribs", r["contribs"], "instances", g["instances"])
     check_parity(r, g)
+
+
+@pytest.mark.parametrize("seed", [3, 17])
+def test_forward_adversarial_geometry_bit_exact(ref, seed):
+    """Edge geometry for the composite's exact quotient and expf: needle-like splats (one log-scale
+    at -9..-6, condition numbers far beyond any per-record range certificate), huge splats covering
+    the whole view, and means placed on pixel centres by inverse projection (numerators of the
+    conic form near or exactly zero). Image, final T, counts and loss stay bit-identical to the
+    reference renderer; gradients within the tolerance."""
+    rng = np.random.default_rng(seed)
+    W, H = 40, 32
+    cam = O.look_at([0.2, -0.1, -3.0], [0.0, 0.0, 0.0], 60.0, 55.0, W, H, 0.1, 50.0)
+    R = cam[0:9].astype(np.float64).reshape(3, 3)
+    t = cam[9:12].astype(np.float64)
+    fx, fy, cx, cy = (float(v) for v in cam[12:16])
+    n = 240
+    rows = np.zeros((n, 59), np.float32)
+    for i in range(n):
+        if i % 3 == 0:  # mean on a pixel centre at a random depth
+            u, v, z = rng.integers(0, W) + 0.5, rng.integers(0, H) + 0.5, rng.uniform(2.0, 4.0)
+            pc = np.array([(u - cx) / fx * z, (v - cy) / fy * z, z])
+            rows[i, 0:3] = R.T @ (pc - t)
+        else:
+            rows[i, 0:3] = rng.uniform(-0.6, 0.6, 3)
+        kind = i % 4
+        if kind == 0:
+            ls = [rng.uniform(-9, -6), rng.uniform(-3, -1), rng.uniform(-3, -1)]  # needle
+        elif kind == 1:
+            ls = [rng.uniform(-1.0, 0.5)] * 3  # huge: covers the view
+        else:
+            ls = rng.uniform(-4.5, -2.0, 3)
+        rows[i, 3:6] = rng.permutation(ls)
+        q = rng.normal(size=4)
+        rows[i, 6:10] = q / np.linalg.norm(q)
+        rows[i, 10] = rng.uniform(-3.0, 1.0)
+        rows[i, 11:14] = rng.uniform(-1.0, 1.0, 3)
+        rows[i, 14:] = rng.normal(0, 0.1, 45)
+    geo, ng = rows[:, :10].copy(), rows[:, 10:].copy()
+    vp = [0, W, 0, H]
+    ids = O.ref_cull(geo, cam, vp)
+    assert ids.size > 100
+    gt = rng.uniform(0, 1, (H, W, 3)).astype(np.float32)
+    r = O.render("ref", ids, geo, ng, cam, vp, gt=gt)
+    g = gpu_render(ids, geo, ng, cam, vp, gt=gt)
+    check_parity(r, g)
