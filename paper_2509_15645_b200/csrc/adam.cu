@@ -1022,7 +1022,15 @@ bool host_resident(const gss_arena& a) {
   }
   return at.type == cudaMemoryTypeHost;
 }
-constexpr int kHostTierBlocks = 64;
+// (GSS_HOST_BLOCKS overrides it for A/B measurements)
+int host_tier_blocks() {
+  static const int b = [] {
+    const char* v = std::getenv("GSS_HOST_BLOCKS");
+    const int x = v ? std::atoi(v) : 0;
+    return x > 0 ? x : 64;
+  }();
+  return b;
+}
 
 unsigned long long* tally_dev(const gss_arena& a);
 __global__ void tally_add_kernel(unsigned long long* dst, const unsigned long long* src_u64, const int64_t* src_i64) {
@@ -1130,7 +1138,7 @@ void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* 
       staged_walk<K, MODE>(a, gd, *L, tl, st);
       return;
     }
-    if (host_resident(a)) wblocks = std::min(wblocks, 4 * kHostTierBlocks);  // reads + writes in flight
+    if (host_resident(a)) wblocks = std::min(wblocks, 4 * host_tier_blocks());  // reads + writes in flight
     if (vector_rows(a))
       walk4_kernel<K, MODE><<<wblocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, *L, tl);
     else
@@ -1402,7 +1410,7 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
   GSS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int64_t cap = count_dev ? std::max<int64_t>(count, a.n) : count;
   int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kRestoreChunk), (int64_t)sms * 64));
-  if (host_resident(a)) blocks = std::min(blocks, kHostTierBlocks);
+  if (host_resident(a)) blocks = std::min(blocks, host_tier_blocks());
   const size_t pb_bytes = ((size_t)(ceil_div(a.n, kRowsPerBlock) + 1) * 4 + 255) / 256 * 256;
   const bool host = host_resident(a);
   // Host tier with a host-known row count: gather the rows into HBM staging over the link first,

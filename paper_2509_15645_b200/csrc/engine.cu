@@ -19,6 +19,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -514,7 +515,17 @@ void stage_forward_params(gss_engine* e, int g) {
 }
 
 // engine.hpp:311-377.
-void stage_render(gss_engine* e, int g, const gss_camera& cam, const float* gt_dev, float* loss_out) {
+// In-place host tier run without overlap of its zero-copy passes and the render (GSS_HOST_SERIAL, A/B).
+bool host_serial(const gss_engine* e) {
+  static const int env = [] {
+    const char* v = std::getenv("GSS_HOST_SERIAL");
+    return v ? (v[0] == '1' ? 1 : 0) : -1;
+  }();
+  return e->ng_host && e->cfg.pipelined && env == 1;
+}
+
+void stage_render(gss_engine* e, int g, const gss_camera& cam, const float* gt_dev, float* loss_out,
+                  int after_lazy = -1) {
   const int p = g % 3, b = g % 2;
   cudaStream_t s = e->sD;
   require(e->fwd_iter[b] == g, "render: forwarded buffer is not for this iteration", GSS_ERR_INVARIANT);
@@ -548,6 +559,7 @@ void stage_render(gss_engine* e, int g, const gss_camera& cam, const float* gt_d
       GSS_CUDA(cudaStreamWaitEvent(s, e->ev_fp[b].e, 0));
       // grads[b] is free once lazy(g-2) consumed it
       GSS_CUDA(cudaStreamWaitEvent(s, e->ev_lazy[b].e, 0));
+      if (after_lazy >= 0) GSS_CUDA(cudaStreamWaitEvent(s, e->ev_lazy[after_lazy % 2].e, 0));
     }
     if (step_gt) GSS_CUDA(cudaStreamWaitEvent(s, e->ev_gt.e, 0));
   };
@@ -663,9 +675,13 @@ void iteration(gss_engine* e, int g, const gss_camera& cam, const float* gt_dev,
   const int owed = e->open_pending;
   // lazy(g-1) runs on stream H after fp(g) in both modes (pipelined: overlapping render(g) on D).
   // It is enqueued after render(g): a host-tier lazy pass reads its touched count back before
-  // chunking (staged_walk), and render(g) must already be queued on D by then.
-  stage_render(e, g, cam, gt_dev, loss_out);
-  if (owed >= 0) stage_lazy(e, owed);
+  // chunking (staged_walk), and render(g) must already be queued on D by then. With the in-place
+  // host tier and host_serial, lazy(g-1) is enqueued first and render(g) waits for it: the host
+  // link's zero-copy traffic then never shares the SMs' memory path with the render.
+  const bool serial_host = host_serial(e);
+  if (serial_host && owed >= 0) stage_lazy(e, owed);
+  stage_render(e, g, cam, gt_dev, loss_out, serial_host && owed >= 0 ? owed : -1);
+  if (!serial_host && owed >= 0) stage_lazy(e, owed);
   stage_geo_update(e, g);
   stage_handoff(e, g);
   e->open_pending = g;
