@@ -1023,12 +1023,17 @@ bool host_resident(const gss_arena& a) {
   return at.type == cudaMemoryTypeHost;
 }
 // (GSS_HOST_BLOCKS overrides it for A/B measurements)
-int host_tier_blocks() {
-  static const int b = [] {
-    const char* v = std::getenv("GSS_HOST_BLOCKS");
-    const int x = v ? std::atoi(v) : 0;
-    return x > 0 ? x : 64;
-  }();
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  const int x = v ? std::atoi(v) : 0;
+  return x > 0 ? x : dflt;
+}
+int host_tier_blocks() {  // forwarding gather over host rows
+  static const int b = env_int("GSS_HOST_BLOCKS", 64);
+  return b;
+}
+int host_walk_blocks() {  // deferred walk over host rows (reads and writes in flight)
+  static const int b = env_int("GSS_HOST_WALK_BLOCKS", 4 * host_tier_blocks());
   return b;
 }
 
@@ -1138,7 +1143,7 @@ void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* 
       staged_walk<K, MODE>(a, gd, *L, tl, st);
       return;
     }
-    if (host_resident(a)) wblocks = std::min(wblocks, 4 * host_tier_blocks());  // reads + writes in flight
+    if (host_resident(a)) wblocks = std::min(wblocks, host_walk_blocks());  // reads + writes in flight
     if (vector_rows(a))
       walk4_kernel<K, MODE><<<wblocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, *L, tl);
     else

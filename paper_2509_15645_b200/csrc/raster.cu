@@ -54,9 +54,6 @@ constexpr int kFwdBlockRows = 4 * kFwdPPT;
 #ifndef GSS_FWD_SAFE
 #define GSS_FWD_SAFE 1  // certified records skip the per-pixel quotient range test: composite -8% at C4
 #endif
-#ifndef GSS_BWD_ROWSKIP
-#define GSS_BWD_ROWSKIP 0
-#endif
 #ifndef GSS_BWD_MINB
 #define GSS_BWD_MINB 10  // 10 sweep CTAs per SM (96 registers, no spill): measured best
 #endif
@@ -1147,16 +1144,8 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
             (void)u;
           }
         } else {
-#if GSS_BWD_ROWSKIP
-          // pixel step q covers band rows 2q, 2q+1: skip the steps whose rows the box misses
-          // (warp-uniform; an idle step adds exact zeros and keeps the state, so skipping is exact)
-          const int rlo = r.by0 - by0w, rhi = r.by1 - by0w;  // box rows relative to the band
-#endif
 #pragma unroll
           for (int q = 0; q < kBwdPPT; ++q) {
-#if GSS_BWD_ROWSKIP
-            if (2 * q + 1 < rlo || 2 * q >= rhi) continue;
-#endif
             const bool u = bwd_contrib<false>(r, k, xin, bstart + jj, px[q], v);
 #if GSS_RASTER_STATS
             st_use += u ? 1 : 0;
