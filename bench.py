@@ -388,7 +388,11 @@ def run_ours(a, rank, world):
                            "contribs_per_step": contribs_per_step,
                            "composite_contribs_per_s": contribs_per_step / (kt["composite_ms"] / a.steps / 1e3),
                            "sweep_contribs_per_s": contribs_per_step / (kt["sweep_ms"] / a.steps / 1e3),
-                           "composite_share_of_step": kt["composite_ms"] / ms, "sweep_share_of_step": kt["sweep_ms"] / ms},
+                           "composite_share_of_step": kt["composite_ms"] / ms, "sweep_share_of_step": kt["sweep_ms"] / ms,
+                           # every timed render phase per step (CUDA events on stream D; the geometry
+                           # phase includes the instance-count round trip to the host)
+                           "phases_ms_per_step": {k: kt[f"{k}_ms"] / a.steps for k in
+                                                  ("geometry", "colour", "composite", "sweep", "slot_sums", "chain")}},
         "kernels": kern,
         "e2e": e2e,
         "host_offload": host,

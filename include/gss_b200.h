@@ -329,6 +329,10 @@ int64_t gss_engine_timeline(gss_engine* e, gss_timeline_row* rows, int64_t cap);
  * two-stream schedule; n = 0 disables. Results must not change (every edge is an event). */
 int gss_engine_stage_delays(gss_engine* e, const uint32_t* ns, int32_t n);
 int gss_engine_kernel_times(gss_engine* e, double* ms2, int64_t* n2, uint64_t* contribs);
+/* The same with every timed render phase: ms6 / n6 = composite, sweep, geometry (projection,
+ * depth sort, binning, tile sort and ranges, including the instance-count round trip), colour,
+ * per-slot sums, chain. */
+int gss_engine_render_times(gss_engine* e, double* ms6, int64_t* n6, uint64_t* contribs);
 
 /* ---- densification (trainer.hpp:166-213, engine.hpp:116-163) ------------- */
 /* DensifyConfig (trainer.hpp:32-47): the thresholds of plan_densify. */

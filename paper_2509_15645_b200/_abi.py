@@ -181,6 +181,7 @@ SIGNATURES = {
     "gss_engine_timeline": (I64, [P, P, I64]),
     "gss_engine_stage_delays": (C.c_int, [P, P, I32]),
     "gss_engine_kernel_times": (C.c_int, [P, P, P, P]),
+    "gss_engine_render_times": (C.c_int, [P, P, P, P]),
     "gss_raster_stats_enabled": (I32, []),
     "gss_ply_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "gss_ply_read": (C.c_int, [P, P, P, P]),

@@ -84,7 +84,7 @@ void engine_kernel_timing(gss_engine* e, bool on);
 void engine_timeline_enable(gss_engine* e, bool on);
 int64_t engine_timeline(gss_engine* e, gss_timeline_row* rows, int64_t cap);
 void engine_stage_delays(gss_engine* e, const uint32_t* ns, int n);
-void engine_kernel_times(gss_engine* e, double* ms2, int64_t* n2, uint64_t* contribs);
+void engine_kernel_times(gss_engine* e, double* ms2, int64_t* n2, uint64_t* contribs, int nk);
 int64_t engine_count(gss_engine* e);
 
 namespace {
@@ -464,6 +464,9 @@ GSS_API int64_t gss_engine_timeline(gss_engine* e, gss_timeline_row* rows, int64
 GSS_API int gss_engine_stage_delays(gss_engine* e, const uint32_t* ns, int32_t n) {
   return guarded([&] { engine_stage_delays(e, ns, n); });
 }
+GSS_API int gss_engine_render_times(gss_engine* e, double* ms6, int64_t* n6, uint64_t* contribs) {
+  return guarded([&] { engine_kernel_times(e, ms6, n6, contribs, 6); });
+}
 GSS_API int gss_engine_kernel_times(gss_engine* e, double* ms2, int64_t* n2, uint64_t* contribs) {
-  return guarded([&] { engine_kernel_times(e, ms2, n2, contribs); });
+  return guarded([&] { engine_kernel_times(e, ms2, n2, contribs, 2); });
 }

@@ -1028,12 +1028,15 @@ int env_int(const char* name, int dflt) {
   const int x = v ? std::atoi(v) : 0;
   return x > 0 ? x : dflt;
 }
+// Measured at 18M rows / 14.5% visible (profiles/r02_host_tier_grid.txt): the in-place passes move
+// the host link's bytes fastest with few CTAs — the deferred walk 48 ms at 16-32 CTAs vs 57 ms at
+// 256, the forwarding gather ~37 ms from 16 CTAs up.
 int host_tier_blocks() {  // forwarding gather over host rows
-  static const int b = env_int("GSS_HOST_BLOCKS", 64);
+  static const int b = env_int("GSS_HOST_BLOCKS", 32);
   return b;
 }
 int host_walk_blocks() {  // deferred walk over host rows (reads and writes in flight)
-  static const int b = env_int("GSS_HOST_WALK_BLOCKS", 4 * host_tier_blocks());
+  static const int b = env_int("GSS_HOST_WALK_BLOCKS", 32);
   return b;
 }
 

@@ -51,7 +51,7 @@ void render_ctx_destroy(gss_render_ctx* ctx);
 gss_render_ctx* render_ctx_create();
 void arena_release(const gss_arena* ap);
 void render_ctx_timing(gss_render_ctx* ctx, bool on);
-void render_ctx_times(gss_render_ctx* ctx, double* ms2, int64_t* n2, uint64_t* contribs);
+void render_ctx_times(gss_render_ctx* ctx, double* ms2, int64_t* n2, uint64_t* contribs, int nk);
 void set_host_chunk_bytes(int64_t bytes);
 }  // namespace gssd
 
@@ -757,13 +757,19 @@ gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss
   e->n = n;
   e->cams.assign(cams, cams + ncams);
   e->ng_host = cfg->nongeo_on_host != 0;
-  GSS_CUDA(cudaStreamCreateWithFlags(&e->sD, cudaStreamNonBlocking));
   {
-    // stream H (the host-tier stage, link-bound with small grids) at the highest priority, so its
-    // CTAs are scheduled ahead of the render's on stream D
+    // Stream priorities (GSS_STREAM_PRIO, A/B): 0 = equal, 1 = stream H first (its link-bound
+    // host-tier passes get their few CTAs scheduled ahead of the render), 2 = stream D first
+    // (the render's geometry phase, on the critical path, is not slowed by the concurrent
+    // forwarding gather / lazy update).
     int lo = 0, hi = 0;
     GSS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    GSS_CUDA(cudaStreamCreateWithPriority(&e->sH, cudaStreamNonBlocking, hi));
+    const char* ev = std::getenv("GSS_STREAM_PRIO");
+    // default 1: measured equal to 0 within noise at C4 and ahead of 2 (which starves the lazy
+    // update behind the render: profiles/r02_stream_priority_ab.txt)
+    const int mode = ev ? std::atoi(ev) : 1;
+    GSS_CUDA(cudaStreamCreateWithPriority(&e->sD, cudaStreamNonBlocking, mode == 2 ? hi : lo));
+    GSS_CUDA(cudaStreamCreateWithPriority(&e->sH, cudaStreamNonBlocking, mode == 1 ? hi : lo));
   }
   GSS_CUDA(cudaStreamCreateWithFlags(&e->sC, cudaStreamNonBlocking));
   const size_t nn = (size_t)std::max<int64_t>(n, 1);
@@ -1173,11 +1179,11 @@ void engine_kernel_timing(gss_engine* e, bool on) {
   require(e != nullptr, "engine: null");
   render_ctx_timing(e->rctx, on);
 }
-void engine_kernel_times(gss_engine* e, double* ms2, int64_t* n2, uint64_t* contribs) {
+void engine_kernel_times(gss_engine* e, double* ms2, int64_t* n2, uint64_t* contribs, int nk) {
   require(e != nullptr, "engine: null");
   if (e->open_pending >= 0) drain(e);
   GSS_CUDA(cudaDeviceSynchronize());
-  render_ctx_times(e->rctx, ms2, n2, contribs);
+  render_ctx_times(e->rctx, ms2, n2, contribs, nk);
 }
 int64_t engine_count(gss_engine* e) { return e ? e->n : 0; }
 

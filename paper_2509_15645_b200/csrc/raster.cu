@@ -153,8 +153,11 @@ struct gss_render_ctx {
   };
   std::vector<KTime> ktimes;
   std::vector<cudaEvent_t> kfree;
-  double kms[2] = {0.0, 0.0};
-  int64_t kn[2] = {0, 0};
+  // kinds: 0 composite, 1 sweep, 2 geometry (projection .. tile order, incl. the instance-count
+  // round trip), 3 colour, 4 per-slot sums, 5 chain
+  static constexpr int kKinds = 6;
+  double kms[kKinds] = {};
+  int64_t kn[kKinds] = {};
   unsigned long long* contribs_dev = nullptr;  // running total of composited contributions
 };
 
@@ -1766,6 +1769,7 @@ void per_slot_sums(gss_render_ctx* ctx, const float* d_img, float* sums, cudaStr
 #ifndef GSS_SUM_DEPTH
 #define GSS_SUM_DEPTH 1
 #endif
+  ktime_begin(ctx, 4, st);
   if (GSS_SUM_DEPTH && ctx->pay_sorted) {
     // slots never binned (V_bin .. V in depth order: depth key 0xffffffff) have no instances: their
     // ranges are empty and their sums are written as zeros like every other slot's
@@ -1775,6 +1779,7 @@ void per_slot_sums(gss_render_ctx* ctx, const float* d_img, float* sums, cudaStr
     slot_sum_kernel<<<(unsigned)ceil_div(V, kSumThreads), kSumThreads, 0, st>>>(V, soff, nts, partials, sums);
   }
   GSS_LAUNCHED();
+  ktime_end(ctx, st);
 }
 
 void launch_chain(const SceneDev& sc, const Cam& cam, const Win& w, int64_t V, const SplatRec* recs, const float* sums,
@@ -1860,8 +1865,10 @@ void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int6
   require(gg && gn, "rasterize_backward: null gradient buffers");
   float* sums = static_cast<float*>(ctx->sums.get((size_t)V * 9 * 4, st));
   per_slot_sums(ctx, d_img, sums, st);
+  ktime_begin(ctx, 5, st);
   launch_chain(ctx->sc, ctx->cam, ctx->win, V, static_cast<const SplatRec*>(ctx->recs.p), sums, gg, gstride, gn,
                nstride, mean2d, st);
+  ktime_end(ctx, st);
 }
 
 // Two-phase forward for the engine: the geometry half (projection, depth/tile sort, tile ranges)
@@ -1870,6 +1877,7 @@ void rasterize_backward(gss_render_ctx* ctx, const float* d_img, float* gg, int6
 void rasterize_forward_geometry(gss_render_ctx* ctx, const gss_render_scene* scene, const gss_camera* cam,
                                 const gss_viewport* vp, cudaStream_t st) {
   require(ctx && scene && cam && vp, "rasterize_forward: null argument");
+  ktime_begin(ctx, 2, st);
   set_scene(ctx, scene);
   if (!ctx->pinned) GSS_CUDA(cudaMallocHost(&ctx->pinned, 4 * sizeof(int64_t)));
   const Win w = make_window(*vp);
@@ -1883,6 +1891,7 @@ void rasterize_forward_geometry(gss_render_ctx* ctx, const gss_render_scene* sce
     GSS_LAUNCHED();
   }
   bin_phase(ctx, w, V, st);
+  ktime_end(ctx, st);
 }
 
 void rasterize_forward_finish(gss_render_ctx* ctx, float* image, const float* gt, int64_t normalizer, float* d_img,
@@ -1896,6 +1905,7 @@ void rasterize_forward_finish(gss_render_ctx* ctx, float* image, const float* gt
           "compute_loss_l1: image and ground-truth shapes differ");
   const float inv = gt ? 1.0f / (float)(double)(normalizer > 0 ? normalizer : npix * 3) : 0.0f;
   if (V > 0 && npix > 0) {
+    ktime_begin(ctx, 3, st);
     auto ck = ctx->sc.sh_degree == 0 ? colour_kernel<0>
               : ctx->sc.sh_degree == 1 ? colour_kernel<1>
               : ctx->sc.sh_degree == 2 ? colour_kernel<2> : colour_kernel<3>;
@@ -1903,6 +1913,7 @@ void rasterize_forward_finish(gss_render_ctx* ctx, float* image, const float* gt
                                                               static_cast<const int32_t*>(ctx->ntiles.p),
                                                               static_cast<SplatRec*>(ctx->recs.p));
     GSS_LAUNCHED();
+    ktime_end(ctx, st);
   }
   composite_phase(ctx, w, V, FwdOut{image, gt, ctx->cam.width, inv, d_img, loss_dev, nullptr, nullptr, nullptr,
                                     nullptr}, st);
@@ -2050,7 +2061,7 @@ void render_ctx_timing(gss_render_ctx* ctx, bool on) {
 // Folds the recorded intervals (all must have completed: call after a sync) into
 // out[0..1] = total ms of forward_kernel / backward_kernel launches, n[0..1] = launches,
 // *contribs = composited contributions; resets the accumulators.
-void render_ctx_times(gss_render_ctx* ctx, double* ms2, int64_t* n2, uint64_t* contribs) {
+void render_ctx_times(gss_render_ctx* ctx, double* ms2, int64_t* n2, uint64_t* contribs, int nk) {
   require(ctx != nullptr, "render ctx: null");
   for (auto& t : ctx->ktimes) {
     float ms = 0.0f;
@@ -2063,9 +2074,9 @@ void render_ctx_times(gss_render_ctx* ctx, double* ms2, int64_t* n2, uint64_t* c
   }
   cudaGetLastError();
   ctx->ktimes.clear();
-  for (int k = 0; k < 2; ++k) {
-    if (ms2) ms2[k] = ctx->kms[k];
-    if (n2) n2[k] = ctx->kn[k];
+  for (int k = 0; k < gss_render_ctx::kKinds; ++k) {
+    if (ms2 && k < nk) ms2[k] = ctx->kms[k];
+    if (n2 && k < nk) n2[k] = ctx->kn[k];
     ctx->kms[k] = 0.0;
     ctx->kn[k] = 0;
   }

@@ -887,12 +887,16 @@ class OffloadEngine:
     def kernel_times(self):
         """Drains; {composite_ms, sweep_ms, composite_launches, sweep_launches, contribs} since the
         last call (contribs = contributions composited = useful backward contributions)."""
-        ms = np.zeros(2, np.float64)
-        n = np.zeros(2, np.int64)
+        ms = np.zeros(6, np.float64)
+        n = np.zeros(6, np.int64)
         c = C.c_uint64()
-        check(lib().gss_engine_kernel_times(self.h, ms.ctypes.data, n.ctypes.data, C.byref(c)))
-        return {"composite_ms": float(ms[0]), "sweep_ms": float(ms[1]), "composite_launches": int(n[0]),
-                "sweep_launches": int(n[1]), "contribs": int(c.value)}
+        check(lib().gss_engine_render_times(self.h, ms.ctypes.data, n.ctypes.data, C.byref(c)))
+        out = {"composite_ms": float(ms[0]), "sweep_ms": float(ms[1]), "composite_launches": int(n[0]),
+               "sweep_launches": int(n[1]), "contribs": int(c.value)}
+        for i, k in ((2, "geometry"), (3, "colour"), (4, "slot_sums"), (5, "chain")):
+            out[f"{k}_ms"] = float(ms[i])
+            out[f"{k}_launches"] = int(n[i])
+        return out
 
     def densify(self, cfg: DensifyConfig, extent: float, seed: int):
         """A densification event (trainer.hpp:578-591): snapshot, plan_densify, apply_densify."""
