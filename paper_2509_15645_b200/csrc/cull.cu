@@ -425,8 +425,13 @@ void cull(const float* geo, int64_t n, int64_t stride, const gss_camera* cam, co
   a.n = n;
   a.stride = stride;
   a.ntiles = ceil_div(n, kTile);
-  const int64_t ctas = std::min<int64_t>(a.ntiles, std::max<int64_t>((int64_t)sm_count() * kCtasPerSm,
-                                                                       ceil_div(a.ntiles, kMaxTiles)));
+  // Whole waves of co-resident CTAs with equal tile counts: a grid of k full waves (k the fewest
+  // waves whose CTAs hold every tile at <= kMaxTiles each) instead of ceil(ntiles / kMaxTiles)
+  // CTAs, whose last wave would run partly empty (40M rows: 611 CTAs = 1.4 waves of 444, i.e. two
+  // CTA durations of 128 tiles; now 888 CTAs of 88 tiles = two durations of 88).
+  const int64_t wave = (int64_t)sm_count() * kCtasPerSm;
+  const int64_t waves = std::max<int64_t>(1, ceil_div(a.ntiles, wave * kMaxTiles));
+  const int64_t ctas = std::min<int64_t>(a.ntiles, wave * waves);
   a.tiles_per_cta = (int)ceil_div(a.ntiles, ctas);
   const int grid = (int)ceil_div(a.ntiles, a.tiles_per_cta);
   a.mask = mask;
