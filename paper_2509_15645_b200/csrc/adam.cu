@@ -108,7 +108,23 @@ struct GradsDev {
   const float* rows;
   int64_t stride;
   int col0;
+  int vec4;  // rows 16-byte aligned with whole float4 units up to the padded dim: one 16-byte load per unit
 };
+
+// gradient unit (4 columns from c0) of grads row `sl`: zero for no row or columns past dim
+__device__ __forceinline__ void grad_unit(const GradsDev& g, int64_t sl, int c0, int dim, bool ok, float out[4]) {
+  const float* row = g.rows + sl * g.stride + g.col0 + c0;
+  if (g.vec4) {
+    const float4 v = (ok && sl >= 0) ? *reinterpret_cast<const float4*>(row) : make_float4(0.f, 0.f, 0.f, 0.f);
+    out[0] = v.x;
+    out[1] = c0 + 1 < dim ? v.y : 0.0f;
+    out[2] = c0 + 2 < dim ? v.z : 0.0f;
+    out[3] = c0 + 3 < dim ? v.w : 0.0f;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[i] = (ok && sl >= 0 && c0 + i < dim) ? row[i] : 0.0f;
+  }
+}
 
 __device__ __forceinline__ int64_t grads_count(const GradsDev& g) { return g.count_dev ? *g.count_dev : g.count; }
 
@@ -598,10 +614,7 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_WALK4_MINB) walk4_kernel(Aren
         w[u] = ok[u] ? ld4(a.w + o) : make_float4(0.f, 0.f, 0.f, 0.f);
         m[u] = ok[u] ? ld4(a.m + o) : make_float4(0.f, 0.f, 0.f, 0.f);
         v[u] = ok[u] ? ld4(a.v + o) : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float* grow = gr.rows + (int64_t)sl * gr.stride + gr.col0 + c0[u];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          gv[u][i] = (ok[u] && sl >= 0 && c0[u] + i < dim) ? grow[i] : 0.0f;
+        grad_unit(gr, sl, c0[u], dim, ok[u], gv[u]);
         r += dq;
         q += dr;
         if (q >= nq) {
@@ -761,9 +774,7 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_RESTORE_MINB) restore_kernel(
           w[u] = ok[u] ? ld4(a.w + o) : make_float4(0.f, 0.f, 0.f, 0.f);
           m[u] = ok[u] ? ld4(a.m + o) : make_float4(0.f, 0.f, 0.f, 0.f);
           v[u] = ok[u] ? ld4(a.v + o) : make_float4(0.f, 0.f, 0.f, 0.f);
-          const float* prow = pend.rows + (int64_t)sl * pend.stride + pend.col0 + c0[u];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) gv[u][i] = (ok[u] && sl >= 0 && c0[u] + i < dim) ? prow[i] : 0.0f;
+          grad_unit(pend, sl, c0[u], dim, ok[u], gv[u]);
           r += dq;
           q += dr;
           if (q >= nq) {
@@ -980,11 +991,18 @@ void validate_arena(const gss_arena& a) {
   require(a.n == 0 || (a.w && a.m && a.v && a.counter), "arena: null buffer");
 }
 
-GradsDev grads_dev(const gss_sparse_grads* g) {
+GradsDev grads_dev(const gss_sparse_grads* g, int dim = 0) {
   GradsDev d{};
   if (g) {
     d.ids = g->ids; d.count = g->count; d.count_dev = g->count_dev; d.rows = g->rows;
     d.stride = g->stride; d.col0 = g->col0;
+    // the engine's gradient stage: 52-float rows, col0 0, 16-byte aligned (the padding columns are
+    // loaded and discarded)
+#ifndef GSS_GRAD_VEC4
+#define GSS_GRAD_VEC4 1
+#endif
+    d.vec4 = GSS_GRAD_VEC4 && dim > 0 && g->rows && reinterpret_cast<uintptr_t>(g->rows) % 16 == 0 && g->stride % 4 == 0 &&
+             g->col0 % 4 == 0 && g->stride >= g->col0 + (dim + 3) / 4 * 4;
   }
   return d;
 }
@@ -1197,7 +1215,7 @@ void adam_update(gss_arena* ap, const gss_sparse_grads* grads, int32_t* touched_
   gss_arena& a = *ap;
   validate_arena(a);
   const int64_t t = a.step + 1;
-  const GradsDev gd = grads_dev(grads);
+  const GradsDev gd = grads_dev(grads, a.dim);
   require(gd.count >= 0, "sparse grads: negative count");
   require(gd.count == 0 || gd.count_dev || (gd.ids && gd.rows), "sparse grads: null ids/rows");
   require(gd.col0 >= 0, "sparse grads: negative col0");
@@ -1362,9 +1380,7 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_RESTORE_MINB) restore_walk_ke
         w[u] = ok[u] ? ld4(a.w + o) : make_float4(0.f, 0.f, 0.f, 0.f);
         m[u] = ok[u] ? ld4(a.m + o) : make_float4(0.f, 0.f, 0.f, 0.f);
         v[u] = ok[u] ? ld4(a.v + o) : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float* prow = pend.rows + (int64_t)sl * pend.stride + pend.col0 + c0[u];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) gv[u][i] = (ok[u] && sl >= 0 && c0[u] + i < dim) ? prow[i] : 0.0f;
+        grad_unit(pend, sl, c0[u], dim, ok[u], gv[u]);
         r += dq;
         q += dr;
         if (q >= nq) {
@@ -1406,7 +1422,7 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
   require(count == 0 || count_dev || (ids && out), "restore_view: null ids/out");
   if (count == 0 && !count_dev) return;
   const int64_t t = a.step + 1;
-  GradsDev pd = grads_dev(pending);
+  GradsDev pd = grads_dev(pending, a.dim);
   if (count_dev) {  // adam.hpp:287-288 with a device-side row count
     tally_add_kernel<<<1, 1, 0, st>>>(tally_dev(a) + 1, nullptr, count_dev);
     GSS_LAUNCHED();

@@ -24,15 +24,16 @@ ng.w.copy_(torch.rand(n, 49, device="cuda", generator=gen) * 2 - 1)
 geo.w.copy_(torch.rand(n, 10, device="cuda", generator=gen) * 2 - 1)
 
 
-def draw():
+def draw():  # gradient rows in the engine's stage layouts: non-geometric 52-float rows, geometric 10
     ids = torch.nonzero(torch.rand(n, device="cuda", generator=gen) < frac).flatten().to(torch.int32)
-    return ids, torch.randn(ids.numel(), 59, device="cuda", generator=gen)
+    return ids, torch.randn(ids.numel(), 52, device="cuda", generator=gen), torch.randn(ids.numel(), 10, device="cuda",
+                                                                                          generator=gen)
 
 
 sets = [draw() for _ in range(4)]
 for it in range(20):  # steady-state counters
-    ids, rows = sets[it % 4]
-    G.deferred_update(ng, G.SparseGrads(ids, rows, 59, 10), want_touched=False, check_invariants=False)
+    ids, rows, _ = sets[it % 4]
+    G.deferred_update(ng, G.SparseGrads(ids, rows, 52, 0), want_touched=False, check_invariants=False)
 torch.cuda.synchronize()
 res = {"n": n, "frac": frac, "lib": os.environ.get("GSS_LIB", "default")}
 reps = 8
@@ -40,9 +41,9 @@ ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 # deferred update (touched count read back for the byte count)
 tms, tbytes = [], []
 for r in range(reps):
-    ids, rows = sets[r % 4]
+    ids, rows, _ = sets[r % 4]
     ev[0].record()
-    t = G.deferred_update(ng, G.SparseGrads(ids, rows, 59, 10), want_touched=False, check_invariants=False)
+    t = G.deferred_update(ng, G.SparseGrads(ids, rows, 52, 0), want_touched=False, check_invariants=False)
     ev[1].record()
     torch.cuda.synchronize()
     touched = int(t.item())
@@ -51,9 +52,9 @@ for r in range(reps):
 res["deferred_ms"] = float(np.median(tms))
 res["deferred_frac"] = float(np.median(tbytes)) / (res["deferred_ms"] / 1e3) / 1e9 / peak
 # forwarding gather with pending grads
-ids, rows = sets[0]
-pids, prow = sets[1]
-pend = G.SparseGrads(pids, prow, 59, 10)
+ids, rows, _ = sets[0]
+pids, prow, _ = sets[1]
+pend = G.SparseGrads(pids, prow, 52, 0)
 out = torch.empty(ids.numel(), 49, device="cuda")
 gms = []
 for r in range(reps):
@@ -68,9 +69,9 @@ res["gather_frac"] = (V * (3 * 196 + 1) + Vp * 196 + V * 196) / (res["gather_ms"
 # dense geo update (defer_max 0)
 dms = []
 for r in range(reps):
-    ids, rows = sets[r % 4]
+    ids, _, grows = sets[r % 4]
     ev[0].record()
-    G.deferred_update(geo, G.SparseGrads(ids, rows, 59, 0), want_touched=False, check_invariants=False)
+    G.deferred_update(geo, G.SparseGrads(ids, grows, 10, 0), want_touched=False, check_invariants=False)
     ev[1].record()
     torch.cuda.synchronize()
     dms.append(ev[0].elapsed_time(ev[1]))
