@@ -836,6 +836,38 @@ gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss
     }
   }
   e->rctx = render_ctx_create();
+  // Reserve every per-view buffer for the stored cameras: each is culled and rendered once (forward
+  // + backward with a zero image gradient; no optimizer state changes), so the stage buffers and
+  // the rasterizer's records, sort keys, instance partials and per-pixel buffers reach their size
+  // before run() — its first visit of a larger view does not stop to grow them. Later growth (the
+  // scene moves, densification) still happens on demand.
+  if (n > 0 && !e->cams.empty()) {
+    int64_t vmax = 0;
+    GSS_CUDA(cudaMemsetAsync(e->d_img, 0, (size_t)e->W * e->H * 3 * sizeof(float), e->sD));
+    for (const auto& c : e->cams) {
+      const gss_viewport vp{0.0f, (float)c.width, 0.0f, (float)c.height};
+      cull(e->gw, e->n, kGeoDim, &c, &vp, cfg->low_pass, nullptr, e->ids[0], e->count[0], e->cull_ws,
+           e->cull_ws_bytes, e->sD);
+      GSS_CUDA(cudaMemcpyAsync(e->count_host, e->count[0], sizeof(int64_t), cudaMemcpyDeviceToHost, e->sD));
+      GSS_CUDA(cudaStreamSynchronize(e->sD));
+      const int64_t V = e->count_host[0];
+      vmax = std::max(vmax, V);
+      ensure_rows(e.get(), std::min<int64_t>(n, vmax + vmax / 4));
+      gss_render_scene sc{};
+      sc.ids = e->ids[0];
+      sc.count = V;
+      sc.geo = e->gw;
+      sc.geo_stride = kGeoDim;
+      sc.nongeo = e->nw;  // the stored rows by id (w segment of the interleaved tier)
+      sc.nongeo_stride = kNgStride;
+      sc.nongeo_compact = 0;
+      sc.sh_degree = cfg->sh_degree;
+      sc.low_pass = cfg->low_pass;
+      rasterize_forward_geometry(e->rctx, &sc, &c, &vp, e->sD);
+      rasterize_forward_finish(e->rctx, e->image, nullptr, 0, nullptr, nullptr, e->sD);
+      rasterize_backward(e->rctx, e->d_img, e->g_geo[0], kGeoDim, e->g_ng[0], kNgGradStride, e->g_m2d[0], e->sD);
+    }
+  }
   GSS_CUDA(cudaStreamSynchronize(e->sD));
   return e.release();
 }
