@@ -55,7 +55,7 @@ constexpr int kFwdBlockRows = 4 * kFwdPPT;
 #define GSS_FWD_SAFE 1  // certified records skip the per-pixel quotient range test: composite -8% at C4
 #endif
 #ifndef GSS_BWD_MINB
-#define GSS_BWD_MINB 10  // 10 sweep CTAs per SM (96 registers, no spill): measured best
+#define GSS_BWD_MINB 11  // 11 sweep CTAs per SM (78 registers, no spill): measured best, 12+ slower
 #endif
 #if GSS_FWD_MINB > 0
 #define GSS_FWD_BOUNDS __launch_bounds__(kFwdThreads, GSS_FWD_MINB)
@@ -1209,7 +1209,7 @@ constexpr int kSumChunk = 128;  // instances per staged chunk (4.5 KB per warp)
 __global__ void __launch_bounds__(kSumWarps * 32) slot_sum_depth_kernel(int64_t V, const int32_t* __restrict__ offsets,
                                                                       const uint64_t* __restrict__ pay,
                                                                       const float* __restrict__ partials, float* sums) {
-  __shared__ float stage[kSumWarps][kSumChunk * 9];
+  __shared__ __align__(16) float stage[kSumWarps][kSumChunk * 9];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t i0 = ((int64_t)blockIdx.x * kSumWarps + warp) * 32;
   if (i0 >= V) return;
@@ -1224,11 +1224,15 @@ __global__ void __launch_bounds__(kSumWarps * 32) slot_sum_depth_kernel(int64_t 
 #pragma unroll
   for (int c = 0; c < 9; ++c) acc[c] = 0.0f;
   float* st = stage[warp];
-  for (int32_t c0 = s0; c0 < s1; c0 += kSumChunk) {
+  // chunks start on multiples of 4 instances (36 x 4 = 144 bytes: 16-byte aligned), so the span is
+  // copied in 16-byte pieces (the instances before s0 are copied and ignored)
+  for (int32_t c0 = s0 & ~3; c0 < s1; c0 += kSumChunk) {
     const int n = (s1 - c0 < kSumChunk ? s1 - c0 : kSumChunk) * 9;
     const float* src = partials + (int64_t)c0 * 9;
     __syncwarp();
-    for (int e = lane; e < n; e += 32) cp_async4(st + e, src + e);
+    const int n4 = n >> 2;
+    for (int e = lane; e < n4; e += 32) cp_async16(st + 4 * e, src + 4 * e);
+    for (int e = 4 * n4 + lane; e < n; e += 32) cp_async4(st + e, src + e);
     cp_async_wait_all();
     __syncwarp();
     const int32_t a = o0 > c0 ? o0 : c0, b = o1 < c0 + kSumChunk ? o1 : c0 + kSumChunk;
