@@ -17,11 +17,11 @@ void expf_device(const float* x, float* y, int64_t n, cudaStream_t st);
 void build_group_luts(double lr, double b1, double b2, double eps, int64_t t, int max_delay, float* param,
                       float* mom, float* var, float* pow_b1, float* pow_b2, float* scalars);
 void adam_update(gss_arena* ap, const gss_sparse_grads* grads, int32_t* touched_ids, int64_t* touched_count,
-                 cudaStream_t st);
+                 cudaStream_t st, const uint32_t* split_mask = nullptr, cudaEvent_t split_before_set = nullptr);
 void adam_dense(gss_arena* ap, const float* grads, cudaStream_t st);
 void adam_flush(gss_arena* ap, cudaStream_t st);
 void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const int64_t* count_dev,
-                  const gss_sparse_grads* pending, float* out, cudaStream_t st);
+                  const gss_sparse_grads* pending, float* out, cudaStream_t st, cudaEvent_t after_resolve = nullptr);
 int arena_check(const gss_arena* ap, cudaStream_t st);
 void arena_release(const gss_arena* ap);
 void arena_access(const gss_arena* ap, uint64_t* out6);

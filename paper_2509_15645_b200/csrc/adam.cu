@@ -219,6 +219,8 @@ struct TouchList {  // rows a deferred pass touches (unordered; each row at most
   uint8_t* del;
   unsigned long long* count;
   int64_t t0 = 0, t1 = INT64_MAX;  // the walk's range of list entries (a staged chunk)
+  const uint32_t* filter = nullptr;  // optional row bit mask: walk only rows whose bit equals want
+  int want = 0;
 };
 
 template <int K, int MODE>
@@ -590,7 +592,11 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_WALK4_MINB) walk4_kernel(Aren
   const int64_t wstride = (int64_t)gridDim.x * (kUpdThreads / 32) * 32;
   for (int64_t t0 = tl.t0 + ((int64_t)blockIdx.x * (kUpdThreads / 32) + (threadIdx.x >> 5)) * 32; t0 < T;
        t0 += wstride) {
-    const bool mine = t0 + lane < T;
+    bool mine = t0 + lane < T;
+    if (mine && tl.filter) {
+      const int32_t rw = tl.row[t0 + lane];
+      mine = (int)((tl.filter[rw >> 5] >> (rw & 31)) & 1u) == tl.want;
+    }
     const int64_t my_base =
         mine ? (a.positional ? (t0 + lane - tl.t0) : (int64_t)tl.row[t0 + lane]) * a.stride : -1;
     const int32_t my_del = mine ? tl.del[t0 + lane] : 0;
@@ -1125,9 +1131,17 @@ void staged_walk(const gss_arena& a, const GradsDev& gd, const LutArgs<K>& L, co
   }
 }
 
+// A deferred pass whose walk is split by a row bit mask (the host tier's concurrent forwarding):
+// rows whose bit is clear are walked first; the walk of the rows whose bit is set waits for
+// `before_set` (recorded by the forwarding gather that must read them first).
+struct WalkSplit {
+  const uint32_t* mask = nullptr;
+  cudaEvent_t before_set = nullptr;
+};
+
 template <int K, int MODE>
 void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* tmask, int64_t* tcount,
-                   cudaStream_t st) {
+                   cudaStream_t st, const WalkSplit* split = nullptr) {
   auto L = std::make_unique<LutArgs<K>>();
   std::memset(L.get(), 0, sizeof(LutArgs<K>));
   fill_luts<K>(a, t, MODE == kFlush, *L);
@@ -1160,11 +1174,23 @@ void launch_update(const gss_arena& a, const GradsDev& gd, int64_t t, uint32_t* 
       GSS_LAUNCHED();
     }
     int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, kUpdThreads), (int64_t)sm_count() * GSS_WALK_GRID));
-    if (host_resident(a) && vector_rows(a) && host_staging()) {
+    if (host_resident(a) && vector_rows(a) && host_staging() && !(split && split->mask)) {
       staged_walk<K, MODE>(a, gd, *L, tl, st);
       return;
     }
     if (host_resident(a)) wblocks = std::min(wblocks, host_walk_blocks());  // reads + writes in flight
+    if (split && split->mask && vector_rows(a)) {
+      TouchList ta = tl, tb = tl;
+      ta.filter = tb.filter = split->mask;
+      ta.want = 0;
+      tb.want = 1;
+      walk4_kernel<K, MODE><<<wblocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, *L, ta);
+      GSS_LAUNCHED();
+      if (split->before_set) GSS_CUDA(cudaStreamWaitEvent(st, split->before_set, 0));
+      walk4_kernel<K, MODE><<<wblocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, *L, tb);
+      GSS_LAUNCHED();
+      return;
+    }
     if (vector_rows(a))
       walk4_kernel<K, MODE><<<wblocks, kUpdThreads, 0, st>>>(arena_dev(a), gd, *L, tl);
     else
@@ -1210,7 +1236,7 @@ std::unordered_map<const void*, HostTally> g_tally;  // guarded by g_flag_mu
 }  // namespace
 
 void adam_update(gss_arena* ap, const gss_sparse_grads* grads, int32_t* touched_ids, int64_t* touched_count,
-                 cudaStream_t st) {
+                 cudaStream_t st, const uint32_t* split_mask, cudaEvent_t split_before_set) {
   require(ap != nullptr, "arena: null");
   gss_arena& a = *ap;
   validate_arena(a);
@@ -1226,10 +1252,13 @@ void adam_update(gss_arena* ap, const gss_sparse_grads* grads, int32_t* touched_
   }
   uint32_t* tmask = nullptr;
   if (touched_ids) GSS_CUDA(cudaMallocAsync((void**)&tmask, (size_t)ceil_div(a.n, 32) * 4, st));
+  WalkSplit ws;
+  ws.mask = split_mask;
+  ws.before_set = split_before_set;
   if (a.defer_max < 16)
-    launch_update<16, kDeferred>(a, gd, t, tmask, touched_count, st);
+    launch_update<16, kDeferred>(a, gd, t, tmask, touched_count, st, split_mask ? &ws : nullptr);
   else
-    launch_update<256, kDeferred>(a, gd, t, tmask, touched_count, st);
+    launch_update<256, kDeferred>(a, gd, t, tmask, touched_count, st, split_mask ? &ws : nullptr);
   if (touched_ids) {
     // Ascending touched ids from the per-row bit mask (stable device select).
     size_t tb = 0;
@@ -1414,7 +1443,7 @@ __global__ void __launch_bounds__(kUpdThreads, GSS_RESTORE_MINB) restore_walk_ke
 }
 
 void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const int64_t* count_dev,
-                  const gss_sparse_grads* pending, float* out, cudaStream_t st) {
+                  const gss_sparse_grads* pending, float* out, cudaStream_t st, cudaEvent_t after_resolve) {
   require(ap != nullptr, "arena: null");
   const gss_arena& a = *ap;
   validate_arena(a);
@@ -1440,7 +1469,8 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
   // Host tier with a host-known row count: gather the rows into HBM staging over the link first,
   // then restore from the staged copy (see move_rows_kernel).
   const bool staged = host && vector_rows(a) && a.defer_max < 16 && !count_dev && host_staging();
-  const bool split = GSS_RESTORE_SPLIT && vector_rows(a) && a.defer_max < 16 && (!host || staged);
+  // (after_resolve: the caller orders a counter update after the resolve pass: split path always)
+  const bool split = GSS_RESTORE_SPLIT && vector_rows(a) && a.defer_max < 16 && (!host || staged || after_resolve);
   char* scr = arena_scratch(a, 1, pb_bytes + (split ? (size_t)std::max<int64_t>(cap, 1) * sizeof(int2) : 0), st);
   int32_t* pbstart = nullptr;
   if (pending && pd.ids) pbstart = build_index(a, pd, err_flag_for(a), reinterpret_cast<int32_t*>(scr), st);
@@ -1471,7 +1501,9 @@ void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const 
     const int rb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, 256), (int64_t)sms * 16));
     restore_resolve_kernel<<<rb, 256, 0, st>>>(arena_dev(a), ids, count, count_dev, pd, pbstart, res);
     GSS_LAUNCHED();
-    const int wb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kUpdThreads), (int64_t)sms * GSS_RESTORE_MINB));
+    if (after_resolve) GSS_CUDA(cudaEventRecord(after_resolve, st));
+    int wb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kUpdThreads), (int64_t)sms * GSS_RESTORE_MINB));
+    if (host) wb = std::min(wb, host_tier_blocks());
     restore_walk_kernel<16><<<wb, kUpdThreads, 0, st>>>(arena_dev(a), ids, count, count_dev, pd, res, pending ? 1 : 0,
                                                          *L, out);
   } else if (a.defer_max < 16) {

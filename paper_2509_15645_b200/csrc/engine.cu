@@ -32,9 +32,9 @@ void cull(const float* geo, int64_t n, int64_t stride, const gss_camera* cam, co
           uint32_t* mask, int32_t* ids, int64_t* count, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t cull_workspace_bytes(int64_t n);
 void adam_update(gss_arena* ap, const gss_sparse_grads* grads, int32_t* touched_ids, int64_t* touched_count,
-                 cudaStream_t st);
+                 cudaStream_t st, const uint32_t* split_mask = nullptr, cudaEvent_t split_before_set = nullptr);
 void adam_restore(const gss_arena* ap, const int32_t* ids, int64_t count, const int64_t* count_dev,
-                  const gss_sparse_grads* pending, float* out, cudaStream_t st);
+                  const gss_sparse_grads* pending, float* out, cudaStream_t st, cudaEvent_t after_resolve = nullptr);
 void rasterize_forward(gss_render_ctx* ctx, const gss_render_scene* scene, const gss_camera* cam,
                        const gss_viewport* vp, float* image, const float* gt, int64_t normalizer, float* d_img,
                        float* loss_dev, float* final_T_opt, int32_t* ncontrib_opt, int64_t* meta, cudaStream_t st);
@@ -100,6 +100,16 @@ __global__ void join_rows_kernel(const float* geo, const float* ng, int64_t n, f
 __global__ void iota_kernel(int32_t* ids, int64_t n) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) ids[i] = (int32_t)i;
+}
+
+// Sets (on) or clears the row bits of a sorted id list in a row bit mask.
+__global__ void mark_rows_kernel(const int32_t* ids, const int64_t* count, uint32_t* mask, int on) {
+  const int64_t V = *count;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < V; k += (int64_t)gridDim.x * blockDim.x) {
+    const int id = ids[k];
+    if (on) atomicOr(&mask[id >> 5], 1u << (id & 31));
+    else atomicAnd(&mask[id >> 5], ~(1u << (id & 31)));
+  }
 }
 
 // ---- split cameras: std::set_union of the two sorted cull lists (engine.hpp:270-272) and the
@@ -224,6 +234,11 @@ struct gss_engine {
   // streams / events
   cudaStream_t sD = nullptr, sH = nullptr, sC = nullptr;  // sC: host->device ground-truth copies of step()
   gssd::Ev ev_cull[3], ev_fp[2], ev_handoff[2], ev_lazy[2], ev_render[2], ev_gt, ev_gt_done[2];
+  // host tier, concurrent forwarding: the lazy update runs on its own stream sL beside the
+  // forwarding gather of the next iteration (disjoint rows; see stage_lazy)
+  cudaStream_t sL = nullptr;
+  gssd::Ev ev_resolved[2];        // fp(g)'s resolve pass (counters read) done
+  uint32_t* vis_mask = nullptr;   // bit per row: in the visible set of the iteration being forwarded
   bool gt_pending = false;  // render must wait for ev_gt (the step's ground truth in flight)
   struct TimeRec {
     int stage;
@@ -276,6 +291,16 @@ namespace {
 
 cudaStream_t S(gss_engine* e, bool host_tier) { return (e->cfg.pipelined && host_tier) ? e->sH : e->sD; }
 
+// The pinned host tier with the lazy update of g-1 beside the forwarding gather of g (both
+// link-bound; GSS_HOST_CONCURRENT=0 keeps them in the reference's serial order on stream H).
+bool host_concurrent(const gss_engine* e) {
+  static const bool on = [] {
+    const char* v = std::getenv("GSS_HOST_CONCURRENT");
+    return !(v && v[0] == '0');
+  }();
+  return e->ng_host && e->cfg.pipelined && e->sL != nullptr && on;
+}
+
 void ensure_rows(gss_engine* e, int64_t V) {
   if (V <= e->cap_rows) return;
   GSS_CUDA(cudaDeviceSynchronize());
@@ -317,7 +342,7 @@ void stage_begin(gss_engine* e, int st, cudaStream_t s, int g, uint64_t bytes = 
     stage_delay_kernel<<<1, 1, 0, s>>>(e->delays_ns[e->delay_next++ % e->delays_ns.size()]);
     GSS_LAUNCHED();
   }
-  gss_engine::TimeRec r{st, take_event(e), take_event(e), g, s == e->sH ? 1 : 0, bytes, touched_slot};
+  gss_engine::TimeRec r{st, take_event(e), take_event(e), g, (s == e->sH || s == e->sL) ? 1 : 0, bytes, touched_slot};
   GSS_CUDA(cudaEventRecord(r.a, s));
   e->pending_times.push_back(r);
 }
@@ -481,11 +506,14 @@ void stage_cull(gss_engine* e, int g, const gss_camera& cam, int col) {
 void stage_forward_params(gss_engine* e, int g) {
   const int p = g % 3, b = g % 2;
   cudaStream_t s = S(e, true);
+  const bool conc = host_concurrent(e);
   if (e->cfg.pipelined) {
     GSS_CUDA(cudaStreamWaitEvent(s, e->ev_cull[p].e, 0));
     if (g > e->seg_begin) GSS_CUDA(cudaStreamWaitEvent(s, e->ev_handoff[(g - 1) % 2].e, 0));
     // fwd[b] is free once render(g-2) consumed it
     GSS_CUDA(cudaStreamWaitEvent(s, e->ev_render[b].e, 0));
+    // concurrent host tier: the lazy updates run on sL; fp(g) reads the state after lazy(g-2)
+    if (conc) GSS_CUDA(cudaStreamWaitEvent(s, e->ev_lazy[b].e, 0));
   }
   // V is needed on the host to size staging buffers: wait for this plan's count.
   GSS_CUDA(cudaEventSynchronize(e->ev_cull[p].e));
@@ -508,24 +536,15 @@ void stage_forward_params(gss_engine* e, int g) {
     pg.col0 = 0;
   }
   // (the host tier takes the host-known count: its gather is staged through HBM in one pass)
-  adam_restore(&e->ng, e->ids[p], V, e->ng_host ? nullptr : e->count[p], pending ? &pg : nullptr, e->fwd[b], s);
+  adam_restore(&e->ng, e->ids[p], V, e->ng_host ? nullptr : e->count[p], pending ? &pg : nullptr, e->fwd[b], s,
+               conc ? e->ev_resolved[b].e : nullptr);
   e->fwd_iter[b] = g;
   stage_end(e, kFwd, s, b);
   GSS_CUDA(cudaEventRecord(e->ev_fp[b].e, s));
 }
 
 // engine.hpp:311-377.
-// In-place host tier run without overlap of its zero-copy passes and the render (GSS_HOST_SERIAL, A/B).
-bool host_serial(const gss_engine* e) {
-  static const int env = [] {
-    const char* v = std::getenv("GSS_HOST_SERIAL");
-    return v ? (v[0] == '1' ? 1 : 0) : -1;
-  }();
-  return e->ng_host && e->cfg.pipelined && env == 1;
-}
-
-void stage_render(gss_engine* e, int g, const gss_camera& cam, const float* gt_dev, float* loss_out,
-                  int after_lazy = -1) {
+void stage_render(gss_engine* e, int g, const gss_camera& cam, const float* gt_dev, float* loss_out) {
   const int p = g % 3, b = g % 2;
   cudaStream_t s = e->sD;
   require(e->fwd_iter[b] == g, "render: forwarded buffer is not for this iteration", GSS_ERR_INVARIANT);
@@ -559,7 +578,6 @@ void stage_render(gss_engine* e, int g, const gss_camera& cam, const float* gt_d
       GSS_CUDA(cudaStreamWaitEvent(s, e->ev_fp[b].e, 0));
       // grads[b] is free once lazy(g-2) consumed it
       GSS_CUDA(cudaStreamWaitEvent(s, e->ev_lazy[b].e, 0));
-      if (after_lazy >= 0) GSS_CUDA(cudaStreamWaitEvent(s, e->ev_lazy[after_lazy % 2].e, 0));
     }
     if (step_gt) GSS_CUDA(cudaStreamWaitEvent(s, e->ev_gt.e, 0));
   };
@@ -643,11 +661,23 @@ void stage_handoff(gss_engine* e, int g) {
 }
 
 // engine.hpp:420-430: lazy deferred update of the non-geometric tier with grads(g).
-void stage_lazy(gss_engine* e, int g) {
+// Concurrent host tier (next >= 0: fp(next) is in flight on stream H): on stream sL, after fp(next)'s
+// resolve pass has read the counters, pass 1 updates them; the walk of the touched rows outside
+// ids(next) runs beside fp(next)'s gather (disjoint rows), and the walk of the touched rows inside
+// ids(next) waits for that gather (it must read them before they are updated) — the reference's
+// order fp(next) -> lazy(g) for every row both touch, with the link's two directions busy at once.
+void stage_lazy(gss_engine* e, int g, int next = -1) {
   const int b = g % 2;
-  cudaStream_t s = S(e, true);
+  const bool conc = host_concurrent(e);
+  cudaStream_t s = conc ? e->sL : S(e, true);
   require(e->g_iter[b] == g, "lazy update: staging buffer holds a different iteration", GSS_ERR_INVARIANT);
   if (e->cfg.pipelined) GSS_CUDA(cudaStreamWaitEvent(s, e->ev_handoff[b].e, 0));
+  const int pn = next >= 0 ? next % 3 : -1;
+  if (conc && next >= 0) {
+    GSS_CUDA(cudaStreamWaitEvent(s, e->ev_resolved[next % 2].e, 0));
+    mark_rows_kernel<<<148 * 4, 256, 0, s>>>(e->ids[pn], e->count[pn], e->vis_mask, 1);
+    GSS_LAUNCHED();
+  }
   const int slot = e->timeline_on ? (e->touched_next++ % kTouchedRing) : -1;
   stage_begin(e, kLazy, s, g, 0, slot);
   const int p = e->g_plan[b];
@@ -659,7 +689,14 @@ void stage_lazy(gss_engine* e, int g) {
   gr.stride = kNgGradStride;
   gr.col0 = 0;
   if (e->ng_host) set_host_chunk_bytes(e->cfg.chunk_bytes);  // staged host-tier chunks (store.hpp:204-213)
-  adam_update(&e->ng, &gr, nullptr, slot >= 0 ? e->touched_ring + slot : nullptr, s);
+  if (conc && next >= 0) {
+    adam_update(&e->ng, &gr, nullptr, slot >= 0 ? e->touched_ring + slot : nullptr, s, e->vis_mask,
+                e->ev_fp[next % 2].e);
+    mark_rows_kernel<<<148 * 4, 256, 0, s>>>(e->ids[pn], e->count[pn], e->vis_mask, 0);
+    GSS_LAUNCHED();
+  } else {
+    adam_update(&e->ng, &gr, nullptr, slot >= 0 ? e->touched_ring + slot : nullptr, s);
+  }
   stage_end(e, kLazy, s, b);
   GSS_CUDA(cudaEventRecord(e->ev_lazy[b].e, s));
 }
@@ -673,15 +710,12 @@ void iteration(gss_engine* e, int g, const gss_camera& cam, const float* gt_dev,
   stage_cull(e, g, cam, col);
   stage_forward_params(e, g);
   const int owed = e->open_pending;
-  // lazy(g-1) runs on stream H after fp(g) in both modes (pipelined: overlapping render(g) on D).
-  // It is enqueued after render(g): a host-tier lazy pass reads its touched count back before
-  // chunking (staged_walk), and render(g) must already be queued on D by then. With the in-place
-  // host tier and host_serial, lazy(g-1) is enqueued first and render(g) waits for it: the host
-  // link's zero-copy traffic then never shares the SMs' memory path with the render.
-  const bool serial_host = host_serial(e);
-  if (serial_host && owed >= 0) stage_lazy(e, owed);
-  stage_render(e, g, cam, gt_dev, loss_out, serial_host && owed >= 0 ? owed : -1);
-  if (!serial_host && owed >= 0) stage_lazy(e, owed);
+  // lazy(g-1) runs on stream H after fp(g) in both modes (pipelined: overlapping render(g) on D;
+  // the concurrent host tier: on stream sL, partly beside fp(g)). It is enqueued after render(g): a
+  // staged host-tier pass reads its touched count back before chunking (staged_walk), and render(g)
+  // must already be queued on D by then.
+  stage_render(e, g, cam, gt_dev, loss_out);
+  if (owed >= 0) stage_lazy(e, owed, g);
   stage_geo_update(e, g);
   stage_handoff(e, g);
   e->open_pending = g;
@@ -696,6 +730,7 @@ void drain(gss_engine* e) {
   }
   GSS_CUDA(cudaStreamSynchronize(e->sD));
   GSS_CUDA(cudaStreamSynchronize(e->sH));
+  if (e->sL) GSS_CUDA(cudaStreamSynchronize(e->sL));
   collect_times(e);
 }
 
@@ -770,6 +805,7 @@ gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss
     const int mode = ev ? std::atoi(ev) : 1;
     GSS_CUDA(cudaStreamCreateWithPriority(&e->sD, cudaStreamNonBlocking, mode == 2 ? hi : lo));
     GSS_CUDA(cudaStreamCreateWithPriority(&e->sH, cudaStreamNonBlocking, mode == 1 ? hi : lo));
+    if (e->ng_host) GSS_CUDA(cudaStreamCreateWithPriority(&e->sL, cudaStreamNonBlocking, mode == 1 ? hi : lo));
   }
   GSS_CUDA(cudaStreamCreateWithFlags(&e->sC, cudaStreamNonBlocking));
   const size_t nn = (size_t)std::max<int64_t>(n, 1);
@@ -784,6 +820,10 @@ gss_engine* engine_create(int64_t n, const float* rows, int32_t ncams, const gss
   else
     e->nw = dmalloc<float>(nn * kNgStride);
   e->ncnt = dmalloc<uint8_t>(nn);
+  if (e->ng_host) {
+    e->vis_mask = dmalloc<uint32_t>((nn + 31) / 32);
+    GSS_CUDA(cudaMemsetAsync(e->vis_mask, 0, (nn + 31) / 32 * 4, e->sD));
+  }
   e->nm = e->nw + kNgSeg;
   e->nv = e->nw + 2 * kNgSeg;
   GSS_CUDA(cudaMemsetAsync(e->gm, 0, nn * kGeoDim * 4, e->sD));
@@ -903,6 +943,8 @@ void engine_destroy(gss_engine* e) {
   if (e->sD) cudaStreamDestroy(e->sD);
   if (e->sH) cudaStreamDestroy(e->sH);
   if (e->sC) cudaStreamDestroy(e->sC);
+  if (e->sL) cudaStreamDestroy(e->sL);
+  f(e->vis_mask);
   cudaGetLastError();
   delete e;
 }
@@ -1110,6 +1152,11 @@ void engine_densify(gss_engine* e, const gss_densify_config* dc, double extent, 
   cudaFree(e->ncnt);
   e->gw = gw2; e->gm = gm2; e->gv = gv2; e->gcnt = gc2;
   e->nw = nw2; e->nm = nw2 + kNgSeg; e->nv = nw2 + 2 * kNgSeg; e->ncnt = nc2;
+  if (e->ng_host) {  // the concurrent host tier's row mask follows the population
+    cudaFree(e->vis_mask);
+    e->vis_mask = dmalloc<uint32_t>((nn + 31) / 32);
+    GSS_CUDA(cudaMemset(e->vis_mask, 0, (nn + 31) / 32 * 4));
+  }
   e->n = n2;
   e->geo.w = gw2; e->geo.m = gm2; e->geo.v = gv2; e->geo.counter = gc2; e->geo.n = n2;
   e->ng.w = e->nw; e->ng.m = e->nm; e->ng.v = e->nv; e->ng.counter = nc2; e->ng.n = n2;
