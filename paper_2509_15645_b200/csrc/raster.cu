@@ -562,8 +562,12 @@ __device__ __forceinline__ float div_rcp_rn(float n, float d, float rd) {
 // errs by < 2^-21 (a + c + |b|) |d|^2. The conditions below bound both ends with a 2x margin
 // (NaN or inf fields fail every comparison).
 #if GSS_FWD_SAFE
+// Certified records also have alpha_base <= 0.999 (so ab * weight, weight <= 1, never reaches the
+// 0.999 clamp) and, by the numerator bound, a quotient >= +0 (max(q, 0) is the identity): the
+// certified pixel path drops the range test, the clamp and the max.
 __device__ __forceinline__ bool fwd_quotient_safe(const SplatRec& r, float rd) {
   if (rd == 0.0f) return false;
+  if (!(r.ab <= 0.999f)) return false;
   const float a = r.a, c = r.c, ab = fabsf(r.b), det = r.det, tr = a + c;
   if (!(a > 0.0f && c > 0.0f)) return false;
   if (!(det >= 0x1p-19f * tr * (tr + ab))) return false;  // cancellation < half the exact value
@@ -716,10 +720,10 @@ __global__ void GSS_FWD_BOUNDS forward_kernel(const SplatRec* __restrict__ recs,
               if (slow) quo = __fdiv_rn(num, q2.w);
             }
           }
-          const float xe = -0.5f * max0(quo);
+          const float xe = -0.5f * (kChecked ? max0(quo) : quo);
           const float wgt = gss_expf_nonpos_sel(xe, ek);
           const float raw = q1.y * wgt;
-          const float alpha = raw > 0.999f ? 0.999f : raw;
+          const float alpha = (kChecked && raw > 0.999f) ? 0.999f : raw;
           if (ev) {
             c0[h] += q1.z * alpha * T[h];
             c1[h] += q1.w * alpha * T[h];
