@@ -687,7 +687,7 @@ constexpr int kRestoreChunk = kUpdThreads;
 #endif
 constexpr int kSeg = 2048;
 template <int K>
-__global__ void __launch_bounds__(kUpdThreads, GSS_RESTORE_MINB) restore_kernel(ArenaDev a, const int32_t* ids, int64_t count,
+__global__ void __launch_bounds__(kUpdThreads, 3) restore_kernel(ArenaDev a, const int32_t* ids, int64_t count,
                                                               const int64_t* count_dev, GradsDev pend,
                                                               const int32_t* pbstart, int has_pending,
                                                               const __grid_constant__ LutArgs<K> L, float* out,

@@ -867,6 +867,9 @@ __global__ void loss_final_kernel(const double* partials, int n, float inv, floa
 // Reverse sweep state of one pixel (render.hpp:542-589). The suffix colour enters the sweep only
 // through its dot product with the pixel's (constant) colour gradient, so the state keeps that
 // scalar S = suf . g (suf_c += rgb_c * w  =>  S += (rgb . g) * w).
+#ifndef GSS_BWD_PPT
+#define GSS_BWD_PPT 4
+#endif
 struct PixB {
   float cx, cy, T, g0, g1, g2, S;
   int x, y, L;
@@ -908,13 +911,46 @@ constexpr float kClampGuard = 0.9989f;
 // arithmetic whenever the fast alpha is within 1e-4 of the threshold, so both passes always take the
 // same branch. Predicated: a lane whose pixel is outside the record's box (or past its last index)
 // adds exact zeros and keeps its state.
-template <bool CLAMP>
-__device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k, bool xin, int jpos, PixB& p,
-                                            float v[9]) {
+//
+// GSS_BWD_XFACT: a lane's 4 pixels share their column, so dx is per (record, lane): the quadratic
+// form is evaluated as q = dy * (ic*dy + ibm2*dx) + ia*dx^2 (2 FMAs per pixel on the lane's
+// per-record ax = ia*dx^2, bx = ibm2*dx) and the moments with a dx factor are formed once per record
+// from the lane's sums (sum t*dx^2 = dx^2 * sum t, sum t*dx = dx * sum t, sum t*dx*dy = dx * sum t*dy):
+// per pixel only sum t, sum t*dy, sum t*dy^2 are swept (bwd_finish_lane completes v[4], v[6], v[7]).
+#ifndef GSS_BWD_XFACT
+#define GSS_BWD_XFACT 1
+#endif
+// GSS_BWD_DYINC: the lane's pixel rows are cy0 + 2h, so dy of pixel h is dy0 + 2h (one add per pixel
+// instead of re-deriving cy from the row index under register pressure).
+#ifndef GSS_BWD_DYINC
+#define GSS_BWD_DYINC 0
+#endif
+struct BwdLane {
+  float dx, ax, bx, dy0;
+};
+__device__ __forceinline__ BwdLane bwd_lane(const SplatRec& r, const BwdConic& k, const PixB& p0) {
+  const float dx = p0.cx - r.mx;
+  return BwdLane{dx, k.ia * (dx * dx), k.ibm2 * dx, p0.cy - r.my};
+}
+__device__ __forceinline__ void bwd_finish_lane(const BwdLane& l, float v[9]) {
+#if GSS_BWD_XFACT
+  v[4] = (l.dx * l.dx) * v[3];
+  v[6] = l.dx * v[8];
+  v[7] = l.dx * v[3];
+#endif
+}
+template <bool CLAMP, int H>
+__device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k, const BwdLane& l, bool xin,
+                                            int jpos, PixB& p, float v[9]) {
   const bool ok = xin & (jpos < p.L) & (p.y >= r.by0) & (p.y < r.by1);
+#if GSS_BWD_XFACT
+  const float dx = l.dx, dy = (GSS_BWD_DYINC && H > 0) ? l.dy0 + (float)(2 * H) : (H == 0 ? l.dy0 : p.cy - r.my);
+  float q = __fmaf_rn(dy, __fmaf_rn(k.ic, dy, l.bx), l.ax);
+#else
   const float dx = p.cx - r.mx, dy = p.cy - r.my;
   const float dxx = dx * dx, dyy = dy * dy, dxy = dx * dy;
   float q = __fmaf_rn(k.ia, dxx, __fmaf_rn(k.ic, dyy, k.ibm2 * dxy));
+#endif
   q = (q < 0.0f || !ok) ? 0.0f : q;  // an idle lane evaluates at q = 0: every term stays finite
   const float weight = ex2_fast(-0.72134752f * q);  // exp(-q/2)
   bool clamped = false;
@@ -942,12 +978,32 @@ __device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k
   p.T = Tb;
   const float t = (ok && !clamped) ? weight * d_alpha : 0.0f;  // render.hpp:572-586 only when not clamped
   v[3] += t;
+#if GSS_BWD_XFACT
+  const float tdy = t * dy;
+  v[8] += tdy;
+  v[5] = __fmaf_rn(tdy, dy, v[5]);
+  (void)dx;
+#else
   v[4] = __fmaf_rn(t, dxx, v[4]);
   v[5] = __fmaf_rn(t, dyy, v[5]);
   v[6] = __fmaf_rn(t, dxy, v[6]);
   v[7] = __fmaf_rn(t, dx, v[7]);
   v[8] = __fmaf_rn(t, dy, v[8]);
+#endif
   return ok;
+}
+
+// The lane's pixels of one record, unrolled with the pixel index as a template argument (row h of
+// the lane is cy0 + 2h); returns how many contributed.
+template <bool CLAMP, int H = 0>
+__device__ __forceinline__ int bwd_pixels(const SplatRec& r, const BwdConic& k, const BwdLane& l, bool xin, int jpos,
+                                          PixB* px, float v[9]) {
+  if constexpr (H < GSS_BWD_PPT) {
+    const int u = bwd_contrib<CLAMP, H>(r, k, l, xin, jpos, px[H], v) ? 1 : 0;
+    return u + bwd_pixels<CLAMP, H + 1>(r, k, l, xin, jpos, px, v);
+  } else {
+    return 0;
+  }
 }
 
 // The 9 SlotAcc terms (rgb3, mean2d2, cov3, alpha_base; render.hpp:538) of one record from its 9
@@ -1014,9 +1070,6 @@ __device__ __forceinline__ float warp_reduce_scatter9(const float v[9], int lane
 // box intersects the band and sweep position < the band's largest last-contribution index) and
 // walks only those. One partial SlotAcc per (splat, tile) instance, fixed-order sums (no float
 // atomics, deterministic). partial layout: [instance][9] = rgb3, m2d2, cov3, ab.
-#ifndef GSS_BWD_PPT
-#define GSS_BWD_PPT 4
-#endif
 constexpr int kBwdPPT = GSS_BWD_PPT;              // pixels per thread
 constexpr int kBwdThreads = kTilePix / kBwdPPT;
 constexpr int kBwdWarps = kBwdThreads / 32;
@@ -1135,31 +1188,20 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
         const SplatRec r = sh[jj];
         const BwdConic k = shk[jj];
         const bool xin = (px[0].x >= r.bx0) & (px[0].x < r.bx1);
+        const BwdLane bl = bwd_lane(r, k, px[0]);
         float v[kNv];
 #pragma unroll
         for (int i = 0; i < kNv; ++i) v[i] = 0.0f;
 #if GSS_RASTER_STATS
         ++st_walk;
 #endif
-        if (r.ab > kClampGuard) {
-#pragma unroll
-          for (int q = 0; q < kBwdPPT; ++q) {
-            const bool u = bwd_contrib<true>(r, k, xin, bstart + jj, px[q], v);
+        const int nuse = r.ab > kClampGuard ? bwd_pixels<true>(r, k, bl, xin, bstart + jj, px, v)
+                                            : bwd_pixels<false>(r, k, bl, xin, bstart + jj, px, v);
 #if GSS_RASTER_STATS
-            st_use += u ? 1 : 0;
+        st_use += nuse;
 #endif
-            (void)u;
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < kBwdPPT; ++q) {
-            const bool u = bwd_contrib<false>(r, k, xin, bstart + jj, px[q], v);
-#if GSS_RASTER_STATS
-            st_use += u ? 1 : 0;
-#endif
-            (void)u;
-          }
-        }
+        (void)nuse;
+        bwd_finish_lane(bl, v);
         // A record no lane contributed to reduces exact zeros: the same partial without a vote.
         const float tot = warp_reduce_scatter9(v, lane);
         if ((lane & 1) == 0 && vidx >= 0) red[jj][warp][vidx] = tot;

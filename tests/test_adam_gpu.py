@@ -269,3 +269,31 @@ def test_host_tier_staged_variant_bitwise():
                         f"{__file__}::test_host_tier_arena_passes_bitwise"], env=env, capture_output=True, text=True,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("defer_max,n", [(1, 1), (6, 31), (15, 4099), (15, 40000)])
+def test_engine_layout_gather_with_pending_bitwise(ref, defer_max, n):
+    """The engine's forwarding gather layout: row-interleaved arena + 52-float pending gradient rows
+    (restore_resolve_kernel + restore_walk_kernel): restored rows bitwise equal to the reference's
+    restore_view with pending grads, at sizes around the 32-row batch boundary; padding columns of
+    the gradient rows (NaN here) never read as data."""
+    rng = np.random.default_rng(11 + defer_max + n)
+    dim = 49
+    ra, ga = make_pair(n, dim, GROUPS49, defer_max, rng, interleaved=True)
+    for _ in range(defer_max + 3):
+        ids = np.nonzero(rng.uniform(size=n) < 0.3)[0].astype(np.int32)
+        rows = rng.normal(size=(ids.size, 52)).astype(np.float32)
+        rows[:, 49:] = np.nan
+        ra.deferred(ids, rows, 52)
+        G.deferred_update(ga, G.SparseGrads(torch.from_numpy(ids).cuda(), torch.from_numpy(rows).cuda(), 52))
+    assert_same(ra, ga)
+    pids = np.nonzero(rng.uniform(size=n) < 0.4)[0].astype(np.int32)
+    prow = rng.normal(size=(pids.size, 52)).astype(np.float32)
+    prow[:, 49:] = np.nan
+    q = np.nonzero(rng.uniform(size=n) < 0.6)[0].astype(np.int32)
+    pend = G.SparseGrads(torch.from_numpy(pids).cuda(), torch.from_numpy(prow).cuda(), 52)
+    got = G.restore_view(ga, torch.from_numpy(q).cuda(), pend).cpu().numpy()
+    assert np.array_equal(bits(got), bits(ra.restore(q, (pids, prow, 52, 0))))
+    got0 = G.restore_view(ga, torch.from_numpy(q).cuda(), None).cpu().numpy()
+    assert np.array_equal(bits(got0), bits(ra.restore(q)))
+    assert_same(ra, ga)
