@@ -923,7 +923,10 @@ constexpr float kClampGuard = 0.9989f;
 // GSS_BWD_DYINC: the lane's pixel rows are cy0 + 2h, so dy of pixel h is dy0 + 2h (one add per pixel
 // instead of re-deriving cy from the row index under register pressure).
 #ifndef GSS_BWD_DYINC
-#define GSS_BWD_DYINC 0
+#define GSS_BWD_DYINC 1
+#endif
+#ifndef GSS_BWD_WSEL
+#define GSS_BWD_WSEL 1
 #endif
 struct BwdLane {
   float dx, ax, bx, dy0;
@@ -950,6 +953,40 @@ __device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k
   const float dx = p.cx - r.mx, dy = p.cy - r.my;
   const float dxx = dx * dx, dyy = dy * dy, dxy = dx * dy;
   float q = __fmaf_rn(k.ia, dxx, __fmaf_rn(k.ic, dyy, k.ibm2 * dxy));
+#endif
+#if GSS_BWD_WSEL
+  if constexpr (!CLAMP) {
+    // One select per pixel: an idle lane takes weight = +0, so alpha = +0, rcp(1 - 0) = 1 exactly
+    // (MUFU.RCP(1) == 1, tools/mufucheck.cu), Tb = T, S unchanged and t = +-0 — the partials of
+    // the three-select form below, bit for bit (x + -0 == x).
+    const float weight = ok ? ex2_fast(-0.72134752f * fmaxf(q, 0.0f)) : 0.0f;
+    const float alpha = r.ab * weight;
+    const float inv1m = rcp_fast(1.0f - alpha);
+    const float Tb = p.T * inv1m;
+    const float w_rgb = alpha * Tb;
+    v[0] = __fmaf_rn(w_rgb, p.g0, v[0]);
+    v[1] = __fmaf_rn(w_rgb, p.g1, v[1]);
+    v[2] = __fmaf_rn(w_rgb, p.g2, v[2]);
+    const float dot_c = __fmaf_rn(r.r, p.g0, __fmaf_rn(r.g, p.g1, r.bl * p.g2));
+    const float d_alpha = __fmaf_rn(Tb, dot_c, -p.S * inv1m);
+    p.S = __fmaf_rn(dot_c, w_rgb, p.S);
+    p.T = Tb;
+    const float t = weight * d_alpha;
+    v[3] += t;
+#if GSS_BWD_XFACT
+    const float tdy = t * dy;
+    v[8] += tdy;
+    v[5] = __fmaf_rn(tdy, dy, v[5]);
+    (void)dx;
+#else
+    v[4] = __fmaf_rn(t, dxx, v[4]);
+    v[5] = __fmaf_rn(t, dyy, v[5]);
+    v[6] = __fmaf_rn(t, dxy, v[6]);
+    v[7] = __fmaf_rn(t, dx, v[7]);
+    v[8] = __fmaf_rn(t, dy, v[8]);
+#endif
+    return ok;
+  }
 #endif
   q = (q < 0.0f || !ok) ? 0.0f : q;  // an idle lane evaluates at q = 0: every term stays finite
   const float weight = ex2_fast(-0.72134752f * q);  // exp(-q/2)
