@@ -1332,6 +1332,91 @@ __global__ void __launch_bounds__(kSumWarps * 32) slot_sum_depth_kernel(int64_t 
   }
 }
 
+// Per-slot sums in depth order as a warp-wide segmented scan (GSS_SUM_SEG): the warp's 32 slots own
+// one contiguous instance span, which the warp walks 32 instances at a time (lane = instance, the 9
+// values loaded coalesced); a segmented inclusive scan (heads = the slots' first instances) sums
+// each slot's piece of the chunk in a fixed tree order, and the piece's last lane adds it to the
+// slot's accumulator in SMEM (pieces in chunk order). Every lane does useful work whatever the
+// slots' instance counts — the lane-per-slot loop above waits for the warp's largest splat.
+// Deterministic (fixed order); the order differs from the lane-per-slot loop's by rounding only.
+#ifndef GSS_SUM_SEG
+#define GSS_SUM_SEG 1
+#endif
+#ifndef GSS_SUM_U
+#define GSS_SUM_U 4
+#endif
+__global__ void __launch_bounds__(kSumWarps * 32) slot_sum_seg_kernel(int64_t V, const int32_t* __restrict__ offsets,
+                                                                    const uint64_t* __restrict__ pay,
+                                                                    const float* __restrict__ partials, float* sums) {
+  __shared__ float acc[kSumWarps][32][9];
+  __shared__ int8_t owner_at[kSumWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t i0 = ((int64_t)blockIdx.x * kSumWarps + warp) * 32;
+  if (i0 >= V) return;
+  const int64_t i = i0 + lane;
+  const bool valid = i < V;
+  const int64_t iend = i0 + 32 < V ? i0 + 32 : V;
+  const int32_t o0 = valid ? offsets[i] : offsets[iend];
+  const int32_t o1 = valid ? offsets[i + 1] : o0;
+  const int32_t s0 = __shfl_sync(0xffffffffu, o0, 0);
+  const int32_t s1 = offsets[iend];
+  float* A = acc[warp][lane];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) A[c] = 0.0f;
+  __syncwarp();
+  // GSS_SUM_U chunks' loads in flight before their scans: a warp whose slots include a splat with
+  // thousands of tile instances walks a long span, and that warp's serial chain of load latencies
+  // is the kernel's tail.
+  for (int32_t cg = s0; cg < s1; cg += 32 * GSS_SUM_U) {
+    float xs[GSS_SUM_U][9];
+#pragma unroll
+    for (int u = 0; u < GSS_SUM_U; ++u) {
+      const int32_t j = cg + 32 * u + lane;
+      const bool in = j < s1;
+      const float* src = partials + (int64_t)j * 9;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) xs[u][c] = in ? __ldg(src + c) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < GSS_SUM_U; ++u) {
+    const int32_t cb = cg + 32 * u;
+    if (cb >= s1) break;
+    const bool head = valid && o1 > o0 && o0 >= cb && o0 < cb + 32;
+    if (head) owner_at[warp][o0 - cb] = (int8_t)lane;
+    const unsigned hmask = __reduce_or_sync(0xffffffffu, head ? 1u << (o0 - cb) : 0u);
+    const unsigned open = __ballot_sync(0xffffffffu, valid && o0 <= cb && cb < o1);  // the slot open at cb
+    __syncwarp();
+    const int32_t j = cb + lane;
+    const bool in = j < s1;
+    float* x = xs[u];
+    const unsigned below = hmask & (0xffffffffu >> (31 - lane));  // heads at lanes 0..lane
+    const int hp = below ? 31 - __clz(below) : -1;                // -1: the piece continues a slot
+    const int lim = hp >= 0 ? lane - hp : lane;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+      for (int c = 0; c < 9; ++c) {
+        const float y = __shfl_up_sync(0xffffffffu, x[c], d);
+        if (d <= lim) x[c] += y;
+      }
+    }
+    const bool end = in && (lane == 31 || j + 1 == s1 || ((hmask >> (lane + 1)) & 1u));
+    if (end) {
+      const int t = hp >= 0 ? owner_at[warp][hp] : __ffs(open) - 1;
+      float* T = acc[warp][t];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) T[c] += x[c];
+    }
+    __syncwarp();
+    }
+  }
+  if (valid) {
+    const int64_t k = (int64_t)(uint32_t)pay[i];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) sums[k * 9 + c] = A[c];
+  }
+}
+
 // render.hpp:600-638 + project_geo_backward (render.hpp:152-237), per slot.
 // Per-slot sums of the backward's instance partials (CSR by slot: instances of slot k are
 // [offsets[k], offsets[k+1])), in a fixed order: each lane sums its own slot's first kHead
@@ -1860,8 +1945,12 @@ void per_slot_sums(gss_render_ctx* ctx, const float* d_img, float* sums, cudaStr
   if (GSS_SUM_DEPTH && ctx->pay_sorted) {
     // slots never binned (V_bin .. V in depth order: depth key 0xffffffff) have no instances: their
     // ranges are empty and their sums are written as zeros like every other slot's
-    slot_sum_depth_kernel<<<(unsigned)ceil_div(V, kSumWarps * 32), kSumWarps * 32, 0, st>>>(
-        V, static_cast<const int32_t*>(ctx->offsets.p), ctx->pay_sorted, partials, sums);
+    if (GSS_SUM_SEG)
+      slot_sum_seg_kernel<<<(unsigned)ceil_div(V, kSumWarps * 32), kSumWarps * 32, 0, st>>>(
+          V, static_cast<const int32_t*>(ctx->offsets.p), ctx->pay_sorted, partials, sums);
+    else
+      slot_sum_depth_kernel<<<(unsigned)ceil_div(V, kSumWarps * 32), kSumWarps * 32, 0, st>>>(
+          V, static_cast<const int32_t*>(ctx->offsets.p), ctx->pay_sorted, partials, sums);
   } else {
     slot_sum_kernel<<<(unsigned)ceil_div(V, kSumThreads), kSumThreads, 0, st>>>(V, soff, nts, partials, sums);
   }

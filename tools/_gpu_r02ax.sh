@@ -1,0 +1,13 @@
+# slot sums as a warp-wide segmented scan (GSS_SUM_SEG): parity + same-box A/B vs the lane-per-slot loop
+set -x
+mkdir -p gpurun_out
+B=paper_2509_15645_b200/_build
+timeout 1500 python -m pytest tests/test_raster_gpu.py tests/test_imgpar_gpu.py tests/test_engine_gpu.py "tests/test_scale_parity_gpu.py::test_c4_strip_forward_backward_vs_reference" "tests/test_scale_parity_gpu.py::test_c2_view_forward_backward_vs_reference" "tests/test_scale_parity_gpu.py::test_c2_engine_three_iterations_vs_reference" -x -q > gpurun_out/pytest_ax.txt 2>&1; tail -n 3 gpurun_out/pytest_ax.txt
+for i in 1 2; do
+  for v in default seg0; do
+    if [ $v = default ]; then L=; else L=$B/var_$v/libgss_b200.so; fi
+    GSS_LIB=$L timeout 900 python bench.py --steps 16 --warmup 8 --no-cpu-baseline --no-probe --no-host-offload > gpurun_out/bench_ax_$v$i.json 2>/dev/null
+    python -c "import json;d=json.loads(open('gpurun_out/bench_ax_$v$i.json').read().strip().splitlines()[-1]);print('$v',round(d['value'],3),{k:round(v,3) for k,v in d['render_kernels']['phases_ms_per_step'].items()})" >> gpurun_out/ab_ax.txt
+  done
+done
+cat gpurun_out/ab_ax.txt
