@@ -877,9 +877,18 @@ struct PixB {
 
 // Per-splat constants of the backward sweep, computed once per batch: the conic (inverse 2D
 // covariance) so the per-pixel exponent needs no division.
+// GSS_BWD_KFOLD: the exp's -log2(e)/2 factor folded into a scaled copy of the conic (sia, sibm2,
+// sic), so the sweep's quadratic form comes out as the ex2 argument (one multiply less per pixel).
+#ifndef GSS_BWD_KFOLD
+#define GSS_BWD_KFOLD 0
+#endif
+constexpr float kExpHalf = -0.72134752f;  // -log2(e) / 2: exp(-q/2) = ex2(kExpHalf * q)
 struct BwdConic {
   float ia, ibm2, ic;  // c/det, -2*b/det, a/det
   float nh;            // -0.5/det
+#if GSS_BWD_KFOLD
+  float sia, sibm2, sic, pad;  // kExpHalf * (ia, ibm2, ic)
+#endif
 };
 
 __device__ __forceinline__ float ex2_fast(float x) {
@@ -933,7 +942,11 @@ struct BwdLane {
 };
 __device__ __forceinline__ BwdLane bwd_lane(const SplatRec& r, const BwdConic& k, const PixB& p0) {
   const float dx = p0.cx - r.mx;
+#if GSS_BWD_KFOLD
+  return BwdLane{dx, k.sia * (dx * dx), k.sibm2 * dx, p0.cy - r.my};
+#else
   return BwdLane{dx, k.ia * (dx * dx), k.ibm2 * dx, p0.cy - r.my};
+#endif
 }
 __device__ __forceinline__ void bwd_finish_lane(const BwdLane& l, float v[9]) {
 #if GSS_BWD_XFACT
@@ -948,7 +961,11 @@ __device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k
   const bool ok = xin & (jpos < p.L) & (p.y >= r.by0) & (p.y < r.by1);
 #if GSS_BWD_XFACT
   const float dx = l.dx, dy = (GSS_BWD_DYINC && H > 0) ? l.dy0 + (float)(2 * H) : (H == 0 ? l.dy0 : p.cy - r.my);
+#if GSS_BWD_KFOLD
+  float q = __fmaf_rn(dy, __fmaf_rn(k.sic, dy, l.bx), l.ax);  // kExpHalf * the quadratic form
+#else
   float q = __fmaf_rn(dy, __fmaf_rn(k.ic, dy, l.bx), l.ax);
+#endif
 #else
   const float dx = p.cx - r.mx, dy = p.cy - r.my;
   const float dxx = dx * dx, dyy = dy * dy, dxy = dx * dy;
@@ -959,7 +976,11 @@ __device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k
     // One select per pixel: an idle lane takes weight = +0, so alpha = +0, rcp(1 - 0) = 1 exactly
     // (MUFU.RCP(1) == 1, tools/mufucheck.cu), Tb = T, S unchanged and t = +-0 — the partials of
     // the three-select form below, bit for bit (x + -0 == x).
-    const float weight = ok ? ex2_fast(-0.72134752f * fmaxf(q, 0.0f)) : 0.0f;
+#if GSS_BWD_XFACT && GSS_BWD_KFOLD
+    const float weight = ok ? ex2_fast(fminf(q, 0.0f)) : 0.0f;
+#else
+    const float weight = ok ? ex2_fast(kExpHalf * fmaxf(q, 0.0f)) : 0.0f;
+#endif
     const float alpha = r.ab * weight;
     const float inv1m = rcp_fast(1.0f - alpha);
     const float Tb = p.T * inv1m;
@@ -988,8 +1009,13 @@ __device__ __forceinline__ bool bwd_contrib(const SplatRec& r, const BwdConic& k
     return ok;
   }
 #endif
+#if GSS_BWD_XFACT && GSS_BWD_KFOLD
+  q = (q > 0.0f || !ok) ? 0.0f : q;  // scaled form: an idle lane evaluates at 0
+  const float weight = ex2_fast(q);  // exp(-q/2)
+#else
   q = (q < 0.0f || !ok) ? 0.0f : q;  // an idle lane evaluates at q = 0: every term stays finite
-  const float weight = ex2_fast(-0.72134752f * q);  // exp(-q/2)
+  const float weight = ex2_fast(kExpHalf * q);  // exp(-q/2)
+#endif
   bool clamped = false;
   float alpha;
   if (CLAMP) {
@@ -1174,7 +1200,14 @@ __global__ void GSS_BWD_BOUNDS backward_kernel(const SplatRec* __restrict__ recs
       load_rec(&sh[j], recs, vals[rg.x + bstart + j]);
       const SplatRec& r = sh[j];
       const float inv = 1.0f / r.det;  // det > 0 for every binned splat
+#if GSS_BWD_KFOLD
+      {
+        const float ia = r.c * inv, ibm2 = -2.0f * (r.b * inv), ic = r.a * inv;
+        shk[j] = BwdConic{ia, ibm2, ic, -0.5f * inv, kExpHalf * ia, kExpHalf * ibm2, kExpHalf * ic, 0.0f};
+      }
+#else
       shk[j] = BwdConic{r.c * inv, -2.0f * (r.b * inv), r.a * inv, -0.5f * inv};
+#endif
       int tx0, ty0, ntx, nty;
       tile_box(r, w, tx0, ty0, ntx, nty);
       sinst[j] = r.off + (ty - ty0) * ntx + (tx - tx0);
