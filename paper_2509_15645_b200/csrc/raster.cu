@@ -880,7 +880,7 @@ struct PixB {
 // GSS_BWD_KFOLD: the exp's -log2(e)/2 factor folded into a scaled copy of the conic (sia, sibm2,
 // sic), so the sweep's quadratic form comes out as the ex2 argument (one multiply less per pixel).
 #ifndef GSS_BWD_KFOLD
-#define GSS_BWD_KFOLD 0
+#define GSS_BWD_KFOLD 1
 #endif
 constexpr float kExpHalf = -0.72134752f;  // -log2(e) / 2: exp(-q/2) = ex2(kExpHalf * q)
 struct BwdConic {
