@@ -915,8 +915,8 @@ def main():
 # the fraction of the lane-pixel slots it issues that are useful contributions (a library built
 # with GSS_RASTER_STATS=1, tools/raster_work.py).
 RASTER_PROFILE = {
-    "sweep": {"kernel": "backward_kernel", "issue_busy": 0.865, "useful_of_offered": 0.534,
-              "dram_bytes_per_launch": 1.963807e9 + 1.389040e9,
+    "sweep": {"kernel": "backward_kernel", "issue_busy": 0.863, "useful_of_offered": 0.534,
+              "dram_bytes_per_launch": 1.961671e9 + 1.389565e9,
               "source": "profiles/r02_ncu_sweep_c4_final.txt (Issue Slots Busy, dram__bytes of camera 0), "
                         "profiles/r02_raster_work_c4.json (bwd_useful_of_offered)"},
     "composite": {"kernel": "forward_kernel", "issue_busy": 0.856, "useful_of_offered": 0.655,
